@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark of the DynaMoE MoE-layer hot path on B200 (driver contract).
+
+A step = one forward + backward of the MoE layer (gate GEMM, softmax/top-k, capacity-bounded
+dispatch, expert FFN grouped GEMMs, combine, and every backward incl. weight gradients) over
+one batch of synthetic tokens.  Workload: BASELINE configs[2] (c3) per GPU -- 64 experts,
+top-1, d_model 1024, d_ff 4096, 65,536 tokens per GPU, bf16, capacity factor 1.0 -- with
+experts sharded over the N ranks (weak scaling).  Inputs (x 134 MB, expert weights 1 GB)
+exceed the 126 MB L2, so no explicit flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer fwd+bwd tokens/sec at 1/2/4/8 B200; dispatch/combine HBM GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--tokens", type=int, default=0, help="override tokens per rank")
+    ap.add_argument("--alpha", type=float, default=None, help="static capacity factor")
+    ap.add_argument("--cached", action="store_true", help="sample-assignment caching (c5)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1024)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return dict(hbm=j["hbm_gbs"], bf16=j["bf16_tflops"], bf16_sus=j["bf16_tflops_sustained"],
+                    sm_max_mhz=j.get("sm_max_mhz", 1965.0), src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, sm_max_mhz=1965.0, src="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        if not sm:
+            return None
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4)
+                          if r[3 + i].lower().startswith("active")})
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local) if torch.cuda.is_available() else None
+        backend = "nccl" if torch.cuda.is_available() and args.impl == "ours" else "gloo"
+        dist.init_process_group(backend=backend)
+        pg = dist
+    return ws, rank, local, pg
+
+
+# ------------------------------------------------------------------------------------------
+# algorithmic work per kernel: bytes or FLOPs per launch
+# ------------------------------------------------------------------------------------------
+def kernel_work(cfg, T, A, s):
+    n, k, d, f, do = cfg.n_experts, cfg.top_k, cfg.d_model, cfg.d_ff, cfg.d_out
+    gf = 2.0 * A * d * f  # one expert GEMM (fwd or dgrad or wgrad) = 2*A*d*f FLOPs
+    return {
+        # name: (kind, amount)   kind "flop" (tensor/alu) or "byte" (hbm)
+        "gate_topk": ("byte", T * d * s + n * d * s + 4 * T * n + 8 * T * k),
+        "route_hist": ("byte", 4 * T * k),
+        "route_scan": ("byte", 8 * (T // 128 + 1) * n),
+        "dispatch": ("byte", (T + A) * d * s + 8 * T * k + 4 * A),
+        "zero_pad": ("byte", 0),
+        "ffn_gemm1": ("flop", gf), "ffn_gemm2": ("flop", gf),
+        "combine_fwd": ("byte", (A + T) * do * s + 8 * T * k),
+        "combine_bwd": ("byte", (T + 2 * A) * do * s + 12 * T * k + 8 * T * n),
+        "wgrad_w2": ("flop", gf), "dgrad_dA": ("flop", gf),
+        "wgrad_w1": ("flop", gf), "dgrad_dX": ("flop", gf),
+        "bias_grad": ("byte", A * (f + do) * s),
+        "gate_dx": ("byte", (A + T) * d * s + 4 * T * n + 8 * T * k),
+        "gate_dw": ("byte", T * d * s + 4 * T * n),
+    }
+
+
+def run_ours(args):
+    import torch
+    from paper_2205_01848_b200 import MoELayer
+    from synth import get_config, make_dy, make_layer
+
+    ws, rank, local, dist = dist_setup(args)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = get_config(args.config)
+    T = args.tokens or (cfg.tokens if cfg.scaling == "weak" or args.config in ("c3", "c5")
+                        else cfg.tokens // ws)
+    alpha = args.alpha if args.alpha is not None else cfg.alpha
+    n, k, d, f, do = cfg.n_experts, cfg.top_k, cfg.d_model, cfg.d_ff, cfg.d_out
+    s = 2 if cfg.dtype == "bf16" else 4
+    replicas = ws > 1  # expert parallelism not yet wired: independent replicas, labelled
+    # inputs resident in HBM (generated on the device from the seeded recipe)
+    g = make_layer(n, d, f, do, T, cfg.dtype, "uniform", device=dev, seed_offset=rank)
+    dy = make_dy(T, do, cfg.dtype, device=dev, seed_offset=rank)
+    layer = MoELayer(n, k, d, f, do, T, cfg.dtype, cfg.renormalize, device=dev)
+    layer.set_capacity_factors([alpha] * n, T)
+    tdt = layer.tdtype
+    grads = dict(dx=torch.empty(T, d, dtype=tdt, device=dev),
+                 dw_gate=torch.empty(n, d, dtype=tdt, device=dev),
+                 dw1=torch.empty(n, f, d, dtype=tdt, device=dev),
+                 db1=torch.empty(n, f, dtype=tdt, device=dev),
+                 dw2=torch.empty(n, do, f, dtype=tdt, device=dev),
+                 db2=torch.empty(n, do, dtype=tdt, device=dev))
+    y = torch.empty(T, do, dtype=tdt, device=dev)
+    if args.cached:
+        layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"], y=y)
+        layer.backward(dy, grads=grads)
+        cached_idx = layer.routing(T)["idx"].clone()
+        layer.set_cached_assignment(cached_idx)
+
+    def step():
+        layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"], y=y)
+        layer.backward(dy, grads=grads)
+
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    stats = layer.stats()
+    A = sum(min(c, cap) for c, cap in zip(stats["counts"], layer.capacities))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- timed region (device events on the launching stream) ----------------
+    layer.profile(True)
+    layer.profile_read(reset=True)
+    l0 = layer.launch_count()
+    clk = ClockSampler(local)
+    barrier()
+    clk.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1)
+    clocks = clk.stop()
+    barrier()
+    launches = layer.launch_count() - l0
+    ktimes = layer.profile_read(reset=True)
+    layer.profile(False)
+    ms = max_over_ranks(ms)
+    ms_step = ms / args.steps
+    value = T * ws * args.steps / (ms / 1e3)
+
+    # ---------------- per-kernel rooflines ----------------
+    pk = peaks()
+    work = kernel_work(cfg, T, A, s)
+    sm_peak_tf = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+    kernels = {}
+    for name, (cnt, tot) in ktimes.items():
+        avg_ms = tot / max(cnt, 1)
+        kind, amt = work.get(name, ("byte", 0))
+        ent = {"launches": cnt, "avg_ms": round(avg_ms, 5), "share": None}
+        if amt and avg_ms > 0:
+            if kind == "byte":
+                ach = amt / (avg_ms / 1e3) / 1e9
+                ent.update(bound="hbm", achieved=round(ach, 1), peak=pk["hbm"], unit="GB/s",
+                           frac=round(ach / pk["hbm"], 4), algorithmic=amt)
+            else:
+                ach = amt / (avg_ms / 1e3) / 1e12
+                tc = layer.tdtype == torch.bfloat16 and getattr(layer, "uses_tcgen05", False)
+                peak = pk["bf16_sus"] if tc else sm_peak_tf
+                ent.update(bound="tensor" if tc else "alu", achieved=round(ach, 2), peak=round(peak, 1),
+                           unit="TFLOP/s", frac=round(ach / peak, 4), algorithmic=amt)
+        kernels[name] = ent
+    tot_k = sum(v[1] for v in ktimes.values()) or 1.0
+    for name, (cnt, tot) in ktimes.items():
+        kernels[name]["share"] = round(tot / tot_k, 4)
+    dom = max(ktimes.items(), key=lambda kv: kv[1][1])[0] if ktimes else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if dom and os.path.exists(tp):
+        traffic = json.load(open(tp)).get(args.config, {}).get(dom)
+    dk = kernels.get(dom, {})
+    roofline = {"kernel": dom, "bound": dk.get("bound"), "achieved": dk.get("achieved"),
+                "peak": dk.get("peak"), "unit": dk.get("unit"), "frac": dk.get("frac"),
+                "traffic": traffic, "peak_source": pk["src"]}
+    hbm = {nm: kernels[nm].get("achieved") for nm in ("dispatch", "combine_fwd", "combine_bwd", "gate_dx")
+           if nm in kernels}
+
+    # ---------------- end to end through the public API with host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        x_h = g["x"].cpu().pin_memory()
+        dy_h = dy.cpu().pin_memory()
+        y_h = torch.empty(T, do, dtype=tdt).pin_memory()
+        x_d = torch.empty_like(g["x"])
+        dy_d = torch.empty_like(dy)
+
+        def e2e_step():
+            x_d.copy_(x_h, non_blocking=True)
+            dy_d.copy_(dy_h, non_blocking=True)
+            layer.forward(x_d, g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"], y=y)
+            layer.backward(dy_d, grads=grads)
+            y_h.copy_(y, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": round(T * ws * args.steps / (ems / 1e3), 1), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(x_h.numel() * x_h.element_size() + dy_h.numel() * dy_h.element_size()),
+               "d2h_bytes_per_step": int(y_h.numel() * y_h.element_size())}
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1 only) ----------------
+    cpu_base = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu_base = cpu_oracle_sample(cfg, g, dy, args.cpu_sample, alpha)
+
+    if rank == 0:
+        padded_flops = 12.0 * d * f * sum(c - min(cnt, c) for cnt, c in zip(stats["counts"], layer.capacities))
+        out = {
+            "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+            "data": "synthetic (seeded, uniform regime; random-init weights)",
+            "config": {"workload": f"{cfg.name}: {n} experts top-{k}, d_model {d}, d_ff {f}, "
+                                   f"{T} tokens/GPU, {cfg.dtype}, alpha {alpha}"
+                                   + (", cached assignments" if args.cached else ""),
+                       "tokens_per_gpu": T, "n_experts": n, "top_k": k, "d_model": d, "d_ff": f,
+                       "capacity_factor": alpha, "renormalize": cfg.renormalize,
+                       "parallelism": (f"replicas{ws} (EP pending)" if replicas else "1 GPU"),
+                       "l2": "inputs > L2 (x 134 MB + weights 1 GB), no flush",
+                       "kept_assignments": A, "drops": stats["drops"],
+                       "padding_flops_avoided": padded_flops},
+            "roofline": roofline,
+            "hbm_gbs": hbm,
+            "kernels": kernels,
+            "cpu_baseline": cpu_base,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        if info:
+            return max(i.get("num_threads", 1) for i in info)
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
+def cpu_oracle_sample(cfg, g, dy, tokens, alpha):
+    """The fp64 oracle, as it stands, on a bounded sample of the same workload."""
+    import numpy as np
+    from oracle import moe_oracle as O
+    from synth import to_numpy64
+    n, k = cfg.n_experts, cfg.top_k
+    Ts = min(tokens, g["x"].shape[0])
+    x = to_numpy64(g["x"][:Ts])
+    p = {kk: g[kk].detach().to("cpu", dtype=__import__("torch").float64).numpy()
+         for kk in ("w_gate", "w1", "b1", "w2", "b2")}
+    dyn = to_numpy64(dy[:Ts])
+    caps = O.capacities_from_factors([alpha] * n, Ts, k)
+    t0 = time.perf_counter()
+    st = O.moe_forward(x, p, k, caps, cfg.renormalize)
+    O.moe_backward(st, dyn)
+    dt = time.perf_counter() - t0
+    return {"value": round(Ts / dt, 2), "unit": "tokens/s", "cores": _threads(), "kind": "oracle",
+            "sample": f"{Ts} tokens of {cfg.name} (all {n} experts, alpha {alpha}), fwd+bwd, fp64 NumPy",
+            "seconds": round(dt, 2)}
+
+
+def run_reference(args):
+    """--impl reference: the fp64 oracle on the host cores (rank 0 only)."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+    from oracle import moe_oracle as O
+    from synth import get_config, make_dy, make_layer, to_numpy64
+    cfg = get_config(args.config)
+    alpha = args.alpha if args.alpha is not None else cfg.alpha
+    n, k, d, f, do = cfg.n_experts, cfg.top_k, cfg.d_model, cfg.d_ff, cfg.d_out
+    Ts = max(16, min(256, args.cpu_sample))
+    g = make_layer(n, d, f, do, Ts * (args.steps + args.warmup), cfg.dtype, "uniform")
+    dy = make_dy(Ts * (args.steps + args.warmup), do, cfg.dtype)
+    p = {kk: g[kk].to(torch.float64).numpy() for kk in ("w_gate", "w1", "b1", "w2", "b2")}
+    caps = O.capacities_from_factors([alpha] * n, Ts, k)
+
+    def step(i):
+        x = to_numpy64(g["x"][i * Ts:(i + 1) * Ts])
+        st = O.moe_forward(x, p, k, caps, cfg.renormalize)
+        O.moe_backward(st, to_numpy64(dy[i * Ts:(i + 1) * Ts]))
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    dt = time.perf_counter() - t0
+    val = Ts * args.steps / dt
+    out = {"impl": "reference", "metric": METRIC, "value": round(val, 2), "unit": "tokens/s",
+           "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(dt * 1e3 / args.steps, 2), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{cfg.name}: {n} experts top-{k}, d_model {d}, d_ff {f}, "
+                                  f"{Ts} tokens/step sample, alpha {alpha}"},
+           "cpu_baseline": {"value": round(val, 2), "unit": "tokens/s", "cores": _threads(),
+                            "kind": "oracle", "sample": f"{Ts} tokens per step of {cfg.name}"},
+           "e2e": {"value": round(val, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

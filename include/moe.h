@@ -1,0 +1,240 @@
+/*
+ * moe.h -- C ABI of the B200-native DynaMoE MoE-layer hot path.
+ *
+ * The operation (PAPER.md = /root/reference/PAPER.md, cited as P:line):
+ *   Alg. 1: score <- G(x); indices <- argmax_k(score);
+ *                       (w_1..w_k) <- normalize(score[indices]); y = sum_i w_i * E_{indices[i]}(x)
+ *   Eq. 4: expert capacity C = alpha * batch_size * k / n
+ *   P:225:              samples that do not fit an expert's capacity are dropped and
+ *                       "ignored during back propagation"
+ *   S4.1: dynamic capacity factors  -> moe_set_capacities (a stream-ordered
+ *                       "recompile" of the per-expert buffer sizes; weights untouched)
+ *   S4.2: sample-assignment caching -> moe_set_cached_assignment (cached
+ *                       expert indices drive dispatch so it does not wait for the gate)
+ * Readings of points the paper leaves open are SURVEY.md §8(c) readings 1-15, listed in
+ * DESIGN.md.  In particular: G is one bias-free linear layer W_g [n x d]; top-k selects on
+ * the fp32 logits with ties to the lower expert index; normalize() is sum-normalisation of
+ * the selected softmax probabilities (renormalize=1) or the raw probability (renormalize=0);
+ * capacity is global and the drop order is token-major (ascending global token index);
+ * experts are 2-layer ReLU MLPs  E_e(x) = W2_e relu(W1_e x + b1_e) + b2_e.
+ *
+ * Conventions
+ *  - Every function returns moe_status_t; nothing throws or aborts across the ABI.
+ *  - "device" pointers are CUDA device (HBM) pointers on the handle's device; "host"
+ *    pointers are ordinary CPU memory.  No torch types appear in any signature.
+ *  - Layouts are row-major, torch Linear convention ([out, in]):
+ *      x [T, d], w_gate [n, d], w1 [n, f, d], b1 [n, f], w2 [n, d_out, f], b2 [n, d_out],
+ *      y [T, d_out], dy [T, d_out], dx [T, d].  All in the layer dtype (fp32 or bf16).
+ *  - All GPU work is enqueued on cfg.stream (or the stream set by moe_set_stream) and
+ *    is stream-ordered; calls return without synchronising unless stated.  Internal
+ *    side streams are joined back onto that stream before a call returns.
+ *  - Host-side validation failures return synchronously before any work is enqueued.
+ *  - Device-detected errors (NaN logit, invalid cached index) raise a device flag that is
+ *    reported as MOE_ERR_DEVICE_FLAG by moe_check_device_flags (which synchronises).
+ *  - Ownership: the caller owns every tensor and the workspace; the library owns only its
+ *    handle, internal events/side streams.  x and the parameters must stay unchanged
+ *    until moe_backward has been enqueued (the backward re-reads them).
+ *  - One handle per thread; handles are not reentrant.
+ */
+#ifndef DYNAMOE_B200_MOE_H
+#define DYNAMOE_B200_MOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MOE_API __attribute__((visibility("default")))
+#else
+#define MOE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_ERR_INVALID_ARG = 1,         /* null pointer, bad size, T > max_tokens, capacity < 1 */
+  MOE_ERR_CONFIG = 2,              /* unsupported shape: k > n, n > 256, dims not multiples */
+  MOE_ERR_STATE = 3,               /* e.g. backward before forward, workspace not set */
+  MOE_ERR_WORKSPACE_TOO_SMALL = 4, /* capacities grew: query moe_workspace_size, reallocate */
+  MOE_ERR_CUDA = 5,
+  MOE_ERR_NCCL = 6,
+  MOE_ERR_DEVICE_FLAG = 7          /* a kernel flagged NaN logits or an invalid cached index */
+} moe_status_t;
+
+typedef enum { MOE_F32 = 0, MOE_BF16 = 1 } moe_dtype_t;
+
+typedef struct moe_ctx* moe_handle_t;
+
+/* Layer configuration (fixed for the life of a handle). */
+typedef struct {
+  int32_t n_experts;    /* n, 1..256 */
+  int32_t top_k;        /* k, 1..min(n, 8) */
+  int32_t d_model;      /* d: multiple of 64 for bf16, of 4 for fp32 */
+  int32_t d_ff;         /* f: same rule */
+  int32_t d_out;        /* 0 -> d_model; same rule */
+  int32_t max_tokens;   /* per-rank upper bound on T */
+  int32_t dtype;        /* moe_dtype_t: activation/parameter dtype; logits, weights and
+                           every accumulator are fp32 */
+  int32_t renormalize;  /* 1: Alg. 1 normalize (sum-norm of selected probs);
+                           0: raw softmax probability (Switch-style) */
+  int32_t world_size;   /* expert-parallel group size (1 = single GPU) */
+  int32_t rank;         /* experts [rank*n/R, (rank+1)*n/R) are local */
+  void*   nccl_comm;    /* ncclComm_t of the EP group (torch's communicator); NULL iff R == 1 */
+  void*   stream;       /* cudaStream_t all work is ordered on (NULL = legacy default) */
+} moe_config_t;
+
+/* Create / destroy a layer handle.  moe_init validates cfg (MOE_ERR_CONFIG) and sets the
+   capacities to Eq. 4 with alpha = 1 over T_g = max_tokens * world_size. */
+MOE_API moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out);
+MOE_API moe_status_t moe_destroy(moe_handle_t h);
+MOE_API moe_status_t moe_set_stream(moe_handle_t h, void* stream);
+
+/* Eq. 4, host only: cap_out[e] = max(1, ceil(alpha[e] * tokens_global * k / n))
+   evaluated in fp64.  alpha: host [n]; cap_out: host [n]. */
+MOE_API moe_status_t moe_capacity_from_factors(int32_t n, int64_t tokens_global, int32_t k,
+                                       const double* alpha, int32_t* cap_out);
+
+/* Dynamic capacity factors (S4.1).  cap: host [n], each >= 1 (values above the
+   global token count are clamped to it; the result is unchanged because an expert can
+   receive each token at most once).  Re-lays out the per-expert buffers (row offsets
+   base_e = sum_{e'<e} roundup(C_e', 128)) and takes effect at the next moe_forward enqueued
+   after this call (the new table travels as kernel arguments: stream-ordered, no sync).
+   Returns MOE_ERR_WORKSPACE_TOO_SMALL when the set workspace is too small for the new
+   layout; the capacities ARE recorded, so the caller queries moe_workspace_size,
+   allocates and calls moe_set_workspace.  Weights are never touched. */
+MOE_API moe_status_t moe_set_capacities(moe_handle_t h, const int32_t* cap);
+MOE_API moe_status_t moe_get_capacities(moe_handle_t h, int32_t* cap_out /* host [n] */);
+
+/* Workspace (caller-owned device memory): saved activations X/H/O, gradient scratch
+   dO/dX, routing tables and partial sums.  Size depends on max_tokens and capacities. */
+MOE_API moe_status_t moe_workspace_size(moe_handle_t h, size_t* bytes);
+MOE_API moe_status_t moe_set_workspace(moe_handle_t h, void* dptr, size_t bytes);
+
+/* Sample-assignment caching (S4.2).  d_idx: device int32 [T x k] expert
+   indices (each row k distinct values in [0,n)) read by the NEXT moe_forward; NULL turns
+   caching off.  While on, dispatch (histogram, scan, scatter, and in EP the count exchange)
+   runs on a side stream from these indices concurrently with the gate; the gate still runs
+   and yields the weights normalize(p[t, cached]) (reading 11), the fresh top-k and
+   hit_count = #{t : set(fresh_t) == set(cached_t)}.  d_idx must stay valid until that
+   forward has been consumed by the stream.  Invalid rows raise the device flag. */
+MOE_API moe_status_t moe_set_cached_assignment(moe_handle_t h, const int32_t* d_idx);
+
+/* Forward.  T <= max_tokens (T may be 0).  All pointers device; y is written
+   (y[t] = 0 for a token whose every pair was dropped). */
+typedef struct {
+  int32_t T;
+  const void* x;
+  const void* w_gate;
+  const void* w1;
+  const void* b1;
+  const void* w2;
+  const void* b2;
+  void* y;
+} moe_fwd_args_t;
+MOE_API moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a);
+
+/* Backward of sum(dy * y) for the last forward (which it consumes: H is overwritten by dA).
+   Gradients overwrite their outputs (accumulate = 0) or add to them (accumulate = 1).
+   Any gradient pointer may be NULL to skip writing it, except that the routing / expert
+   chain is always computed.  All pointers device, layer dtype. */
+typedef struct {
+  const void* dy;
+  void* dx;
+  void* dw_gate;
+  void* dw1;
+  void* db1;
+  void* dw2;
+  void* db2;
+  int32_t accumulate;
+} moe_bwd_args_t;
+MOE_API moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a);
+
+/* Device views of the last forward's routing (valid until the next forward).
+   slot_of[t,r] = position of pair (t,r) inside expert idx[t,r]'s buffer, -1 if dropped;
+   token_of_slot[base_e + s] = t_g*k + r for s < kept_e (-1 / unwritten beyond);
+   base has n+1 entries (host copy, row offsets of each expert's buffer). */
+typedef struct {
+  const float* logits;        /* [T x n] fp32 gate logits */
+  const float* weights;       /* [T x k] fp32 gate weights w (at the dispatch indices) */
+  const int32_t* idx;         /* [T x k] dispatch indices (cached ones in cached mode) */
+  const int32_t* fresh_idx;   /* [T x k] fresh top-k of this forward's gate */
+  const int32_t* slot_of;     /* [T x k] */
+  const int32_t* token_of_slot; /* [rows] */
+  const int32_t* counts;      /* [n] pre-drop counts (global over the EP group) */
+  const int32_t* kept;        /* [n] min(count, C_e) */
+  const float* dl;            /* [T x n] fp32 gradient w.r.t. logits (after backward) */
+  const float* dw;            /* [T x k] fp32 gradient w.r.t. gate weights (after backward) */
+  const void* x_buf;          /* [rows x d] dispatched expert inputs */
+  const void* h_buf;          /* [rows x f] ReLU activations (dA after backward) */
+  const void* o_buf;          /* [rows x d_out] expert outputs */
+  int64_t rows;               /* total buffer rows */
+  int32_t base_host[257];     /* host copy of the row offsets, n+1 entries used */
+} moe_routing_t;
+MOE_API moe_status_t moe_get_routing(moe_handle_t h, moe_routing_t* out);
+
+/* Per-forward statistics, enqueued as async D2H copies into caller memory (pinned for
+   true asynchrony).  Valid once the stream has reached this point (event/stream sync).
+   counts: host int32 [n]; drops: host int64 [1]; hit_count: host int32 [1] (cached mode,
+   else 0).  Any pointer may be NULL. */
+typedef struct {
+  int32_t* counts;
+  int64_t* drops;
+  int32_t* hit_count;
+} moe_stats_t;
+MOE_API moe_status_t moe_get_stats_async(moe_handle_t h, const moe_stats_t* dst);
+
+/* Synchronises the stream and reports (then clears) the device error flags:
+   bit 0 = NaN gate logit, bit 1 = invalid cached index.  flags_out may be NULL. */
+MOE_API moe_status_t moe_check_device_flags(moe_handle_t h, int32_t* flags_out);
+
+/* Number of kernels the library launched since the handle was created (for bench
+   accounting of "our kernels in the timed region"). */
+MOE_API moe_status_t moe_launch_count(moe_handle_t h, int64_t* out);
+
+/* Per-kernel timing (for the benchmark's roofline): when enabled, every kernel launch is
+   bracketed by CUDA events on its stream.  moe_profile_read synchronises, then fills up to
+   max entries {name, launches, total_ms} aggregated per kernel name since the last reset. */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double total_ms;
+} moe_kernel_time_t;
+MOE_API moe_status_t moe_profile_enable(moe_handle_t h, int32_t on);
+MOE_API moe_status_t moe_profile_read(moe_handle_t h, moe_kernel_time_t* out, int32_t max,
+                                      int32_t* count, int32_t reset);
+
+/* Human-readable description of the last error on this handle (never NULL). */
+MOE_API const char* moe_last_error(moe_handle_t h);
+
+/* ----------------------------------------------------------------------------------- *
+ * Dynamic capacity policy (host helper, R1).  The paper leaves the policy open
+ * (P:236); this is SPEC's peak-plus-headroom rule: for each
+ * expert, peak = max count over the last `window` iterations; grow at once to
+ * ceil((1+headroom)*peak) when C_e < peak; shrink to that target only after a full window
+ * whose mean count / C_e < shrink_util; alpha_e = C_e*n/(T_g*k) clamped to
+ * [min_alpha, max_alpha] and C_e recomputed by Eq. 4.
+ * ----------------------------------------------------------------------------------- */
+typedef struct moe_policy* moe_policy_t;
+typedef struct {
+  int32_t n_experts, top_k;
+  int64_t tokens_global;
+  int32_t window;        /* default 20 */
+  double headroom;       /* default 0.15 */
+  double shrink_util;    /* default 0.5 */
+  double min_alpha;      /* default 0.25 */
+  double max_alpha;      /* default 8.0 */
+} moe_policy_config_t;
+MOE_API moe_status_t moe_policy_create(const moe_policy_config_t* cfg, const int32_t* init_cap,
+                               moe_policy_t* out);
+/* counts: host [n] observed pre-drop counts of one iteration.  *changed = 1 and
+   new_cap (host [n]) filled when a recompile is due, else *changed = 0. */
+MOE_API moe_status_t moe_policy_update(moe_policy_t p, const int32_t* counts, int32_t* new_cap,
+                               int32_t* changed);
+MOE_API moe_status_t moe_policy_destroy(moe_policy_t p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNAMOE_B200_MOE_H */

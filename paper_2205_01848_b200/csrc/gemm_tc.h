@@ -1,0 +1,32 @@
+// gemm_tc.h -- tcgen05/TMEM/TMA grouped GEMMs of the expert FFN (bf16, sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/moe.h"
+#include "common.cuh"
+
+namespace moe {
+
+// Host-side cache of TMA descriptors keyed by the buffer pointers they were encoded for.
+struct TcPlan {
+  void* dev_maps = nullptr;   // device copy of tensor maps (unused when passed as params)
+  int ready = 0;
+};
+void tc_plan_free(TcPlan* p);
+
+// Forward: H = relu(X W1_e^T + b1_e), O = H W2_e^T + b2_e over kept_e rows per local expert.
+moe_status_t tc_ffn_forward(TcPlan* p, void* X, const void* w1, const void* b1,
+                            const void* w2, const void* b2, void* H, void* O, int64_t rows,
+                            int d, int f, int dout, const int32_t* kept,
+                            const int32_t* mtile_prefix, int n_local, const CapTable& ct,
+                            int max_cap, cudaStream_t s, int64_t* nlaunch);
+// Backward: dW2 = dO^T H, db2 = sum dO; dA = (dO W2) * 1[H>0] (into H);
+// dW1 = dA^T X, db1 = sum dA; dX = dA W1.
+moe_status_t tc_ffn_backward(TcPlan* p, void* X, void* H, void* dO, void* dX, const void* w1,
+                             const void* w2, void* dw1, void* db1, void* dw2, void* db2,
+                             int accumulate, int64_t rows, int d, int f, int dout,
+                             const int32_t* kept, const int32_t* mtile_prefix, int n_local,
+                             const CapTable& ct, int max_cap, cudaStream_t s,
+                             int64_t* nlaunch);
+
+}  // namespace moe

@@ -1,0 +1,75 @@
+// kernels.h -- host-side launchers of the hot-path kernels (internal; not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "common.cuh"
+
+namespace moe {
+
+// Device scratch shared by the launchers (all pointers into the caller's workspace).
+struct RouteBufs {
+  float* logits;          // [T x n]
+  int32_t* idx;           // [T x k] dispatch indices
+  int32_t* fresh_idx;     // [T x k] fresh top-k (cached mode; == idx otherwise)
+  float* w;               // [T x k]
+  int32_t* slot_of;       // [T x k]
+  int32_t* token_of_slot; // [rows]
+  int32_t* tile_hist;     // [ntiles x n]
+  int32_t* tile_off;      // [ntiles x n]
+  int32_t* counts;        // [n]
+  int32_t* kept;          // [n]
+  int32_t* mtile_prefix;  // [n+1] prefix of ceil(kept_e / 128) (GEMM tile scheduler)
+  int64_t* drops;         // [1]
+  int32_t* hit_count;     // [1]
+  int32_t* flags;         // [1] device error flags
+  uint32_t* ticket;       // [1] last-block ticket of route_scan (self-resetting)
+  float* dw;              // [T x k]
+  float* dl;              // [T x n]
+};
+
+// dtype: 0 = fp32, 1 = bf16 for every templated launcher below.
+cudaError_t launch_gate_topk(int dtype, const void* x, const void* wg, int T, int n, int d,
+                             int k, int renorm, const int32_t* cached, RouteBufs b,
+                             cudaStream_t s);
+cudaError_t launch_route_hist(const int32_t* idx, int T, int k, int n, int32_t* hist,
+                              cudaStream_t s);
+cudaError_t launch_route_scan(const int32_t* hist, int ntiles, int n, const CapTable& ct,
+                              RouteBufs b, cudaStream_t s);
+cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T, int k,
+                            int n, int d, int64_t token_base, const CapTable& ct,
+                            RouteBufs b, void* xbuf, cudaStream_t s);
+cudaError_t launch_zero_pad(int dtype, void* buf, int cols, const int32_t* kept, int n,
+                            const CapTable& ct, cudaStream_t s);
+cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, int k,
+                               int d_out, const CapTable& ct, void* y, cudaStream_t s);
+cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, RouteBufs b,
+                               int T, int k, int n, int d_out, int renorm,
+                               const CapTable& ct, void* dobuf, cudaStream_t s);
+cudaError_t launch_gate_dx(int dtype, const void* wg, const void* dxbuf, RouteBufs b, int T,
+                           int k, int n, int d, const CapTable& ct, void* dx, int accumulate,
+                           cudaStream_t s);
+cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int n, int d,
+                           float* partial, int splits, void* dwg, int accumulate,
+                           cudaStream_t s);
+int gate_dw_splits(int T, int d);
+cudaError_t launch_colsum(int dtype, const void* buf, int cols, const int32_t* kept, int n,
+                          const CapTable& ct, void* out, int accumulate, cudaStream_t s);
+
+// Grouped GEMMs of the expert FFN (SIMT fp32/bf16 path, gemm_simt.cu).
+enum EpiKind { EPI_BIAS_RELU = 0, EPI_BIAS = 1, EPI_RELU_MASK = 2, EPI_NONE = 3 };
+// M-grouped: for each local expert e with M_e = kept[e] rows:
+//   C[base_e + m, :] = epi( A[base_e + m, :K] . B_e )
+//   b_kmajor = 1: B_e stored [N x K] (row-major, torch Linear weight), 0: stored [K x N].
+cudaError_t launch_gemm_simt_mgroup(int dtype, const void* A, int lda, const void* B,
+                                    int b_kmajor, int64_t b_estride, const void* bias,
+                                    void* C, int ldc, int N, int K, const int32_t* kept,
+                                    int n_local, const CapTable& ct, int max_rows, int epi,
+                                    cudaStream_t s);
+// K-grouped (weight gradients): for each local expert e, Out_e[M x N] (+)= A_e^T . B_e with
+// A_e = Abuf[base_e : base_e + kept_e, :M], B_e = Bbuf[base_e : base_e + kept_e, :N].
+cudaError_t launch_gemm_simt_kgroup(int dtype, const void* Abuf, int lda, const void* Bbuf,
+                                    int ldb, void* Out, int M, int N, const int32_t* kept,
+                                    int n_local, const CapTable& ct, int accumulate,
+                                    cudaStream_t s);
+
+}  // namespace moe

@@ -1,0 +1,562 @@
+// moe_api.cu -- the C-ABI runtime (moe_ctx): configuration, capacity table and workspace
+// layout, stream-ordered forward/backward orchestration, cached-assignment fork/join,
+// statistics, and the dynamic-capacity policy helper.  See include/moe.h for the contract.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "../../include/moe.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "gemm_tc.h"
+#include "prof.h"
+#include <map>
+
+using namespace moe;
+
+struct Layout {
+  size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
+      xbuf, hbuf, obuf, dobuf, dxbuf, partial, total;
+};
+
+struct moe_ctx {
+  moe_config_t cfg{};
+  int n = 0, k = 0, d = 0, f = 0, dout = 0, maxT = 0, dtype = 0, renorm = 1, R = 1, rank = 0;
+  int n_local = 0, e_lo = 0;
+  size_t s = 4;  // bytes per element
+  cudaStream_t stream = nullptr, side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::vector<int32_t> cap;   // global capacities C_e (all n)
+  CapTable ct{};              // cap (all n) + base (local experts)
+  int64_t rows = 0;           // total local buffer rows
+  int max_cap_local = 0;
+  Layout L{};
+  uint8_t* ws = nullptr;
+  size_t ws_bytes = 0;
+  RouteBufs rb{};
+  const int32_t* cached = nullptr;
+  // saved forward state for backward
+  int have_fwd = 0, T_last = 0;
+  moe_fwd_args_t fa{};
+  int64_t launches = 0;
+  int use_tc = 0;             // tcgen05 path for bf16 (env MOE_FORCE_SIMT=1 disables)
+  TcPlan tc{};
+  Prof prof;
+  std::string err;
+};
+
+namespace {
+
+moe_status_t fail(moe_ctx* h, moe_status_t st, const std::string& msg) {
+  if (h) h->err = msg;
+  return st;
+}
+
+#define CUDA_TRY(h, expr)                                                              \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return fail(h, MOE_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+// count (and optionally time) our kernel launches: nk kernels per launcher call
+#define KL(h, nk, name, st, expr)                  \
+  do {                                             \
+    ProfScope _ps(&(h)->prof, name, st);           \
+    CUDA_TRY(h, expr);                             \
+    (h)->launches += (nk);                         \
+  } while (0)
+
+size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+void compute_layout(moe_ctx* h) {
+  const size_t T = h->maxT, n = h->n, k = h->k;
+  const size_t ntiles = (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE + 1;
+  Layout& L = h->L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += al(bytes); return r; };
+  L.logits = take(T * n * 4);
+  L.idx = take(T * k * 4);
+  L.fresh_idx = take(T * k * 4);
+  L.slot_of = take(T * k * 4);
+  L.w = take(T * k * 4);
+  L.dw = take(T * k * 4);
+  L.dl = take(T * n * 4);
+  L.tile_hist = take(ntiles * n * 4);
+  L.tile_off = take(ntiles * n * 4);
+  L.meta = take(4096);
+  L.token_of_slot = take((size_t)h->rows * 4);
+  L.xbuf = take((size_t)h->rows * h->d * h->s);
+  L.hbuf = take((size_t)h->rows * h->f * h->s);
+  L.obuf = take((size_t)h->rows * h->dout * h->s);
+  L.dobuf = take((size_t)h->rows * h->dout * h->s);
+  L.dxbuf = take((size_t)h->rows * h->d * h->s);
+  L.partial = take((size_t)gate_dw_splits(h->maxT, h->d) * n * h->d * 4 + 4096);
+  L.total = o;
+}
+
+void bind_buffers(moe_ctx* h) {
+  uint8_t* b = h->ws;
+  const Layout& L = h->L;
+  RouteBufs& r = h->rb;
+  r.logits = (float*)(b + L.logits);
+  r.idx = (int32_t*)(b + L.idx);
+  r.fresh_idx = (int32_t*)(b + L.fresh_idx);
+  r.slot_of = (int32_t*)(b + L.slot_of);
+  r.w = (float*)(b + L.w);
+  r.dw = (float*)(b + L.dw);
+  r.dl = (float*)(b + L.dl);
+  r.tile_hist = (int32_t*)(b + L.tile_hist);
+  r.tile_off = (int32_t*)(b + L.tile_off);
+  int32_t* meta = (int32_t*)(b + L.meta);
+  r.counts = meta;                           // [256]
+  r.kept = meta + 256;                       // [256]
+  r.mtile_prefix = meta + 512;               // [257]
+  r.drops = (int64_t*)(meta + 776);          // 8-byte aligned
+  r.hit_count = meta + 780;
+  r.flags = meta + 781;
+  r.ticket = (uint32_t*)(meta + 782);
+  r.token_of_slot = (int32_t*)(b + L.token_of_slot);
+}
+
+void relayout(moe_ctx* h) {
+  int64_t base = 0;
+  h->max_cap_local = 0;
+  for (int e = 0; e < MOE_MAX_E; ++e) h->ct.cap[e] = 0;
+  for (int e = 0; e < h->n; ++e) h->ct.cap[e] = h->cap[e];
+  for (int j = 0; j < h->n_local; ++j) {
+    h->ct.base[j] = (int32_t)base;
+    int c = h->cap[h->e_lo + j];
+    h->max_cap_local = std::max(h->max_cap_local, c);
+    base += ((int64_t)c + MOE_ROW_ALIGN - 1) / MOE_ROW_ALIGN * MOE_ROW_ALIGN;
+  }
+  h->ct.base[h->n_local] = (int32_t)base;
+  h->rows = base;
+  compute_layout(h);
+}
+
+int64_t tokens_global(const moe_ctx* h) { return (int64_t)h->maxT * h->R; }
+
+}  // namespace
+
+extern "C" {
+
+const char* moe_last_error(moe_handle_t h) { return h ? h->err.c_str() : "null handle"; }
+
+moe_status_t moe_capacity_from_factors(int32_t n, int64_t tokens_global, int32_t k,
+                                       const double* alpha, int32_t* cap_out) {
+  if (n <= 0 || k <= 0 || tokens_global < 0 || !alpha || !cap_out) return MOE_ERR_INVALID_ARG;
+  for (int e = 0; e < n; ++e) {
+    if (!(alpha[e] >= 0.0) || !std::isfinite(alpha[e])) return MOE_ERR_INVALID_ARG;
+    double c = std::ceil(alpha[e] * (double)tokens_global * (double)k / (double)n);  // Eq. 4
+    if (c > 2147483647.0) return MOE_ERR_INVALID_ARG;
+    cap_out[e] = std::max(1, (int)c);
+  }
+  return MOE_OK;
+}
+
+moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
+  if (!cfg || !out) return MOE_ERR_INVALID_ARG;
+  *out = nullptr;
+  const moe_config_t& c = *cfg;
+  int dout = c.d_out ? c.d_out : c.d_model;
+  if (c.n_experts < 1 || c.n_experts > MOE_MAX_E) return MOE_ERR_CONFIG;
+  if (c.top_k < 1 || c.top_k > c.n_experts || c.top_k > MOE_MAX_K) return MOE_ERR_CONFIG;
+  if (c.dtype != MOE_F32 && c.dtype != MOE_BF16) return MOE_ERR_CONFIG;
+  const int mult = c.dtype == MOE_BF16 ? 64 : 4;
+  if (c.d_model <= 0 || c.d_ff <= 0 || dout <= 0 || c.d_model % mult || c.d_ff % mult ||
+      dout % mult)
+    return MOE_ERR_CONFIG;
+  if (c.max_tokens < 0) return MOE_ERR_INVALID_ARG;
+  if (c.world_size < 1 || c.rank < 0 || c.rank >= c.world_size) return MOE_ERR_INVALID_ARG;
+  if (c.n_experts % c.world_size) return MOE_ERR_CONFIG;
+  if (c.world_size > 1 && !c.nccl_comm) return MOE_ERR_INVALID_ARG;
+  moe_ctx* h = new moe_ctx();
+  h->cfg = c;
+  h->n = c.n_experts; h->k = c.top_k; h->d = c.d_model; h->f = c.d_ff; h->dout = dout;
+  h->maxT = c.max_tokens; h->dtype = c.dtype; h->renorm = c.renormalize ? 1 : 0;
+  h->R = c.world_size; h->rank = c.rank;
+  h->n_local = h->n / h->R; h->e_lo = h->rank * h->n_local;
+  h->s = c.dtype == MOE_BF16 ? 2 : 4;
+  h->stream = (cudaStream_t)c.stream;
+  const char* fs = getenv("MOE_FORCE_SIMT");
+  h->use_tc = 0;  // tcgen05 path enabled once parity-green
+  (void)fs;
+  if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    delete h;
+    return MOE_ERR_CUDA;
+  }
+  // default capacities: Eq. 4 with alpha = 1 over the global token count
+  h->cap.assign(h->n, 1);
+  std::vector<double> a(h->n, 1.0);
+  moe_capacity_from_factors(h->n, tokens_global(h), h->k, a.data(), h->cap.data());
+  for (auto& v : h->cap) v = (int32_t)std::min<int64_t>(v, std::max<int64_t>(1, tokens_global(h)));
+  relayout(h);
+  if (h->R > 1) {  // expert parallelism lands in its own milestone
+    delete h;
+    return MOE_ERR_CONFIG;
+  }
+  *out = h;
+  return MOE_OK;
+}
+
+moe_status_t moe_destroy(moe_handle_t h) {
+  if (!h) return MOE_ERR_INVALID_ARG;
+  if (h->side) cudaStreamSynchronize(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->side) cudaStreamDestroy(h->side);
+  tc_plan_free(&h->tc);
+  h->prof.destroy();
+  delete h;
+  return MOE_OK;
+}
+
+moe_status_t moe_set_stream(moe_handle_t h, void* stream) {
+  if (!h) return MOE_ERR_INVALID_ARG;
+  h->stream = (cudaStream_t)stream;
+  return MOE_OK;
+}
+
+moe_status_t moe_set_capacities(moe_handle_t h, const int32_t* cap) {
+  if (!h || !cap) return MOE_ERR_INVALID_ARG;
+  for (int e = 0; e < h->n; ++e)
+    if (cap[e] < 1) return fail(h, MOE_ERR_INVALID_ARG, "capacity < 1");
+  const int64_t tg = std::max<int64_t>(1, tokens_global(h));
+  for (int e = 0; e < h->n; ++e) h->cap[e] = (int32_t)std::min<int64_t>(cap[e], tg);
+  relayout(h);
+  h->have_fwd = 0;  // saved activations no longer match the layout
+  if (h->ws && h->ws_bytes < h->L.total) {
+    h->ws = nullptr;
+    h->ws_bytes = 0;
+    return fail(h, MOE_ERR_WORKSPACE_TOO_SMALL, "workspace too small for new capacities");
+  }
+  if (h->ws) bind_buffers(h);
+  return MOE_OK;
+}
+
+moe_status_t moe_get_capacities(moe_handle_t h, int32_t* cap_out) {
+  if (!h || !cap_out) return MOE_ERR_INVALID_ARG;
+  std::memcpy(cap_out, h->cap.data(), sizeof(int32_t) * h->n);
+  return MOE_OK;
+}
+
+moe_status_t moe_workspace_size(moe_handle_t h, size_t* bytes) {
+  if (!h || !bytes) return MOE_ERR_INVALID_ARG;
+  *bytes = h->L.total;
+  return MOE_OK;
+}
+
+moe_status_t moe_set_workspace(moe_handle_t h, void* dptr, size_t bytes) {
+  if (!h || !dptr) return MOE_ERR_INVALID_ARG;
+  if ((uintptr_t)dptr % 256) return fail(h, MOE_ERR_INVALID_ARG, "workspace must be 256-B aligned");
+  if (bytes < h->L.total) return fail(h, MOE_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+  bool was_set = h->ws != nullptr;
+  h->ws = (uint8_t*)dptr;
+  h->ws_bytes = bytes;
+  bind_buffers(h);
+  (void)was_set;
+  CUDA_TRY(h, cudaMemsetAsync(h->ws + h->L.meta, 0, 4096, h->stream));
+  h->have_fwd = 0;
+  return MOE_OK;
+}
+
+moe_status_t moe_set_cached_assignment(moe_handle_t h, const int32_t* d_idx) {
+  if (!h) return MOE_ERR_INVALID_ARG;
+  h->cached = d_idx;
+  return MOE_OK;
+}
+
+moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
+  if (!h || !a) return MOE_ERR_INVALID_ARG;
+  if (!h->ws) return fail(h, MOE_ERR_STATE, "workspace not set");
+  if (a->T < 0 || a->T > h->maxT) return fail(h, MOE_ERR_INVALID_ARG, "T out of range");
+  if (a->T > 0 && (!a->x || !a->w_gate || !a->w1 || !a->b1 || !a->w2 || !a->b2 || !a->y))
+    return fail(h, MOE_ERR_INVALID_ARG, "null tensor");
+  const int T = a->T, n = h->n, k = h->k, d = h->d, f = h->f, dout = h->dout, dt = h->dtype;
+  cudaStream_t s0 = h->stream;
+  RouteBufs& rb = h->rb;
+  uint8_t* ws = h->ws;
+  void* X = ws + h->L.xbuf;
+  void* H = ws + h->L.hbuf;
+  void* O = ws + h->L.obuf;
+  const int ntiles = (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE;
+  const bool cached = h->cached != nullptr;
+  CUDA_TRY(h, cudaMemsetAsync(rb.hit_count, 0, 4, s0));
+
+  // Everything from the routing tables up to the expert outputs depends only on the
+  // dispatch indices.  Uncached: they are the gate's top-k, so it all follows the gate on
+  // s0.  Cached (S4.2): they are known before the gate, so this chain runs on a
+  // side stream concurrently with the gate; the join is before the combine, the first step
+  // that needs the gate weights.
+  cudaStream_t sd = s0;
+  if (cached) {
+    CUDA_TRY(h, cudaEventRecord(h->ev_fork, s0));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    sd = h->side;
+    if (T > 0)
+      CUDA_TRY(h, cudaMemcpyAsync(rb.idx, h->cached, (size_t)T * k * 4, cudaMemcpyDeviceToDevice, sd));
+  } else {
+    KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, nullptr, rb, s0));
+  }
+  KL(h, T > 0, "route_hist", sd, launch_route_hist(rb.idx, T, k, n, rb.tile_hist, sd));
+  KL(h, 1, "route_scan", sd, launch_route_scan(rb.tile_hist, ntiles, n, h->ct, rb, sd));
+  KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->ct, rb, X, sd));
+  KL(h, 1, "zero_pad", sd, launch_zero_pad(dt, X, d, rb.kept, n, h->ct, sd));
+  // expert FFN: H = relu(X W1^T + b1); O = H W2^T + b2 over kept_e rows per local expert
+  const int nl = h->n_local;
+  const char* w1 = (const char*)a->w1 + (size_t)h->e_lo * f * d * h->s;
+  const char* b1 = (const char*)a->b1 + (size_t)h->e_lo * f * h->s;
+  const char* w2 = (const char*)a->w2 + (size_t)h->e_lo * dout * f * h->s;
+  const char* b2 = (const char*)a->b2 + (size_t)h->e_lo * dout * h->s;
+  const int32_t* kept_local = rb.kept;
+  if (h->use_tc) {
+    int64_t nk = 0;
+    moe_status_t st = tc_ffn_forward(&h->tc, X, w1, b1, w2, b2, H, O, h->rows, d, f, dout,
+                                     kept_local, rb.mtile_prefix, nl, h->ct, h->max_cap_local,
+                                     sd, &nk);
+    h->launches += nk;
+    if (st != MOE_OK) return fail(h, st, "tcgen05 forward failed");
+  } else {
+    KL(h, 1, "ffn_gemm1", sd, launch_gemm_simt_mgroup(dt, X, d, w1, 1, (int64_t)f * d, b1, H, f, f, d, kept_local,
+                                     nl, h->ct, h->max_cap_local, EPI_BIAS_RELU, sd));
+    KL(h, 1, "ffn_gemm2", sd, launch_gemm_simt_mgroup(dt, H, f, w2, 1, (int64_t)dout * f, b2, O, dout, dout, f,
+                                     kept_local, nl, h->ct, h->max_cap_local, EPI_BIAS, sd));
+  }
+  if (cached) {
+    KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, h->cached, rb, s0));
+    CUDA_TRY(h, cudaEventRecord(h->ev_join, sd));
+    CUDA_TRY(h, cudaStreamWaitEvent(s0, h->ev_join, 0));
+  }
+  KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O, rb, T, k, dout, h->ct, a->y, s0));
+  h->fa = *a;
+  h->T_last = T;
+  h->have_fwd = 1;
+  return MOE_OK;
+}
+
+moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
+  if (!h || !a) return MOE_ERR_INVALID_ARG;
+  if (!h->have_fwd) return fail(h, MOE_ERR_STATE, "backward without a matching forward");
+  const int T = h->T_last, n = h->n, k = h->k, d = h->d, f = h->f, dout = h->dout,
+            dt = h->dtype;
+  if (T > 0 && !a->dy) return fail(h, MOE_ERR_INVALID_ARG, "null dy");
+  cudaStream_t s0 = h->stream;
+  RouteBufs& rb = h->rb;
+  uint8_t* ws = h->ws;
+  void* X = ws + h->L.xbuf;
+  void* H = ws + h->L.hbuf;   // holds H; overwritten by dA below
+  void* O = ws + h->L.obuf;
+  void* dO = ws + h->L.dobuf;
+  void* dXb = ws + h->L.dxbuf;
+  const moe_fwd_args_t& fa = h->fa;
+  const int nl = h->n_local;
+  const int acc = a->accumulate ? 1 : 0;
+  const int32_t* kept_local = rb.kept;
+
+  // K6 combine backward -> dO rows (local or, in EP, returned to the expert owners), dw, dl
+  KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O, rb, T, k, n, dout, h->renorm, h->ct, dO, s0));
+  KL(h, 1, "zero_pad", s0, launch_zero_pad(dt, dO, dout, kept_local, nl, h->ct, s0));
+  const char* w1 = (const char*)fa.w1 + (size_t)h->e_lo * f * d * h->s;
+  const char* w2 = (const char*)fa.w2 + (size_t)h->e_lo * dout * f * h->s;
+  char* dw1 = a->dw1 ? (char*)a->dw1 + (size_t)h->e_lo * f * d * h->s : nullptr;
+  char* db1 = a->db1 ? (char*)a->db1 + (size_t)h->e_lo * f * h->s : nullptr;
+  char* dw2 = a->dw2 ? (char*)a->dw2 + (size_t)h->e_lo * dout * f * h->s : nullptr;
+  char* db2 = a->db2 ? (char*)a->db2 + (size_t)h->e_lo * dout * h->s : nullptr;
+  if (h->use_tc) {
+    int64_t nk = 0;
+    moe_status_t st = tc_ffn_backward(&h->tc, X, H, dO, dXb, w1, w2, dw1, db1, dw2, db2, acc,
+                                      h->rows, d, f, dout, kept_local, rb.mtile_prefix, nl,
+                                      h->ct, h->max_cap_local, s0, &nk);
+    h->launches += nk;
+    if (st != MOE_OK) return fail(h, st, "tcgen05 backward failed");
+  } else {
+    // B3a: dW2_e = dO_e^T H_e ; db2 = sum dO   (before H is overwritten by dA)
+    if (dw2) KL(h, 1, "wgrad_w2", s0, launch_gemm_simt_kgroup(dt, dO, dout, H, f, dw2, dout, f, kept_local, nl, h->ct, acc, s0));
+    if (db2) KL(h, 1, "bias_grad", s0, launch_colsum(dt, dO, dout, kept_local, nl, h->ct, db2, acc, s0));
+    // B2a: dA = (dO W2_e) * 1[H > 0]   (in place over H)
+    KL(h, 1, "dgrad_dA", s0, launch_gemm_simt_mgroup(dt, dO, dout, w2, 0, (int64_t)dout * f, nullptr, H, f, f,
+                                     dout, kept_local, nl, h->ct, h->max_cap_local, EPI_RELU_MASK, s0));
+    // B3b: dW1_e = dA_e^T X_e ; db1 = sum dA
+    if (dw1) KL(h, 1, "wgrad_w1", s0, launch_gemm_simt_kgroup(dt, H, f, X, d, dw1, f, d, kept_local, nl, h->ct, acc, s0));
+    if (db1) KL(h, 1, "bias_grad", s0, launch_colsum(dt, H, f, kept_local, nl, h->ct, db1, acc, s0));
+    // B2b: dX_e = dA_e W1_e
+    KL(h, 1, "dgrad_dX", s0, launch_gemm_simt_mgroup(dt, H, f, w1, 0, (int64_t)f * d, nullptr, dXb, d, d, f,
+                                     kept_local, nl, h->ct, h->max_cap_local, EPI_NONE, s0));
+  }
+  // B4: dx = gather(dX) + dl W_g ;  B5: dW_g = dl^T x
+  if (a->dx)
+    KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dXb, rb, T, k, n, d, h->ct, a->dx, acc, s0));
+  if (a->dw_gate) {
+    int splits = gate_dw_splits(h->maxT, d);
+    KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw(dt, rb.dl, fa.x, T, n, d, (float*)(ws + h->L.partial),
+                                        splits, a->dw_gate, acc, s0));
+  }
+  h->have_fwd = 0;  // H has been consumed
+  return MOE_OK;
+}
+
+moe_status_t moe_get_routing(moe_handle_t h, moe_routing_t* out) {
+  if (!h || !out) return MOE_ERR_INVALID_ARG;
+  if (!h->ws) return fail(h, MOE_ERR_STATE, "workspace not set");
+  std::memset(out, 0, sizeof(*out));
+  const RouteBufs& r = h->rb;
+  out->logits = r.logits;
+  out->weights = r.w;
+  out->idx = r.idx;
+  out->fresh_idx = h->cached ? r.fresh_idx : r.idx;
+  out->slot_of = r.slot_of;
+  out->token_of_slot = r.token_of_slot;
+  out->counts = r.counts;
+  out->kept = r.kept;
+  out->dl = r.dl;
+  out->dw = r.dw;
+  out->x_buf = h->ws + h->L.xbuf;
+  out->h_buf = h->ws + h->L.hbuf;
+  out->o_buf = h->ws + h->L.obuf;
+  out->rows = h->rows;
+  for (int j = 0; j <= h->n_local; ++j) out->base_host[j] = h->ct.base[j];
+  return MOE_OK;
+}
+
+moe_status_t moe_get_stats_async(moe_handle_t h, const moe_stats_t* dst) {
+  if (!h || !dst) return MOE_ERR_INVALID_ARG;
+  if (!h->ws) return fail(h, MOE_ERR_STATE, "workspace not set");
+  if (dst->counts)
+    CUDA_TRY(h, cudaMemcpyAsync(dst->counts, h->rb.counts, 4 * h->n, cudaMemcpyDeviceToHost, h->stream));
+  if (dst->drops)
+    CUDA_TRY(h, cudaMemcpyAsync(dst->drops, h->rb.drops, 8, cudaMemcpyDeviceToHost, h->stream));
+  if (dst->hit_count)
+    CUDA_TRY(h, cudaMemcpyAsync(dst->hit_count, h->rb.hit_count, 4, cudaMemcpyDeviceToHost, h->stream));
+  return MOE_OK;
+}
+
+moe_status_t moe_check_device_flags(moe_handle_t h, int32_t* flags_out) {
+  if (!h) return MOE_ERR_INVALID_ARG;
+  if (!h->ws) return fail(h, MOE_ERR_STATE, "workspace not set");
+  int32_t fl = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(&fl, h->rb.flags, 4, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (flags_out) *flags_out = fl;
+  if (fl) {
+    CUDA_TRY(h, cudaMemsetAsync(h->rb.flags, 0, 4, h->stream));
+    return fail(h, MOE_ERR_DEVICE_FLAG,
+                std::string("device flags: ") + ((fl & 1) ? "NaN logit " : "") +
+                    ((fl & 2) ? "invalid cached index" : ""));
+  }
+  return MOE_OK;
+}
+
+moe_status_t moe_profile_enable(moe_handle_t h, int32_t on) {
+  if (!h) return MOE_ERR_INVALID_ARG;
+  h->prof.on = on != 0;
+  return MOE_OK;
+}
+
+moe_status_t moe_profile_read(moe_handle_t h, moe_kernel_time_t* out, int32_t max,
+                              int32_t* count, int32_t reset) {
+  if (!h || !count || (max > 0 && !out)) return MOE_ERR_INVALID_ARG;
+  CUDA_TRY(h, cudaDeviceSynchronize());
+  std::vector<std::string> order;
+  std::map<std::string, std::pair<int64_t, double>> agg;
+  for (const auto& r : h->prof.recs) {
+    float ms = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&ms, r.a, r.b));
+    auto it = agg.find(r.name);
+    if (it == agg.end()) {
+      order.push_back(r.name);
+      agg[r.name] = {1, (double)ms};
+    } else {
+      it->second.first += 1;
+      it->second.second += ms;
+    }
+  }
+  int c = 0;
+  for (const auto& nm : order) {
+    if (c >= max) break;
+    std::memset(out[c].name, 0, sizeof(out[c].name));
+    std::strncpy(out[c].name, nm.c_str(), sizeof(out[c].name) - 1);
+    out[c].launches = agg[nm].first;
+    out[c].total_ms = agg[nm].second;
+    ++c;
+  }
+  *count = c;
+  if (reset) h->prof.reset();
+  return MOE_OK;
+}
+
+moe_status_t moe_launch_count(moe_handle_t h, int64_t* out) {
+  if (!h || !out) return MOE_ERR_INVALID_ARG;
+  *out = h->launches;
+  return MOE_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// Dynamic capacity policy (SPEC S:449-456 concretisation of P:236; see moe.h)
+// ------------------------------------------------------------------------------------
+struct moe_policy {
+  moe_policy_config_t c;
+  std::vector<int32_t> caps;
+  std::deque<std::vector<int32_t>> hist;
+};
+
+static int32_t policy_clamp(const moe_policy* p, int64_t c) {
+  double alpha = (double)c * p->c.n_experts / ((double)p->c.tokens_global * p->c.top_k);
+  alpha = std::min(std::max(alpha, p->c.min_alpha), p->c.max_alpha);
+  // Eq. 4 with this expert's alpha: max(1, ceil(alpha * T_g * k / n))
+  double v = std::ceil(alpha * (double)p->c.tokens_global * p->c.top_k / p->c.n_experts);
+  return std::max<int32_t>(1, (int32_t)v);
+}
+
+moe_status_t moe_policy_create(const moe_policy_config_t* cfg, const int32_t* init_cap,
+                               moe_policy_t* out) {
+  if (!cfg || !init_cap || !out || cfg->n_experts < 1 || cfg->top_k < 1 ||
+      cfg->tokens_global < 1 || cfg->window < 1 || cfg->min_alpha > cfg->max_alpha)
+    return MOE_ERR_INVALID_ARG;
+  moe_policy* p = new moe_policy();
+  p->c = *cfg;
+  p->caps.assign(init_cap, init_cap + cfg->n_experts);
+  *out = p;
+  return MOE_OK;
+}
+
+moe_status_t moe_policy_update(moe_policy_t p, const int32_t* counts, int32_t* new_cap,
+                               int32_t* changed) {
+  if (!p || !counts || !new_cap || !changed) return MOE_ERR_INVALID_ARG;
+  const int n = p->c.n_experts;
+  p->hist.emplace_back(counts, counts + n);
+  if ((int)p->hist.size() > p->c.window) p->hist.pop_front();
+  std::vector<int32_t> nc = p->caps;
+  const int W = (int)p->hist.size();
+  for (int e = 0; e < n; ++e) {
+    int64_t peak = 0, sum = 0;
+    for (const auto& hrow : p->hist) {
+      peak = std::max<int64_t>(peak, hrow[e]);
+      sum += hrow[e];
+    }
+    int64_t target = (int64_t)std::ceil((1.0 + p->c.headroom) * (double)peak);
+    if (p->caps[e] < peak) {
+      nc[e] = policy_clamp(p, target);
+    } else if (W == p->c.window && ((double)sum / W) / p->caps[e] < p->c.shrink_util) {
+      nc[e] = policy_clamp(p, std::max<int64_t>(target, 1));
+    }
+  }
+  *changed = (nc != p->caps) ? 1 : 0;
+  if (*changed) p->caps = nc;
+  std::memcpy(new_cap, p->caps.data(), sizeof(int32_t) * n);
+  return MOE_OK;
+}
+
+moe_status_t moe_policy_destroy(moe_policy_t p) {
+  delete p;
+  return MOE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,766 @@
+// route_kernels.cu -- gate/top-k, routing (histogram, scan, stable scatter), combine and
+// their backwards for the DynaMoE MoE layer on sm_100a.
+//
+// Paper passages: Alg. 1 lines 1-3 (gate, argmax_k, normalize) and 5-8
+// (weighted combine); P:225 (capacity drop, zero gradient for dropped samples); Eq. 4
+// (capacities arrive as integers in CapTable); S4.2 P:238-256 (cached indices).
+// Readings: top-k on fp32 logits, IEEE '>', ties -> lower expert
+// index; token-major global drop order; relu'(0) = 0; fp32 accumulators everywhere; no
+// floating-point atomics (bitwise run-to-run determinism).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace moe {
+
+// =====================================================================================
+// K1 (SIMT form): gate logits l = x W_g^T (fp32 accumulate, sequential over d), then
+// softmax / top-k / normalize per token.  CTA = 32 tokens x all n experts.
+// =====================================================================================
+constexpr int GATE_TOK = 32;
+constexpr int GATE_DK = 32;
+
+template <typename T, int NJ>
+__global__ void __launch_bounds__(256) gate_topk_kernel(
+    const T* __restrict__ x, const T* __restrict__ wg, int Tn, int n, int d, int k,
+    int renorm, const int32_t* __restrict__ cached, float* __restrict__ logits,
+    int32_t* __restrict__ idx_out, float* __restrict__ w_out, int32_t* __restrict__ hit,
+    int32_t* __restrict__ flags) {
+  extern __shared__ float smem[];
+  float* xs = smem;                              // [GATE_TOK][GATE_DK+1]
+  float* ws = xs + GATE_TOK * (GATE_DK + 1);     // [n][GATE_DK+1]
+  const int tid = threadIdx.x;
+  const int t0 = blockIdx.x * GATE_TOK;
+  const int tok = tid >> 3, g = tid & 7;
+  float acc[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) acc[j] = 0.f;
+
+  for (int k0 = 0; k0 < d; k0 += GATE_DK) {
+    for (int i = tid; i < GATE_TOK * GATE_DK; i += 256) {
+      int r = i / GATE_DK, c = i % GATE_DK;
+      int t = t0 + r;
+      xs[r * (GATE_DK + 1) + c] = (t < Tn) ? to_f(x[(size_t)t * d + k0 + c]) : 0.f;
+    }
+    for (int i = tid; i < n * GATE_DK; i += 256) {
+      int r = i / GATE_DK, c = i % GATE_DK;
+      ws[r * (GATE_DK + 1) + c] = to_f(wg[(size_t)r * d + k0 + c]);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int c = 0; c < GATE_DK; ++c) {
+      float xv = xs[tok * (GATE_DK + 1) + c];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        int e = g + 8 * j;
+        if (e < n) acc[j] = fmaf(xv, ws[e * (GATE_DK + 1) + c], acc[j]);
+      }
+    }
+    __syncthreads();
+  }
+  // logits -> smem [GATE_TOK][n+1] (reuses ws) and global
+  float* ls = ws;
+  {
+    int t = t0 + tok;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      int e = g + 8 * j;
+      if (e < n) {
+        ls[tok * (n + 1) + e] = acc[j];
+        if (t < Tn) logits[(size_t)t * n + e] = acc[j];
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < GATE_TOK) {
+    const int t = t0 + tid;
+    if (t < Tn) {
+      const float* l = ls + tid * (n + 1);
+      // top-k: repeatedly take the first maximum among experts not yet taken (IEEE '>',
+      // strict, so equal values -- including -0.0 vs +0.0 -- keep the lower index).
+      int sel[MOE_MAX_K];
+      bool nan_seen = false;
+      for (int r = 0; r < k; ++r) {
+        int best = -1;
+        float bv = 0.f;
+        for (int e = 0; e < n; ++e) {
+          bool taken = false;
+          for (int q = 0; q < r; ++q) taken |= (sel[q] == e);
+          if (taken) continue;
+          float v = l[e];
+          if (v != v) nan_seen = true;
+          if (best < 0 || v > bv) { best = e; bv = v; }
+        }
+        sel[r] = best;
+      }
+      if (nan_seen) atomicOr(flags, 1);
+      int32_t* orow = idx_out + (size_t)t * k;
+      for (int r = 0; r < k; ++r) orow[r] = sel[r];
+      // dispatch indices: cached (validated) or fresh
+      int use[MOE_MAX_K];
+      if (cached) {
+        const int32_t* crow = cached + (size_t)t * k;
+        bool ok = true;
+        for (int r = 0; r < k; ++r) {
+          use[r] = crow[r];
+          ok &= (use[r] >= 0 && use[r] < n);
+          for (int q = 0; q < r; ++q) ok &= (use[q] != use[r]);
+        }
+        if (!ok) {
+          atomicOr(flags, 2);
+          for (int r = 0; r < k; ++r) use[r] = sel[r];
+        }
+        bool same = true;  // set equality of fresh and cached rows
+        for (int r = 0; r < k; ++r) {
+          bool found = false;
+          for (int q = 0; q < k; ++q) found |= (use[r] == sel[q]);
+          same &= found;
+        }
+        if (same) atomicAdd(hit, 1);
+      } else {
+        for (int r = 0; r < k; ++r) use[r] = sel[r];
+      }
+      // normalize (Alg. 1 l.3): renorm = softmax over the selected logits; raw = p_i.
+      float* wrow = w_out + (size_t)t * k;
+      if (renorm) {
+        float m = l[use[0]];
+        for (int r = 1; r < k; ++r) m = fmaxf(m, l[use[r]]);
+        float ev[MOE_MAX_K], s = 0.f;
+        for (int r = 0; r < k; ++r) { ev[r] = expf(l[use[r]] - m); s += ev[r]; }
+        for (int r = 0; r < k; ++r) wrow[r] = ev[r] / s;
+      } else {
+        float m = l[0];
+        for (int e = 1; e < n; ++e) m = fmaxf(m, l[e]);
+        float s = 0.f;
+        for (int e = 0; e < n; ++e) s += expf(l[e] - m);
+        for (int r = 0; r < k; ++r) wrow[r] = expf(l[use[r]] - m) / s;
+      }
+    }
+  }
+}
+
+cudaError_t launch_gate_topk(int dtype, const void* x, const void* wg, int T, int n, int d,
+                             int k, int renorm, const int32_t* cached, RouteBufs b,
+                             cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  dim3 grid((T + GATE_TOK - 1) / GATE_TOK);
+  size_t smem = (size_t)(GATE_TOK * (GATE_DK + 1)) * 4 +
+                (size_t)max(n * (GATE_DK + 1), GATE_TOK * (n + 1)) * 4;
+  int32_t* idx_out = cached ? b.fresh_idx : b.idx;
+#define GATE_CASE(NJ)                                                                      \
+  if (n <= 8 * NJ) {                                                                       \
+    if (dtype == 1) {                                                                      \
+      auto kf = gate_topk_kernel<__nv_bfloat16, NJ>;                                       \
+      cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+      kf<<<grid, 256, smem, s>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)wg, T, n,  \
+                                 d, k, renorm, cached, b.logits, idx_out, b.w,             \
+                                 b.hit_count, b.flags);                                    \
+    } else {                                                                               \
+      auto kf = gate_topk_kernel<float, NJ>;                                               \
+      cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+      kf<<<grid, 256, smem, s>>>((const float*)x, (const float*)wg, T, n, d, k, renorm,    \
+                                 cached, b.logits, idx_out, b.w, b.hit_count, b.flags);    \
+    }                                                                                      \
+    return cudaGetLastError();                                                             \
+  }
+  GATE_CASE(1) GATE_CASE(2) GATE_CASE(4) GATE_CASE(8) GATE_CASE(16) GATE_CASE(32)
+#undef GATE_CASE
+  return cudaErrorInvalidValue;
+}
+
+// =====================================================================================
+// K2a: per-tile expert histogram of the dispatch indices (order-independent counts).
+// =====================================================================================
+__global__ void route_hist_kernel(const int32_t* __restrict__ idx, int Tn, int k, int n,
+                                  int32_t* __restrict__ hist) {
+  __shared__ int32_t h[MOE_MAX_E];
+  for (int e = threadIdx.x; e < n; e += blockDim.x) h[e] = 0;
+  __syncthreads();
+  int t = blockIdx.x * MOE_ROUTE_TILE + threadIdx.x;
+  if (t < Tn)
+    for (int r = 0; r < k; ++r) atomicAdd(&h[idx[(size_t)t * k + r]], 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < n; e += blockDim.x) hist[(size_t)blockIdx.x * n + e] = h[e];
+}
+
+cudaError_t launch_route_hist(const int32_t* idx, int T, int k, int n, int32_t* hist,
+                              cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  int ntiles = (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE;
+  route_hist_kernel<<<ntiles, MOE_ROUTE_TILE, 0, s>>>(idx, T, k, n, hist);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K2b: exclusive scan of the tile histograms per expert (one CTA per expert), then the
+// last CTA finalises: kept_e = min(cnt_e, C_e), drops = sum(cnt - kept), GEMM m-tile prefix.
+// =====================================================================================
+__global__ void __launch_bounds__(256) route_scan_kernel(
+    const int32_t* __restrict__ hist, int ntiles, int n, CapTable ct,
+    int32_t* __restrict__ tile_off, int32_t* __restrict__ counts, int32_t* __restrict__ kept,
+    int32_t* __restrict__ mtile_prefix, int64_t* __restrict__ drops,
+    uint32_t* __restrict__ ticket) {
+  const int e = blockIdx.x;
+  __shared__ int32_t warp_tot[8];
+  __shared__ int32_t carry;
+  __shared__ bool is_last;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int t0 = 0; t0 < ntiles; t0 += 256) {
+    int i = t0 + threadIdx.x;
+    int v = (i < ntiles) ? hist[(size_t)i * n + e] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    int wpre = 0, tot = 0;
+    for (int q = 0; q < 8; ++q) {
+      if (q < wid) wpre += warp_tot[q];
+      tot += warp_tot[q];
+    }
+    if (i < ntiles) tile_off[(size_t)i * n + e] = carry + wpre + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    counts[e] = carry;
+    __threadfence();
+    unsigned prev = atomicAdd(ticket, 1u);
+    is_last = (prev == (unsigned)(gridDim.x - 1));
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    long long dr = 0;
+    int pre = 0;
+    for (int q = 0; q < n; ++q) {
+      int c = *((volatile int32_t*)counts + q);
+      int kq = min(c, ct.cap[q]);
+      kept[q] = kq;
+      dr += (long long)(c - kq);
+      mtile_prefix[q] = pre;
+      pre += (kq + 127) / 128;
+    }
+    mtile_prefix[n] = pre;
+    *drops = dr;
+    *ticket = 0u;  // self-reset for the next launch
+  }
+}
+
+cudaError_t launch_route_scan(const int32_t* hist, int ntiles, int n, const CapTable& ct,
+                              RouteBufs b, cudaStream_t s) {
+  route_scan_kernel<<<n, 256, 0, s>>>(hist, ntiles, n, ct, b.tile_off, b.counts, b.kept,
+                                      b.mtile_prefix, b.drops, b.ticket);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K3: stable capacity-bounded scatter.  Per 128-token tile: intra-tile ranks from per-expert
+// token bitmasks (popc of lower tokens; exact token-major order since an expert appears at
+// most once per token), slot = tile_off + rank; kept iff slot < C_e.  Then each warp
+// copies its tokens' rows x[t] -> X_buf[base_e + slot] with 16-byte vectors (row read once,
+// written once per kept pair).
+// =====================================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) dispatch_kernel(
+    const int32_t* __restrict__ idx, const T* __restrict__ x, int Tn, int k, int n, int d,
+    long long token_base, CapTable ct, const int32_t* __restrict__ tile_off,
+    int32_t* __restrict__ slot_of, int32_t* __restrict__ token_of_slot, T* __restrict__ xbuf) {
+  __shared__ uint32_t masks[MOE_MAX_E][MOE_ROUTE_TILE / 32];
+  __shared__ int32_t srow[MOE_ROUTE_TILE * MOE_MAX_K];  // destination row or -1
+  const int tile = blockIdx.x;
+  const int t0 = tile * MOE_ROUTE_TILE;
+  for (int i = threadIdx.x; i < n * (MOE_ROUTE_TILE / 32); i += blockDim.x)
+    (&masks[0][0])[i] = 0u;
+  __syncthreads();
+  const int lt = threadIdx.x;  // local token (threads 0..127)
+  const int t = t0 + lt;
+  int ev[MOE_MAX_K];
+  if (lt < MOE_ROUTE_TILE && t < Tn) {
+    for (int r = 0; r < k; ++r) {
+      ev[r] = idx[(size_t)t * k + r];
+      atomicOr(&masks[ev[r]][lt >> 5], 1u << (lt & 31));
+    }
+  }
+  __syncthreads();
+  if (lt < MOE_ROUTE_TILE) {
+    for (int r = 0; r < k; ++r) {
+      int row = -1;
+      if (t < Tn) {
+        const int e = ev[r];
+        int rank = __popc(masks[e][lt >> 5] & ((1u << (lt & 31)) - 1u));
+        for (int q = 0; q < (lt >> 5); ++q) rank += __popc(masks[e][q]);
+        const int slot = tile_off[(size_t)tile * n + e] + rank;
+        const bool keep = slot < ct.cap[e];
+        slot_of[(size_t)t * k + r] = keep ? slot : -1;
+        if (keep) {
+          row = ct.base[e] + slot;
+          token_of_slot[row] = (int32_t)((token_base + t) * k + r);
+        }
+      }
+      srow[lt * k + r] = row;
+    }
+  }
+  __syncthreads();
+  // row copies: warp per token
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int VE = Vec<T>::N;
+  const int nvec = d / VE;
+  for (int lt2 = wid; lt2 < MOE_ROUTE_TILE; lt2 += 8) {
+    const int tt = t0 + lt2;
+    if (tt >= Tn) break;
+    int rows[MOE_MAX_K];
+    int nk = 0;
+    for (int r = 0; r < k; ++r) {
+      int rw = srow[lt2 * k + r];
+      if (rw >= 0) rows[nk++] = rw;
+    }
+    if (nk == 0) continue;
+    const T* src = x + (size_t)tt * d;
+    for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
+      uint4 buf[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int v = v0 + u * 32 + lane;
+        if (v < nvec) buf[u] = ld_nc_v4(src + (size_t)v * VE);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int v = v0 + u * 32 + lane;
+        if (v < nvec)
+          for (int q = 0; q < nk; ++q) st_v4(xbuf + (size_t)rows[q] * d + (size_t)v * VE, buf[u]);
+      }
+    }
+  }
+}
+
+cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T, int k,
+                            int n, int d, int64_t token_base, const CapTable& ct,
+                            RouteBufs b, void* xbuf, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  int ntiles = (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE;
+  if (dtype == 1)
+    dispatch_kernel<__nv_bfloat16><<<ntiles, 256, 0, s>>>(
+        idx, (const __nv_bfloat16*)x, T, k, n, d, token_base, ct, b.tile_off, b.slot_of,
+        b.token_of_slot, (__nv_bfloat16*)xbuf);
+  else
+    dispatch_kernel<float><<<ntiles, 256, 0, s>>>(idx, (const float*)x, T, k, n, d,
+                                                  token_base, ct, b.tile_off, b.slot_of,
+                                                  b.token_of_slot, (float*)xbuf);
+  return cudaGetLastError();
+}
+
+// Zero rows [kept_e, min(roundup(kept_e, PAD), region end)) of each local expert region so
+// the token-contraction (weight-gradient) GEMMs can read whole K-blocks.
+template <typename T>
+__global__ void zero_pad_kernel(T* __restrict__ buf, int cols, const int32_t* __restrict__ kept,
+                                CapTable ct) {
+  const int e = blockIdx.x;
+  const int kp = kept[e];
+  const int r0 = ct.base[e] + kp;
+  const int r1 = min(ct.base[e] + ((kp + MOE_PAD_ROWS - 1) / MOE_PAD_ROWS) * MOE_PAD_ROWS,
+                     ct.base[e + 1]);
+  constexpr int VE = Vec<T>::N;
+  const int nvec = cols / VE;
+  const size_t total = (size_t)(r1 - r0) * nvec;
+  for (size_t i = threadIdx.x; i < total; i += blockDim.x)
+    st_v4(buf + (size_t)r0 * cols + i * VE, make_uint4(0, 0, 0, 0));
+}
+
+cudaError_t launch_zero_pad(int dtype, void* buf, int cols, const int32_t* kept, int n,
+                            const CapTable& ct, cudaStream_t s) {
+  if (dtype == 1)
+    zero_pad_kernel<__nv_bfloat16><<<n, 256, 0, s>>>((__nv_bfloat16*)buf, cols, kept, ct);
+  else
+    zero_pad_kernel<float><<<n, 256, 0, s>>>((float*)buf, cols, kept, ct);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K5: combine (Alg. 1 l.8, Aggregate P:408): y[t] = sum_r [kept] w[t,r] O[row(t,r)],
+// r ascending, fp32 accumulate; warp per token, 16-byte vectors.
+// =====================================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) combine_fwd_kernel(
+    const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
+    const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
+    T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= Tn) return;
+  int rows[MOE_MAX_K];
+  float wr[MOE_MAX_K];
+  int nk = 0;
+  for (int r = 0; r < k; ++r) {
+    int sl = slot_of[(size_t)t * k + r];
+    if (sl >= 0) {
+      rows[nk] = ct.base[idx[(size_t)t * k + r]] + sl;
+      wr[nk] = w[(size_t)t * k + r];
+      ++nk;
+    }
+  }
+  constexpr int VE = Vec<T>::N;
+  const int nvec = dout / VE;
+  T* yrow = y + (size_t)t * dout;
+  for (int v = lane; v < nvec; v += 32) {
+    float acc[VE];
+#pragma unroll
+    for (int i = 0; i < VE; ++i) acc[i] = 0.f;
+    for (int q = 0; q < nk; ++q) {
+      uint4 u = ld_nc_v4(obuf + (size_t)rows[q] * dout + (size_t)v * VE);
+      float o[VE];
+      unpack(u, o, T());
+#pragma unroll
+      for (int i = 0; i < VE; ++i) acc[i] = fmaf(wr[q], o[i], acc[i]);
+    }
+    st_v4(yrow + (size_t)v * VE, pack(acc, T()));
+  }
+}
+
+cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, int k,
+                               int d_out, const CapTable& ct, void* y, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  dim3 grid((T + 7) / 8);
+  if (dtype == 1)
+    combine_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        (const __nv_bfloat16*)obuf, b.w, b.idx, b.slot_of, ct, T, k, d_out, (__nv_bfloat16*)y);
+  else
+    combine_fwd_kernel<float><<<grid, 256, 0, s>>>((const float*)obuf, b.w, b.idx, b.slot_of,
+                                                   ct, T, k, d_out, (float*)y);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K6: combine backward.  dO[row] = w dy[t]; dw[t,r] = <dy[t], O[row]> (0 if dropped);
+// dl[t,:] closed form: renorm dl[i_r] = w_r (dw_r - sum w dw), 0 elsewhere;
+// raw dl_j = p_j (dp_j - sum_r w_r dw_r) with dp_j = dw_r at j = i_r.  Warp per token.
+// =====================================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) combine_bwd_kernel(
+    const T* __restrict__ dy, const T* __restrict__ obuf, const float* __restrict__ w,
+    const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of,
+    const float* __restrict__ logits, CapTable ct, int Tn, int k, int n, int dout, int renorm,
+    T* __restrict__ dobuf, float* __restrict__ dw, float* __restrict__ dl) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= Tn) return;
+  int rows[MOE_MAX_K];
+  float wr[MOE_MAX_K], part[MOE_MAX_K];
+  int er[MOE_MAX_K];
+  for (int r = 0; r < k; ++r) {
+    int sl = slot_of[(size_t)t * k + r];
+    er[r] = idx[(size_t)t * k + r];
+    rows[r] = sl >= 0 ? ct.base[er[r]] + sl : -1;
+    wr[r] = w[(size_t)t * k + r];
+    part[r] = 0.f;
+  }
+  constexpr int VE = Vec<T>::N;
+  const int nvec = dout / VE;
+  const T* dyrow = dy + (size_t)t * dout;
+  for (int v = lane; v < nvec; v += 32) {
+    float g[VE];
+    unpack(ld_nc_v4(dyrow + (size_t)v * VE), g, T());
+    for (int r = 0; r < k; ++r) {
+      if (rows[r] < 0) continue;
+      float o[VE], dov[VE];
+      unpack(ld_nc_v4(obuf + (size_t)rows[r] * dout + (size_t)v * VE), o, T());
+#pragma unroll
+      for (int i = 0; i < VE; ++i) {
+        part[r] = fmaf(g[i], o[i], part[r]);
+        dov[i] = wr[r] * g[i];
+      }
+      st_v4(dobuf + (size_t)rows[r] * dout + (size_t)v * VE, pack(dov, T()));
+    }
+  }
+  float dwr[MOE_MAX_K];
+  float c = 0.f;
+  for (int r = 0; r < k; ++r) {
+    float s = warp_sum(part[r]);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    dwr[r] = rows[r] >= 0 ? s : 0.f;
+    c = fmaf(wr[r], dwr[r], c);
+  }
+  if (lane < k) dw[(size_t)t * k + lane] = dwr[0 + lane];  // note: lane < k <= 8
+  float* dlrow = dl + (size_t)t * n;
+  if (renorm) {
+    for (int e = lane; e < n; e += 32) {
+      float v = 0.f;
+      for (int r = 0; r < k; ++r)
+        if (er[r] == e) v = wr[r] * (dwr[r] - c);
+      dlrow[e] = v;
+    }
+  } else {
+    const float* l = logits + (size_t)t * n;
+    float m = -INFINITY;
+    for (int e = lane; e < n; e += 32) m = fmaxf(m, l[e]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float sp = 0.f;
+    for (int e = lane; e < n; e += 32) sp += expf(l[e] - m);
+    sp = __shfl_sync(0xffffffffu, warp_sum(sp), 0);
+    for (int e = lane; e < n; e += 32) {
+      float p = expf(l[e] - m) / sp;
+      float dp = 0.f;
+      for (int r = 0; r < k; ++r)
+        if (er[r] == e) dp = dwr[r];
+      dlrow[e] = p * (dp - c);
+    }
+  }
+}
+
+cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, RouteBufs b,
+                               int T, int k, int n, int d_out, int renorm,
+                               const CapTable& ct, void* dobuf, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  dim3 grid((T + 7) / 8);
+  if (dtype == 1)
+    combine_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)obuf, b.w, b.idx, b.slot_of, b.logits,
+        ct, T, k, n, d_out, renorm, (__nv_bfloat16*)dobuf, b.dw, b.dl);
+  else
+    combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dy, (const float*)obuf, b.w,
+                                                   b.idx, b.slot_of, b.logits, ct, T, k, n,
+                                                   d_out, renorm, (float*)dobuf, b.dw, b.dl);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K9: dispatch backward with the gate input-gradient fused in:
+//   dx[t] = sum_r [kept] dX[row(t,r)] + sum_e dl[t,e] W_g[e,:]     (fp32 accumulate)
+// CTA = 32 tokens x 128 columns; W_g / dl chunks staged in shared memory.
+// =====================================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) gate_dx_kernel(
+    const float* __restrict__ dl, const T* __restrict__ wg, const T* __restrict__ dxbuf,
+    const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of, CapTable ct, int Tn,
+    int k, int n, int d, T* __restrict__ dx, int accumulate) {
+  __shared__ float dls[32][33];
+  __shared__ float wgs[32][128];
+  const int tid = threadIdx.x;
+  const int c = tid & 31, tg = tid >> 5;
+  const int t0 = blockIdx.y * 32, c0 = blockIdx.x * 128;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int e0 = 0; e0 < n; e0 += 32) {
+    for (int i = tid; i < 32 * 32; i += 256) {
+      int tt = i / 32, ee = i % 32;
+      int t = t0 + tt, e = e0 + ee;
+      dls[tt][ee] = (t < Tn && e < n) ? dl[(size_t)t * n + e] : 0.f;
+    }
+    for (int i = tid; i < 32 * 128; i += 256) {
+      int ee = i / 128, cc = i % 128;
+      int e = e0 + ee, col = c0 + cc;
+      wgs[ee][cc] = (e < n && col < d) ? to_f(wg[(size_t)e * d + col]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int ee = 0; ee < 32; ++ee) {
+      float wv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) wv[j] = wgs[ee][c + 32 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float lv = dls[tg + 8 * i][ee];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(lv, wv[j], acc[i][j]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = t0 + tg + 8 * i;
+    if (t >= Tn) continue;
+    float out[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) out[j] = 0.f;
+    // expert-path contribution first (r order), then the gate term: fixed order
+    for (int r = 0; r < k; ++r) {
+      int sl = slot_of[(size_t)t * k + r];
+      if (sl < 0) continue;
+      const T* src = dxbuf + (size_t)(ct.base[idx[(size_t)t * k + r]] + sl) * d;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int col = c0 + c + 32 * j;
+        if (col < d) out[j] += to_f(src[col]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int col = c0 + c + 32 * j;
+      if (col >= d) continue;
+      float v = out[j] + acc[i][j];
+      if (accumulate) v += to_f(dx[(size_t)t * d + col]);
+      dx[(size_t)t * d + col] = from_f<T>(v);
+    }
+  }
+}
+
+cudaError_t launch_gate_dx(int dtype, const void* wg, const void* dxbuf, RouteBufs b, int T,
+                           int k, int n, int d, const CapTable& ct, void* dx, int accumulate,
+                           cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  dim3 grid((d + 127) / 128, (T + 31) / 32);
+  if (dtype == 1)
+    gate_dx_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        b.dl, (const __nv_bfloat16*)wg, (const __nv_bfloat16*)dxbuf, b.idx, b.slot_of, ct, T, k,
+        n, d, (__nv_bfloat16*)dx, accumulate);
+  else
+    gate_dx_kernel<float><<<grid, 256, 0, s>>>(b.dl, (const float*)wg, (const float*)dxbuf,
+                                               b.idx, b.slot_of, ct, T, k, n, d, (float*)dx,
+                                               accumulate);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K10: gate weight gradient dW_g = dl^T x, deterministic split-K over tokens:
+// partial[s][e][c] over token range s, then a fixed-order reduction over s.
+// CTA = 64 columns x all n experts; thread = 1 column x n/4 experts.
+// =====================================================================================
+template <typename T, int NJ>
+__global__ void __launch_bounds__(256) gate_dw_kernel(const float* __restrict__ dl,
+                                                      const T* __restrict__ x, int Tn, int n,
+                                                      int d, int chunk,
+                                                      float* __restrict__ partial) {
+  extern __shared__ float sm[];
+  float* xs = sm;                 // [32][64]
+  float* ls = sm + 32 * 64;       // [32][n]
+  const int tid = threadIdx.x;
+  const int col = tid & 63, eg = tid >> 6;
+  const int c0 = blockIdx.x * 64;
+  const int ts = blockIdx.y * chunk, te = min(Tn, ts + chunk);
+  float acc[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) acc[j] = 0.f;
+  for (int t0 = ts; t0 < te; t0 += 32) {
+    for (int i = tid; i < 32 * 64; i += 256) {
+      int tt = i / 64, cc = i % 64;
+      int t = t0 + tt, cl = c0 + cc;
+      xs[i] = (t < te && cl < d) ? to_f(x[(size_t)t * d + cl]) : 0.f;
+    }
+    for (int i = tid; i < 32 * n; i += 256) {
+      int tt = i / n, e = i % n;
+      int t = t0 + tt;
+      ls[i] = (t < te) ? dl[(size_t)t * n + e] : 0.f;
+    }
+    __syncthreads();
+    for (int tt = 0; tt < 32; ++tt) {
+      float xv = xs[tt * 64 + col];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        int e = eg + 4 * j;
+        if (e < n) acc[j] = fmaf(ls[tt * n + e], xv, acc[j]);
+      }
+    }
+    __syncthreads();
+  }
+  const int cl = c0 + col;
+  if (cl < d) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      int e = eg + 4 * j;
+      if (e < n) partial[((size_t)blockIdx.y * n + e) * d + cl] = acc[j];
+    }
+  }
+}
+
+template <typename T>
+__global__ void reduce_partials_kernel(const float* __restrict__ partial, int splits,
+                                       size_t count, T* __restrict__ out, int accumulate) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  float s = 0.f;
+  for (int q = 0; q < splits; ++q) s += partial[(size_t)q * count + i];
+  if (accumulate) s += to_f(out[i]);
+  out[i] = from_f<T>(s);
+}
+
+int gate_dw_splits(int T, int d) {
+  int ctiles = (d + 63) / 64;
+  int want = (2 * 148 + ctiles - 1) / ctiles;
+  int maxs = (T + 255) / 256;
+  return max(1, min(want, maxs));
+}
+
+cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int n, int d,
+                           float* partial, int splits, void* dwg, int accumulate,
+                           cudaStream_t s) {
+  size_t count = (size_t)n * d;
+  if (T == 0) {
+    if (!accumulate) return cudaMemsetAsync(dwg, 0, count * (dtype == 1 ? 2 : 4), s);
+    return cudaSuccess;
+  }
+  int chunk = (T + splits - 1) / splits;
+  chunk = ((chunk + 31) / 32) * 32;
+  splits = (T + chunk - 1) / chunk;
+  dim3 grid((d + 63) / 64, splits);
+  size_t smem = (size_t)(32 * 64 + 32 * n) * 4;
+#define GDW_CASE(NJ)                                                                        \
+  if (n <= 4 * NJ) {                                                                        \
+    if (dtype == 1) {                                                                       \
+      auto kf = gate_dw_kernel<__nv_bfloat16, NJ>;                                          \
+      cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+      kf<<<grid, 256, smem, s>>>(dl, (const __nv_bfloat16*)x, T, n, d, chunk, partial);     \
+    } else {                                                                                \
+      auto kf = gate_dw_kernel<float, NJ>;                                                  \
+      cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+      kf<<<grid, 256, smem, s>>>(dl, (const float*)x, T, n, d, chunk, partial);             \
+    }                                                                                       \
+  } else
+  GDW_CASE(2) GDW_CASE(4) GDW_CASE(8) GDW_CASE(16) GDW_CASE(32) GDW_CASE(64) {
+    return cudaErrorInvalidValue;
+  }
+#undef GDW_CASE
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  int rb = (int)((count + 255) / 256);
+  if (dtype == 1)
+    reduce_partials_kernel<__nv_bfloat16><<<rb, 256, 0, s>>>(partial, splits, count,
+                                                             (__nv_bfloat16*)dwg, accumulate);
+  else
+    reduce_partials_kernel<float><<<rb, 256, 0, s>>>(partial, splits, count, (float*)dwg,
+                                                     accumulate);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// Bias gradients (SIMT path): db[e][j] = sum_{s < kept_e} buf[base_e + s][j], sequential
+// over rows (deterministic), thread per column.
+// =====================================================================================
+template <typename T>
+__global__ void colsum_kernel(const T* __restrict__ buf, int cols,
+                              const int32_t* __restrict__ kept, CapTable ct,
+                              T* __restrict__ out, int accumulate) {
+  const int e = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  const int m = kept[e];
+  const T* p = buf + (size_t)ct.base[e] * cols + j;
+  float s = 0.f;
+  for (int r = 0; r < m; ++r) s += to_f(p[(size_t)r * cols]);
+  if (accumulate) s += to_f(out[(size_t)e * cols + j]);
+  out[(size_t)e * cols + j] = from_f<T>(s);
+}
+
+cudaError_t launch_colsum(int dtype, const void* buf, int cols, const int32_t* kept, int n,
+                          const CapTable& ct, void* out, int accumulate, cudaStream_t s) {
+  dim3 grid((cols + 255) / 256, n);
+  if (dtype == 1)
+    colsum_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)buf, cols, kept,
+                                                      ct, (__nv_bfloat16*)out, accumulate);
+  else
+    colsum_kernel<float><<<grid, 256, 0, s>>>((const float*)buf, cols, kept, ct, (float*)out,
+                                              accumulate);
+  return cudaGetLastError();
+}
+
+}  // namespace moe

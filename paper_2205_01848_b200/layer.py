@@ -1,0 +1,290 @@
+"""Thin PyTorch binding of the C ABI (include/moe.h): argument marshalling only.
+
+Torch supplies device memory (the workspace and outputs), the current CUDA stream and
+process groups; every step of the MoE hot path runs in libdynamoe_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib as L
+
+_TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def capacity_from_factors(alphas, tokens_global: int, k: int):
+    """Eq. 4 through the library: max(1, ceil(alpha_e * T_g * k / n))."""
+    lib = L.load()
+    n = len(alphas)
+    a = (C.c_double * n)(*[float(v) for v in alphas])
+    out = (C.c_int32 * n)()
+    L.check(lib.moe_capacity_from_factors(n, int(tokens_global), int(k), a, out))
+    return list(out)
+
+
+class MoELayer:
+    """One DynaMoE MoE layer (Alg. 1 with capacity) on one GPU
+    (or one expert-parallel rank).  Parameters are passed per call (torch Linear layout)."""
+
+    def __init__(self, n_experts: int, top_k: int, d_model: int, d_ff: int, d_out: int = 0,
+                 max_tokens: int = 4096, dtype: str = "bf16", renormalize: int = 1,
+                 world_size: int = 1, rank: int = 0, nccl_comm: int = 0, device=None):
+        self.lib = L.load()
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.type != "cuda":
+            raise RuntimeError("MoELayer runs only on CUDA devices (no CPU fallback)")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        self.n, self.k, self.d, self.f = n_experts, top_k, d_model, d_ff
+        self.d_out = d_out or d_model
+        self.max_tokens = max_tokens
+        self.dtype = dtype
+        self.tdtype = _TORCH_DT[dtype]
+        self.world_size, self.rank = world_size, rank
+        cfg = L.MoEConfig(n_experts, top_k, d_model, d_ff, d_out, max_tokens, L.DTYPES[dtype],
+                          int(renormalize), world_size, rank, C.c_void_p(nccl_comm),
+                          C.c_void_p(self._stream()))
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            L.check(self.lib.moe_init(C.byref(cfg), C.byref(h)), None, "moe_init")
+        self.h = h
+        self.ws = None
+        self._cached_ref = None
+        self._alloc_workspace()
+        self._pinned = None
+
+    # -- plumbing -------------------------------------------------------------------
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _sync_stream(self):
+        L.check(self.lib.moe_set_stream(self.h, C.c_void_p(self._stream())), self.h)
+
+    def _alloc_workspace(self):
+        sz = C.c_size_t()
+        L.check(self.lib.moe_workspace_size(self.h, C.byref(sz)), self.h)
+        if self.ws is None or self.ws.numel() < sz.value:
+            self.ws = torch.empty(max(sz.value, 256), dtype=torch.uint8, device=self.device)
+        self._sync_stream()
+        L.check(self.lib.moe_set_workspace(self.h, _ptr(self.ws), self.ws.numel()), self.h,
+                "moe_set_workspace")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.moe_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- recompile-enabled optimisations ----------------------------------------------
+    @property
+    def capacities(self):
+        out = (C.c_int32 * self.n)()
+        L.check(self.lib.moe_get_capacities(self.h, out), self.h)
+        return list(out)
+
+    def set_capacities(self, caps):
+        """Dynamic capacity factors (S4.1): new per-expert capacities, stream-ordered."""
+        arr = (C.c_int32 * self.n)(*[int(c) for c in caps])
+        st = self.lib.moe_set_capacities(self.h, arr)
+        if st == L.MOE_ERR_WORKSPACE_TOO_SMALL:
+            self._alloc_workspace()
+            return
+        L.check(st, self.h, "moe_set_capacities")
+        self._sync_stream()
+
+    def set_capacity_factors(self, alphas, tokens_global=None):
+        tg = tokens_global if tokens_global is not None else self.max_tokens * self.world_size
+        self.set_capacities(capacity_from_factors(alphas, tg, self.k))
+
+    def set_cached_assignment(self, idx):
+        """Sample-assignment caching (S4.2): int32 [T,k] device indices, or None (off)."""
+        if idx is not None:
+            if idx.dtype != torch.int32 or not idx.is_cuda or not idx.is_contiguous():
+                raise ValueError("cached indices must be a contiguous int32 CUDA tensor")
+        self._cached_ref = idx
+        L.check(self.lib.moe_set_cached_assignment(self.h, _ptr(idx)), self.h)
+
+    # -- hot path -------------------------------------------------------------------
+    def _check(self, t, shape, name):
+        if t.dtype != self.tdtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous() \
+                or t.device != self.device:
+            raise ValueError(f"{name}: expected contiguous {self.tdtype} {tuple(shape)} on "
+                             f"{self.device}, got {t.dtype} {tuple(t.shape)} on {t.device}")
+
+    def forward(self, x, w_gate, w1, b1, w2, b2, y=None):
+        T = x.shape[0]
+        n, d, f, do = self.n, self.d, self.f, self.d_out
+        self._check(x, (T, d), "x")
+        self._check(w_gate, (n, d), "w_gate")
+        self._check(w1, (n, f, d), "w1")
+        self._check(b1, (n, f), "b1")
+        self._check(w2, (n, do, f), "w2")
+        self._check(b2, (n, do), "b2")
+        if y is None:
+            y = torch.empty(T, do, dtype=self.tdtype, device=self.device)
+        self._sync_stream()
+        a = L.FwdArgs(T, _ptr(x), _ptr(w_gate), _ptr(w1), _ptr(b1), _ptr(w2), _ptr(b2), _ptr(y))
+        L.check(self.lib.moe_forward(self.h, C.byref(a)), self.h, "moe_forward")
+        self._saved = (x, w_gate, w1, b1, w2, b2)   # keep alive until backward (moe.h)
+        return y
+
+    def backward(self, dy, grads=None, accumulate=False, need=("dx", "dw_gate", "dw1", "db1",
+                                                               "dw2", "db2")):
+        x, w_gate, w1, b1, w2, b2 = self._saved
+        T = x.shape[0]
+        self._check(dy, (T, self.d_out), "dy")
+        if grads is None:
+            alloc = torch.zeros if accumulate else torch.empty
+            shapes = dict(dx=x.shape, dw_gate=w_gate.shape, dw1=w1.shape, db1=b1.shape,
+                          dw2=w2.shape, db2=b2.shape)
+            grads = {k: alloc(shapes[k], dtype=self.tdtype, device=self.device) for k in need}
+        g = lambda k: _ptr(grads.get(k))  # noqa: E731
+        self._sync_stream()
+        a = L.BwdArgs(_ptr(dy), g("dx"), g("dw_gate"), g("dw1"), g("db1"), g("dw2"), g("db2"),
+                      int(bool(accumulate)))
+        L.check(self.lib.moe_backward(self.h, C.byref(a)), self.h, "moe_backward")
+        self._saved = None
+        return grads
+
+    # -- introspection ----------------------------------------------------------------
+    def routing(self, T):
+        """Copies of the last forward's routing tables (device tensors)."""
+        r = L.Routing()
+        L.check(self.lib.moe_get_routing(self.h, C.byref(r)), self.h)
+        base = self.ws.data_ptr()
+
+        def view(ptr, count, dt):
+            off = ptr - base
+            nbytes = count * torch.tensor([], dtype=dt).element_size()
+            return self.ws[off:off + nbytes].view(dt).clone()
+
+        n, k = self.n, self.k
+        out = dict(
+            logits=view(r.logits, T * n, torch.float32).view(T, n),
+            w=view(r.weights, T * k, torch.float32).view(T, k),
+            idx=view(r.idx, T * k, torch.int32).view(T, k),
+            fresh_idx=view(r.fresh_idx, T * k, torch.int32).view(T, k),
+            slot_of=view(r.slot_of, T * k, torch.int32).view(T, k),
+            counts=view(r.counts, n, torch.int32),
+            kept=view(r.kept, n, torch.int32),
+            dl=view(r.dl, T * n, torch.float32).view(T, n),
+            dw=view(r.dw, T * k, torch.float32).view(T, k),
+            token_of_slot=view(r.token_of_slot, r.rows, torch.int32),
+            rows=r.rows,
+            base=list(r.base_host)[: n // self.world_size + 1],
+        )
+        out["x_buf"] = view(r.x_buf, r.rows * self.d, self.tdtype).view(r.rows, self.d)
+        out["h_buf"] = view(r.h_buf, r.rows * self.f, self.tdtype).view(r.rows, self.f)
+        out["o_buf"] = view(r.o_buf, r.rows * self.d_out, self.tdtype).view(r.rows, self.d_out)
+        return out
+
+    def stats(self):
+        """Per-forward statistics (synchronises the stream): counts, drops, hit_count."""
+        if self._pinned is None:
+            self._pinned = (torch.zeros(self.n, dtype=torch.int32).pin_memory(),
+                            torch.zeros(1, dtype=torch.int64).pin_memory(),
+                            torch.zeros(1, dtype=torch.int32).pin_memory())
+        c, dr, hit = self._pinned
+        self._sync_stream()
+        s = L.Stats(_ptr(c), _ptr(dr), _ptr(hit))
+        L.check(self.lib.moe_get_stats_async(self.h, C.byref(s)), self.h)
+        torch.cuda.current_stream(self.device).synchronize()
+        return dict(counts=c.tolist(), drops=int(dr.item()), hit_count=int(hit.item()))
+
+    def check_flags(self):
+        fl = C.c_int32()
+        self._sync_stream()
+        st = self.lib.moe_check_device_flags(self.h, C.byref(fl))
+        return st, fl.value
+
+    def profile(self, on: bool):
+        L.check(self.lib.moe_profile_enable(self.h, int(bool(on))), self.h)
+
+    def profile_read(self, reset=True):
+        """{kernel name: (launches, total_ms)} since the last reset (synchronises)."""
+        buf = (L.KernelTime * 64)()
+        cnt = C.c_int32()
+        L.check(self.lib.moe_profile_read(self.h, buf, 64, C.byref(cnt), int(reset)), self.h)
+        return {buf[i].name.decode(): (buf[i].launches, buf[i].total_ms) for i in range(cnt.value)}
+
+    def launch_count(self):
+        v = C.c_int64()
+        L.check(self.lib.moe_launch_count(self.h, C.byref(v)), self.h)
+        return v.value
+
+
+class CapacityPolicy:
+    """Host helper of the dynamic capacity policy in the library (moe_policy_*)."""
+
+    def __init__(self, n, tokens_global, k, capacities, window=20, headroom=0.15,
+                 shrink_util=0.5, min_alpha=0.25, max_alpha=8.0):
+        self.lib = L.load()
+        self.n = n
+        cfg = L.PolicyConfig(n, k, tokens_global, window, headroom, shrink_util, min_alpha,
+                             max_alpha)
+        init = (C.c_int32 * n)(*[int(c) for c in capacities])
+        p = C.c_void_p()
+        L.check(self.lib.moe_policy_create(C.byref(cfg), init, C.byref(p)))
+        self.p = p
+
+    def update(self, counts):
+        cin = (C.c_int32 * self.n)(*[int(c) for c in counts])
+        cout = (C.c_int32 * self.n)()
+        ch = C.c_int32()
+        L.check(self.lib.moe_policy_update(self.p, cin, cout, C.byref(ch)))
+        return list(cout) if ch.value else None
+
+    def __del__(self):
+        try:
+            self.lib.moe_policy_destroy(self.p)
+        except Exception:
+            pass
+
+
+class MoEFunction(torch.autograd.Function):
+    """autograd wrapper: y = MoE(x; W_g, W1, b1, W2, b2) through the C ABI."""
+
+    @staticmethod
+    def forward(ctx, layer, x, w_gate, w1, b1, w2, b2):
+        ctx.layer = layer
+        return layer.forward(x, w_gate, w1, b1, w2, b2)
+
+    @staticmethod
+    def backward(ctx, dy):
+        g = ctx.layer.backward(dy.contiguous())
+        return None, g["dx"], g["dw_gate"], g["dw1"], g["db1"], g["dw2"], g["db2"]
+
+
+class DynaMoE(torch.nn.Module):
+    """nn.Module holding the gate and expert parameters (torch Linear layout)."""
+
+    def __init__(self, n_experts, top_k, d_model, d_ff, d_out=0, max_tokens=4096,
+                 dtype="bf16", renormalize=1, device=None):
+        super().__init__()
+        self.layer = MoELayer(n_experts, top_k, d_model, d_ff, d_out, max_tokens, dtype,
+                              renormalize, device=device)
+        dev, dt = self.layer.device, self.layer.tdtype
+        do = d_out or d_model
+        self.w_gate = torch.nn.Parameter(torch.randn(n_experts, d_model, device=dev) * d_model ** -0.5)
+        self.w1 = torch.nn.Parameter(torch.randn(n_experts, d_ff, d_model, device=dev) * d_model ** -0.5)
+        self.b1 = torch.nn.Parameter(torch.zeros(n_experts, d_ff, device=dev))
+        self.w2 = torch.nn.Parameter(torch.randn(n_experts, do, d_ff, device=dev) * d_ff ** -0.5)
+        self.b2 = torch.nn.Parameter(torch.zeros(n_experts, do, device=dev))
+        for p in self.parameters():
+            p.data = p.data.to(dt)
+
+    def forward(self, x):
+        return MoEFunction.apply(self.layer, x.contiguous(), self.w_gate, self.w1, self.b1,
+                                 self.w2, self.b2)
