@@ -1,17 +1,588 @@
-// gemm_tc.cu -- tcgen05 grouped GEMMs (placeholder until the tcgen05 kernels land).
+// gemm_tc.cu -- tcgen05 / TMEM / TMA grouped GEMMs of the expert FFN (bf16 in, fp32 accum).
+//
+// The expert FFN (Alg. 1 l.7; reading 9) is the dense contraction of the hot path, so
+// it runs on the 5th-generation tensor cores.  One persistent, warp-specialised kernel
+// template covers all six GEMMs of forward + backward:
+//
+//   kind        C (per local expert e)                         A major   B major   M rows
+//   FWD1        H  = relu(X W1_e^T + b1_e)                      K         K         kept_e
+//   FWD2        O  = H W2_e^T + b2_e                             K         K         kept_e
+//   DGRAD_A     dA = (dO W2_e) * 1[H > 0]   (written over H)     K         MN        kept_e
+//   DGRAD_X     dX = dA W1_e                                     K         MN        kept_e
+//   WGRAD       dW = A^T B over kept_e tokens (dW2 = dO^T H,     MN        MN        d_out / f
+//               dW1 = dA^T X)
+//
+// M-grouped GEMMs run over exactly kept_e rows per expert (no capacity-padding FLOPs, the
+// waste P:234 and P:370 point at); weight gradients contract over exactly the kept tokens
+// (K rounded up to 64 with zero rows).
+//
+// Roles (256 threads): warp 0 = TMA producer (one lane), warp 1 = MMA issuer (one lane),
+// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM lanes 0..127).  Shared-memory ring of
+// STAGES {A 128x64, B BNx64} bf16 tiles (128B swizzle), mbarrier full/empty pairs; two TMEM
+// accumulators of BN fp32 columns so the epilogue of tile i overlaps the MMAs of tile i+1.
+// Tile schedule: static persistent (tile = blockIdx.x + i*gridDim.x), identical in all roles.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
 #include "gemm_tc.h"
+#include "kernels.h"
+#include "prof.h"
 
 namespace moe {
+
+enum TcKind { TC_FWD1 = 0, TC_FWD2 = 1, TC_DGRAD_A = 2, TC_DGRAD_X = 3, TC_WGRAD = 4 };
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 64;
+constexpr int TC_THREADS = 256;
+
+struct TcParams {
+  const int32_t* kept;          // [n_local] M_e (M-grouped) or K_e (WGRAD)
+  const int32_t* mtile_prefix;  // [n_local+1] prefix of ceil(kept/128) (M-grouped)
+  int n_local;
+  int M, N, K;                  // WGRAD: M, N output dims; M-grouped: N cols, K depth
+  const __nv_bfloat16* bias;    // FWD1/FWD2 bias [n_local, N]
+  __nv_bfloat16* C;             // output base (buffer or weight-gradient tensor)
+  int ldc;                      // leading dim of C (M-grouped buffers)
+  int accumulate;               // WGRAD
+  CapTable ct;                  // base rows of each local expert region
+};
+
+// ------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t addr = smem_u32(b);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), Blackwell version 1.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, M=128, N=BN
+__host__ __device__ constexpr uint32_t make_idesc(int n, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+}
+
+template <int KIND>
+struct KindTraits {
+  static constexpr bool kgroup = (KIND == TC_WGRAD);
+  static constexpr int a_mn = (KIND == TC_WGRAD) ? 1 : 0;
+  static constexpr int b_mn = (KIND == TC_DGRAD_A || KIND == TC_DGRAD_X || KIND == TC_WGRAD) ? 1 : 0;
+};
+
+// Decode a linear tile index into (expert, m0, n0).
+template <bool KG>
+__device__ __forceinline__ bool decode_tile(int t, const int32_t* s_prefix, int n_local, int MT,
+                                            int NT, int& e, int& mt, int& nt) {
+  if (KG) {
+    int per = MT * NT;
+    e = t / per;
+    if (e >= n_local) return false;
+    int r = t - e * per;
+    nt = r / MT;
+    mt = r - nt * MT;
+    return true;
+  } else {
+    // s_prefix[j] = sum_{e<j} mtiles(e); tiles of expert e: [prefix[e]*NT, prefix[e+1]*NT)
+    int total = s_prefix[n_local] * NT;
+    if (t >= total) return false;
+    int lo = 0, hi = n_local - 1;
+    while (lo < hi) {  // largest e with prefix[e]*NT <= t
+      int mid = (lo + hi + 1) >> 1;
+      if (s_prefix[mid] * NT <= t) lo = mid; else hi = mid - 1;
+    }
+    e = lo;
+    int r = t - s_prefix[e] * NT;
+    int mte = s_prefix[e + 1] - s_prefix[e];
+    nt = r / mte;
+    mt = r - nt * mte;
+    return true;
+  }
+}
+
+template <int KIND, int BN, int STAGES>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   TcParams p) {
+  using Tr = KindTraits<KIND>;
+  constexpr int A_BYTES = TC_BM * TC_BK * 2;
+  constexpr int B_BYTES = BN * TC_BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t IDESC = make_idesc(BN, Tr::a_mn, Tr::b_mn);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int32_t* s_prefix = reinterpret_cast<int32_t*>(s_tmem + 4);   // [n_local + 1]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_local = p.n_local;
+  for (int i = threadIdx.x; i <= n_local; i += blockDim.x)
+    s_prefix[i] = Tr::kgroup ? 0 : p.mtile_prefix[i];
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(s_tmem)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *s_tmem;
+
+  const int NT = (p.N + BN - 1) / BN;
+  const int MT = Tr::kgroup ? (p.M + TC_BM - 1) / TC_BM : 0;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ============================ TMA producer ============================
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x;; t += gridDim.x) {
+        int e, mt, nt;
+        if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+        const int m0 = mt * TC_BM, n0 = nt * BN;
+        const int base = p.ct.base[e];
+        const int nk = Tr::kgroup ? (p.kept[e] + TC_BK - 1) / TC_BK : p.K / TC_BK;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+          const int k0 = kb * TC_BK;
+          if (Tr::a_mn) {  // A^T tiles: {64 M, 64 K} boxes
+            tma_load_2d(sa, &tmA, &full_bar[stage], m0, base + k0);
+            tma_load_2d(sa + 8192, &tmA, &full_bar[stage], m0 + 64, base + k0);
+          } else {         // A K-major: {64 K, 128 rows}
+            tma_load_2d(sa, &tmA, &full_bar[stage], k0, base + m0);
+          }
+          if (Tr::b_mn) {
+            if (Tr::kgroup) {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage], n0 + j * 64, base + k0);
+            } else {  // weight [K x N] of expert e: rows e*K + k
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage], n0 + j * 64, e * p.K + k0);
+            }
+          } else {  // weight [N x K] of expert e: rows e*N + n
+            tma_load_2d(sb, &tmB, &full_bar[stage], k0, e * p.N + n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ============================ MMA issuer ============================
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x;; t += gridDim.x, ++it) {
+        int e, mt, nt;
+        if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+        const int acc = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        const int nk = Tr::kgroup ? (p.kept[e] + TC_BK - 1) / TC_BK : p.K / TC_BK;
+        mbar_wait(&tempty_bar[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            uint64_t da = Tr::a_mn ? umma_desc(sa + k * 2048, 8192, 1024)
+                                   : umma_desc(sa + k * 32, 16, 1024);
+            uint64_t db = Tr::b_mn ? umma_desc(sb + k * 2048, 8192, 1024)
+                                   : umma_desc(sb + k * 32, 16, 1024);
+            tc_mma(tmem_d, da, db, IDESC, (kb | k) != 0);
+          }
+          tc_commit(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull_bar[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ============================ epilogue ============================
+    const int q = warp & 3;          // TMEM lane quarter
+    const int row_in_tile = q * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x;; t += gridDim.x, ++it) {
+      int e, mt, nt;
+      if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+      const int acc = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tfull_bar[acc], aphase);
+      tc_fence_after();
+      const int m0 = mt * TC_BM, n0 = nt * BN;
+      const int row = m0 + row_in_tile;
+      const bool zero_acc = Tr::kgroup && p.kept[e] == 0;
+      const int Me = Tr::kgroup ? p.M : p.kept[e];
+      const bool row_ok = row < Me;
+      __nv_bfloat16* crow;
+      if (Tr::kgroup)
+        crow = p.C + ((size_t)e * p.M + row) * p.N;
+      else
+        crow = p.C + (size_t)(p.ct.base[e] + row) * p.ldc;
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col0 = n0 + c * 32;
+        uint32_t r[32];
+        if (!zero_acc) {
+          tmem_ld32(taddr + c * 32, r);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (col0 >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        bool store = true;
+        if (KIND == TC_FWD1 || KIND == TC_FWD2) {
+          if (row_ok) {
+            const __nv_bfloat16* bp = p.bias + (size_t)e * p.N + col0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              float bb[8];
+              unpack(ld_v4(bp + i), bb, __nv_bfloat16());
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float x = v[i + j] + bb[j];
+                v[i + j] = (KIND == TC_FWD1) ? (x > 0.f ? x : 0.f) : x;
+              }
+            }
+          } else {
+            store = (KIND == TC_FWD1);  // zero the padding rows of H (token-K GEMMs read them)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+        } else if (KIND == TC_DGRAD_A) {
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              float h[8];
+              unpack(ld_v4(crow + col0 + i), h, __nv_bfloat16());
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[i + j] = h[j] > 0.f ? v[i + j] : 0.f;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+        } else if (KIND == TC_DGRAD_X) {
+          store = row_ok;
+        } else {  // WGRAD
+          store = row_ok;
+          if (row_ok && p.accumulate) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              float o[8];
+              unpack(ld_v4(crow + col0 + i), o, __nv_bfloat16());
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[i + j] += o[j];
+            }
+          }
+        }
+        if (store) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) st_v4(crow + col0 + i, pack(v + i, __nv_bfloat16()));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(2 * BN));
+  }
+}
+
+// ------------------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static int g_num_sms = 0;
+
+static bool ensure_encode() {
+  if (g_encode) return true;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return false;
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  return true;
+}
+
+// 2-D bf16 tensor map over a row-major [outer x inner] matrix, 128-byte swizzle.
+static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                     uint32_t box_inner, uint32_t box_outer) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int KIND, int BN>
+static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p,
+                             cudaStream_t s) {
+  constexpr int STAGES = (BN == 256) ? 4 : 6;
+  constexpr int STAGE_BYTES = (TC_BM + BN) * TC_BK * 2;
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                      4 * (MOE_MAX_E + 1) + 64;
+  auto kf = tc_gemm_kernel<KIND, BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kf<<<g_num_sms, TC_THREADS, smem, s>>>(a, b, p);
+  return cudaGetLastError();
+}
+
+template <int KIND>
+static cudaError_t launch_tc_bn(int N, const CUtensorMap& a, const CUtensorMap& b,
+                                const TcParams& p, cudaStream_t s) {
+  if (N % 256 == 0) return launch_tc<KIND, 256>(a, b, p, s);
+  if (N % 128 == 0) return launch_tc<KIND, 128>(a, b, p, s);
+  return launch_tc<KIND, 64>(a, b, p, s);
+}
+
+static int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64); }
+
 void tc_plan_free(TcPlan* p) { (void)p; }
-moe_status_t tc_ffn_forward(TcPlan*, void*, const void*, const void*, const void*, const void*,
-                            void*, void*, int64_t, int, int, int, const int32_t*, const int32_t*,
-                            int, const CapTable&, int, cudaStream_t, int64_t*) {
-  return MOE_ERR_CONFIG;
+
+#define TC_TRY(expr)                                        \
+  do {                                                      \
+    if (!(expr)) return MOE_ERR_CUDA;                       \
+  } while (0)
+#define TC_CUDA(expr)                                       \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) {                                \
+      fprintf(stderr, "tcgen05: %s\n", cudaGetErrorString(_e)); \
+      return MOE_ERR_CUDA;                                  \
+    }                                                       \
+  } while (0)
+
+// M-grouped GEMM: C[base_e + m, :N] = epi(A[base_e + m, :K] . B_e), B_e [N x K] (K-major)
+// or [K x N] (MN-major, b_mn).
+template <int KIND>
+static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, int N,
+                           int n_local, const void* bias, void* C, int ldc, const int32_t* kept,
+                           const int32_t* prefix, const CapTable& ct, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  const int bn = pick_bn(N);
+  TC_TRY(make_map(&ma, A, K, rows, 64, 128));
+  if (KindTraits<KIND>::b_mn)
+    TC_TRY(make_map(&mb, B, N, (uint64_t)n_local * K, 64, 64));
+  else
+    TC_TRY(make_map(&mb, B, K, (uint64_t)n_local * N, 64, bn));
+  TcParams p{};
+  p.kept = kept; p.mtile_prefix = prefix; p.n_local = n_local; p.M = 0; p.N = N; p.K = K;
+  p.bias = (const __nv_bfloat16*)bias; p.C = (__nv_bfloat16*)C; p.ldc = ldc; p.ct = ct;
+  TC_CUDA(launch_tc_bn<KIND>(N, ma, mb, p, s));
+  return MOE_OK;
 }
-moe_status_t tc_ffn_backward(TcPlan*, void*, void*, void*, void*, const void*, const void*,
-                             void*, void*, void*, void*, int, int64_t, int, int, int,
-                             const int32_t*, const int32_t*, int, const CapTable&, int,
-                             cudaStream_t, int64_t*) {
-  return MOE_ERR_CONFIG;
+
+// WGRAD: Out_e[M x N] (+)= A_e^T B_e, A = Abuf[rows x M], B = Bbuf[rows x N] over kept_e rows.
+static moe_status_t wgrad(const void* Abuf, int M, const void* Bbuf, int N, int64_t rows,
+                          int n_local, void* Out, int accumulate, const int32_t* kept,
+                          const CapTable& ct, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  TC_TRY(make_map(&ma, Abuf, M, rows, 64, 64));
+  TC_TRY(make_map(&mb, Bbuf, N, rows, 64, 64));
+  TcParams p{};
+  p.kept = kept; p.mtile_prefix = nullptr; p.n_local = n_local; p.M = M; p.N = N; p.K = 0;
+  p.C = (__nv_bfloat16*)Out; p.accumulate = accumulate; p.ct = ct;
+  TC_CUDA(launch_tc_bn<TC_WGRAD>(N, ma, mb, p, s));
+  return MOE_OK;
 }
+
+moe_status_t tc_ffn_forward(TcPlan* plan, void* X, const void* w1, const void* b1,
+                            const void* w2, const void* b2, void* H, void* O, int64_t rows,
+                            int d, int f, int dout, const int32_t* kept,
+                            const int32_t* mtile_prefix, int n_local, const CapTable& ct,
+                            int max_cap, cudaStream_t s, int64_t* nlaunch, Prof* prof) {
+  (void)plan; (void)max_cap;
+  if (!ensure_encode()) return MOE_ERR_CUDA;
+  if (rows == 0 || n_local == 0) { *nlaunch = 0; return MOE_OK; }
+  moe_status_t st;
+  {
+    ProfScope ps(prof, "ffn_gemm1", s);
+    st = mgroup<TC_FWD1>(X, rows, d, w1, f, n_local, b1, H, f, kept, mtile_prefix, ct, s);
+  }
+  if (st != MOE_OK) return st;
+  {
+    ProfScope ps(prof, "ffn_gemm2", s);
+    st = mgroup<TC_FWD2>(H, rows, f, w2, dout, n_local, b2, O, dout, kept, mtile_prefix, ct, s);
+  }
+  *nlaunch = 2;
+  return st;
+}
+
+moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX, const void* w1,
+                             const void* w2, void* dw1, void* db1, void* dw2, void* db2,
+                             int accumulate, int64_t rows, int d, int f, int dout,
+                             const int32_t* kept, const int32_t* mtile_prefix, int n_local,
+                             const CapTable& ct, int max_cap, cudaStream_t s,
+                             int64_t* nlaunch, Prof* prof) {
+  (void)plan; (void)max_cap;
+  if (!ensure_encode()) return MOE_ERR_CUDA;
+  int64_t nl = 0;
+  if (rows == 0 || n_local == 0) { *nlaunch = 0; return MOE_OK; }
+  moe_status_t st;
+  if (dw2) {  // dW2_e = dO_e^T H_e   (before H is overwritten)
+    ProfScope ps(prof, "wgrad_w2", s);
+    st = wgrad(dO, dout, H, f, rows, n_local, dw2, accumulate, kept, ct, s);
+    if (st != MOE_OK) return st;
+    ++nl;
+  }
+  if (db2) {
+    ProfScope ps(prof, "bias_grad", s);
+    TC_CUDA(launch_colsum(1, dO, dout, kept, n_local, ct, db2, accumulate, s));
+    ++nl;
+  }
+  // dA = (dO W2_e) * 1[H > 0], W2_e stored [d_out x f] = [K x N]
+  {
+    ProfScope ps(prof, "dgrad_dA", s);
+    st = mgroup<TC_DGRAD_A>(dO, rows, dout, w2, f, n_local, nullptr, H, f, kept, mtile_prefix, ct, s);
+  }
+  if (st != MOE_OK) return st;
+  ++nl;
+  if (dw1) {  // dW1_e = dA_e^T X_e
+    ProfScope ps(prof, "wgrad_w1", s);
+    st = wgrad(H, f, X, d, rows, n_local, dw1, accumulate, kept, ct, s);
+    if (st != MOE_OK) return st;
+    ++nl;
+  }
+  if (db1) {
+    ProfScope ps(prof, "bias_grad", s);
+    TC_CUDA(launch_colsum(1, H, f, kept, n_local, ct, db1, accumulate, s));
+    ++nl;
+  }
+  // dX = dA W1_e, W1_e stored [f x d] = [K x N]
+  {
+    ProfScope ps(prof, "dgrad_dX", s);
+    st = mgroup<TC_DGRAD_X>(H, rows, f, w1, d, n_local, nullptr, dX, d, kept, mtile_prefix, ct, s);
+  }
+  if (st != MOE_OK) return st;
+  ++nl;
+  *nlaunch = nl;
+  return MOE_OK;
+}
+
 }  // namespace moe

@@ -185,8 +185,7 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
   h->s = c.dtype == MOE_BF16 ? 2 : 4;
   h->stream = (cudaStream_t)c.stream;
   const char* fs = getenv("MOE_FORCE_SIMT");
-  h->use_tc = 0;  // tcgen05 path enabled once parity-green
-  (void)fs;
+  h->use_tc = (c.dtype == MOE_BF16) && !(fs && fs[0] == '1');
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -321,7 +320,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     int64_t nk = 0;
     moe_status_t st = tc_ffn_forward(&h->tc, X, w1, b1, w2, b2, H, O, h->rows, d, f, dout,
                                      kept_local, rb.mtile_prefix, nl, h->ct, h->max_cap_local,
-                                     sd, &nk);
+                                     sd, &nk, &h->prof);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 forward failed");
   } else {
@@ -374,7 +373,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
     int64_t nk = 0;
     moe_status_t st = tc_ffn_backward(&h->tc, X, H, dO, dXb, w1, w2, dw1, db1, dw2, db2, acc,
                                       h->rows, d, f, dout, kept_local, rb.mtile_prefix, nl,
-                                      h->ct, h->max_cap_local, s0, &nk);
+                                      h->ct, h->max_cap_local, s0, &nk, &h->prof);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 backward failed");
   } else {

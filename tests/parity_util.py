@@ -10,6 +10,14 @@ from synth import make_dy, make_layer, to_numpy64
 TOL = {"f32": 1e-5, "bf16": 2e-2}
 
 
+def _np(v):
+    if not torch.is_tensor(v):
+        return v
+    if v.dtype == torch.bfloat16:
+        v = v.float()
+    return v.cpu().numpy()
+
+
 def rel(a, b):
     """Per-tensor ||a-b||_inf / ||b||_inf (reading 13)."""
     a = np.asarray(a, np.float64)
@@ -52,8 +60,8 @@ def run_pair(n, k, d, f, T, dtype, caps, renorm=1, regime="uniform", d_out=None,
     torch.cuda.synchronize()
     rt = layer.routing(T)
     gpu = dict(y=to_numpy64(y), **{kk: to_numpy64(v) for kk, v in grads.items()})
-    gpu["routing"] = {kk: (v.cpu().numpy() if torch.is_tensor(v) else v) for kk, v in rt.items()}
-    gpu["routing_fwd"] = {kk: (v.cpu().numpy() if torch.is_tensor(v) else v) for kk, v in rt_f.items()}
+    gpu["routing"] = {kk: _np(v) for kk, v in rt.items()}
+    gpu["routing_fwd"] = {kk: _np(v) for kk, v in rt_f.items()}
     gpu["stats"] = stats
     gpu["flags"] = st_flags
     # oracle: routing decisions from the GPU's fp32 logits (north star), fp64 values

@@ -1,0 +1,34 @@
+"""Stage-by-stage checks of the tcgen05 expert-FFN GEMMs (bf16) against plain PyTorch fp32
+on the GPU's own dispatched buffers: localises a failure to FWD1 / FWD2 / backward."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n,k,d,f,T", [(4, 1, 128, 256, 500), (6, 2, 192, 320, 777),
+                                       (3, 1, 64, 64, 130)])
+def test_tc_forward_buffers(n, k, d, f, T):
+    from paper_2205_01848_b200 import MoELayer
+    from synth import make_layer
+    g = {kk: v.cuda() for kk, v in make_layer(n, d, f, d, T, "bf16").items()}
+    layer = MoELayer(n, k, d, f, 0, T, "bf16", 1, device="cuda")
+    layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+    torch.cuda.synchronize()
+    r = layer.routing(T)
+    kept = r["kept"].tolist()
+    for e in range(n):
+        b, m = r["base"][e], kept[e]
+        if m == 0:
+            continue
+        X = r["x_buf"][b:b + m].float()
+        Href = torch.relu(X @ g["w1"][e].float().T + g["b1"][e].float())
+        H = r["h_buf"][b:b + m].float()
+        err = (H - Href).abs().max() / Href.abs().max()
+        assert err < 1e-2, (e, float(err))
+        Oref = H @ g["w2"][e].float().T + g["b2"][e].float()
+        O = r["o_buf"][b:b + m].float()
+        err = (O - Oref).abs().max() / Oref.abs().max()
+        assert err < 1e-2, (e, float(err))
+        pad = r["h_buf"][b + m: min(b + ((m + 127) // 128) * 128, r["base"][e + 1])]
+        assert pad.abs().max().item() == 0.0 if pad.numel() else True
