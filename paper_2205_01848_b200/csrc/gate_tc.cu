@@ -1,0 +1,686 @@
+// gate_tc.cu -- the gating network's three dense contractions on tcgen05 tensor cores (bf16).
+//
+//  K1  gate forward (Alg. 1 l.1-3): logits = x W_g^T with the softmax / top-k /
+//      normalize epilogue fused: each epilogue thread owns one token row (one TMEM lane) and
+//      streams its n logits through registers -- top-k by strict '>' in ascending expert order
+//      (ties -> lower index, reading 3), online softmax denominator, cached-index weights and
+//      the hit test of sample-assignment caching.
+//  K9  gate input gradient fused with the dispatch backward: dx = dl W_g + sum_r dX[row(t,r)].
+//  K10 gate weight gradient: dW_g = dl^T x, split-K over tokens, fixed-order reduction.
+//
+// dl is fp32; the tensor cores take it as an exact-ish bf16 pair dl = hi + lo (hi = bf16(dl),
+// lo = bf16(dl - hi); relative error <= 2^-17), i.e. two accumulating MMAs per K step.  The
+// pair is written by the combine-backward kernel (dlb buffer: hi rows [0,maxT), lo rows
+// [maxT, 2 maxT), n padded to a multiple of 64 with zeros).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+
+#include "common.cuh"
+#include "gate_tc.h"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace moe {
+
+constexpr int G_THREADS = 256;
+
+struct GateFwdParams {
+  int T, n, k, renorm;
+  const int32_t* cached;  // [T x k] or null
+  float* logits;          // [T x n]
+  int32_t* idx_out;       // [T x k] fresh top-k
+  float* w_out;           // [T x k]
+  int32_t* hit;
+  int32_t* flags;
+};
+
+struct GateDxParams {
+  int T, n_pad, k, d;
+  const int32_t* idx;
+  const int32_t* slot_of;
+  const __nv_bfloat16* dxbuf;  // [rows x d]
+  __nv_bfloat16* dx;           // [T x d]
+  int accumulate;
+  CapTable ct;
+};
+
+struct GateDwParams {
+  int T, n, d, chunk, splits;
+  float* partial;  // [splits x n x d]
+};
+
+// --------------------------------------------------------------------------------------
+// common pipeline skeleton pieces
+// --------------------------------------------------------------------------------------
+struct Bars {
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* tfull;
+  uint64_t* tempty;
+  uint32_t* tmem;
+};
+
+template <int STAGES>
+__device__ __forceinline__ Bars setup_bars(uint8_t* after_stages, int ncols, int warp, int lane) {
+  Bars b;
+  b.full = reinterpret_cast<uint64_t*>(after_stages);
+  b.empty = b.full + STAGES;
+  b.tfull = b.empty + STAGES;
+  b.tempty = b.tfull + 2;
+  b.tmem = reinterpret_cast<uint32_t*>(b.tempty + 2);
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&b.full[s], 1);
+      mbar_init(&b.empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&b.tfull[s], 1);
+      mbar_init(&b.tempty[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(b.tmem)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  return b;
+}
+
+__device__ __forceinline__ void teardown(uint32_t tmem_base, int ncols, int warp) {
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(ncols));
+  }
+}
+
+__device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// ======================================================================================
+// K1: gate forward + fused softmax / top-k / normalize epilogue
+// ======================================================================================
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(G_THREADS, 1)
+    gate_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmX,
+                       const __grid_constant__ CUtensorMap tmW, GateFwdParams p, int K) {
+  constexpr int A_BYTES = TC_BM * TC_BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + BN * TC_BK * 2;
+  constexpr uint32_t IDESC = make_idesc(BN, 0, 0);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmW);
+  }
+  Bars b = setup_bars<STAGES>(smem + STAGES * STAGE_BYTES, 2 * BN, warp, lane);
+  const uint32_t tmem_base = *b.tmem;
+  const int MT = (p.T + TC_BM - 1) / TC_BM;
+  const int nk = K / TC_BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < MT; t += gridDim.x) {
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&b.empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&b.full[stage], STAGE_BYTES);
+          tma_load_2d(sa, &tmX, &b.full[stage], kb * TC_BK, t * TC_BM);
+          tma_load_2d(sa + A_BYTES, &tmW, &b.full[stage], kb * TC_BK, 0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < MT; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&b.tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&b.full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k)
+            tc_mma(tmem_d, umma_desc(sa + k * 32, 16, 1024), umma_desc(sa + A_BYTES + k * 32, 16, 1024),
+                   IDESC, (kb | k) != 0);
+          tc_commit(&b.empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&b.tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int n = p.n, k = p.k;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < MT; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      mbar_wait(&b.tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int t = tile * TC_BM + q * 32 + lane;
+      const bool valid = t < p.T;
+      float sel_v[MOE_MAX_K];
+      int sel_e[MOE_MAX_K];
+      int cidx[MOE_MAX_K];
+      float cval[MOE_MAX_K];
+#pragma unroll
+      for (int r = 0; r < MOE_MAX_K; ++r) {
+        sel_v[r] = 0.f;
+        sel_e[r] = -1;
+        cidx[r] = -1;
+        cval[r] = 0.f;
+      }
+      if (valid && p.cached) {
+        for (int r = 0; r < k; ++r) cidx[r] = p.cached[(size_t)t * k + r];
+      }
+      float m_run = -INFINITY, s_run = 0.f;
+      bool nan_seen = false;
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      float* lrow = p.logits + (size_t)t * n;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        if (c * 32 >= n) break;  // warp-uniform
+        uint32_t r32[32];
+        tmem_ld32(taddr + c * 32, r32);
+        if (!valid) continue;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int e = c * 32 + j;
+          if (e >= n) break;
+          const float v = __uint_as_float(r32[j]);
+          lrow[e] = v;
+          nan_seen |= (v != v);
+          // streaming top-k, strict '>' keeps the lower index first among equals
+          if (sel_e[k - 1] < 0 || v > sel_v[k - 1]) {
+            int pos = k - 1;
+            while (pos > 0 && (sel_e[pos - 1] < 0 || v > sel_v[pos - 1])) {
+              sel_v[pos] = sel_v[pos - 1];
+              sel_e[pos] = sel_e[pos - 1];
+              --pos;
+            }
+            sel_v[pos] = v;
+            sel_e[pos] = e;
+          }
+          // online softmax denominator
+          if (v > m_run) {
+            s_run = s_run * expf(m_run - v) + 1.f;
+            m_run = v;
+          } else {
+            s_run += expf(v - m_run);
+          }
+          for (int r = 0; r < k; ++r)
+            if (cidx[r] == e) cval[r] = v;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&b.tempty[acc]);
+      if (valid) {
+        if (nan_seen) atomicOr(p.flags, 1);
+        int use[MOE_MAX_K];
+        float lv[MOE_MAX_K];
+        if (p.cached) {
+          bool ok = true;
+          for (int r = 0; r < k; ++r) {
+            ok &= (cidx[r] >= 0 && cidx[r] < n);
+            for (int q2 = 0; q2 < r; ++q2) ok &= (cidx[q2] != cidx[r]);
+          }
+          if (!ok) atomicOr(p.flags, 2);
+          bool same = true;
+          for (int r = 0; r < k; ++r) {
+            bool found = false;
+            for (int q2 = 0; q2 < k; ++q2) found |= (cidx[r] == sel_e[q2]);
+            same &= found;
+          }
+          if (same && ok) atomicAdd(p.hit, 1);
+          for (int r = 0; r < k; ++r) {
+            use[r] = ok ? cidx[r] : sel_e[r];
+            lv[r] = ok ? cval[r] : sel_v[r];
+          }
+        } else {
+          for (int r = 0; r < k; ++r) {
+            use[r] = sel_e[r];
+            lv[r] = sel_v[r];
+          }
+        }
+        int32_t* orow = p.idx_out + (size_t)t * k;
+        for (int r = 0; r < k; ++r) orow[r] = sel_e[r];
+        float* wrow = p.w_out + (size_t)t * k;
+        if (p.renorm) {
+          float m = lv[0];
+          for (int r = 1; r < k; ++r) m = fmaxf(m, lv[r]);
+          float ev[MOE_MAX_K], s = 0.f;
+          for (int r = 0; r < k; ++r) { ev[r] = expf(lv[r] - m); s += ev[r]; }
+          for (int r = 0; r < k; ++r) wrow[r] = ev[r] / s;
+        } else {
+          for (int r = 0; r < k; ++r) wrow[r] = expf(lv[r] - m_run) / s_run;
+        }
+        (void)use;
+      }
+    }
+  }
+  teardown(tmem_base, 2 * BN, warp);
+}
+
+// ======================================================================================
+// K9: dx = [hi | lo](dl) . [W_g ; W_g] + gather(dX)
+// ======================================================================================
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(G_THREADS, 1)
+    gate_dx_tc_kernel(const __grid_constant__ CUtensorMap tmHi,
+                      const __grid_constant__ CUtensorMap tmLo,
+                      const __grid_constant__ CUtensorMap tmW, GateDxParams p) {
+  constexpr int A_BYTES = TC_BM * TC_BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + BN * TC_BK * 2;
+  constexpr uint32_t IDESC = make_idesc(BN, 0, 1);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmHi);
+    prefetch_tmap(&tmLo);
+    prefetch_tmap(&tmW);
+  }
+  Bars b = setup_bars<STAGES>(smem + STAGES * STAGE_BYTES, 2 * BN, warp, lane);
+  const uint32_t tmem_base = *b.tmem;
+  const int MT = (p.T + TC_BM - 1) / TC_BM;
+  const int NT = p.d / BN;
+  const int nb = p.n_pad / TC_BK;
+  const int nk = 2 * nb;
+  const int total = MT * NT;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int mt = t % MT, nt = t / MT;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&b.empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&b.full[stage], STAGE_BYTES);
+          const int kk = (kb % nb) * TC_BK;
+          tma_load_2d(sa, kb < nb ? &tmHi : &tmLo, &b.full[stage], kk, mt * TC_BM);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j)
+            tma_load_2d(sb + j * 8192, &tmW, &b.full[stage], nt * BN + j * 64, kk);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&b.tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&b.full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k)
+            tc_mma(tmem_d, umma_desc(sa + k * 32, 16, 1024), umma_desc(sb + k * 2048, 8192, 1024),
+                   IDESC, (kb | k) != 0);
+          tc_commit(&b.empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&b.tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const int mt = tile % MT, nt = tile / MT;
+      mbar_wait(&b.tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int t = mt * TC_BM + q * 32 + lane;
+      const bool valid = t < p.T;
+      int rows[MOE_MAX_K];
+      int nr = 0;
+      if (valid) {
+        for (int r = 0; r < p.k; ++r) {
+          const int sl = p.slot_of[(size_t)t * p.k + r];
+          if (sl >= 0) rows[nr++] = p.ct.base[p.idx[(size_t)t * p.k + r]] + sl;
+        }
+      }
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      __nv_bfloat16* drow = p.dx + (size_t)t * p.d;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r32[32];
+        tmem_ld32(taddr + c * 32, r32);
+        if (!valid) continue;
+        const int col0 = nt * BN + c * 32;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        for (int q2 = 0; q2 < nr; ++q2) {  // expert path first, r order (as the SIMT form)
+          const __nv_bfloat16* src = p.dxbuf + (size_t)rows[q2] * p.d + col0;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            float xv[8];
+            unpack(ld_nc_v4(src + i), xv, __nv_bfloat16());
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[i + j] += xv[j];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r32[i]);
+        if (p.accumulate) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            float o[8];
+            unpack(ld_v4(drow + col0 + i), o, __nv_bfloat16());
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[i + j] += o[j];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) st_v4(drow + col0 + i, pack(v + i, __nv_bfloat16()));
+      }
+      tc_fence_before();
+      mbar_arrive(&b.tempty[acc]);
+    }
+  }
+  teardown(tmem_base, 2 * BN, warp);
+}
+
+// ======================================================================================
+// K10: dW_g partials = [hi ; lo](dl)^T x over a token chunk per split
+// ======================================================================================
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(G_THREADS, 1)
+    gate_dw_tc_kernel(const __grid_constant__ CUtensorMap tmHi,
+                      const __grid_constant__ CUtensorMap tmLo,
+                      const __grid_constant__ CUtensorMap tmX, GateDwParams p) {
+  constexpr int A_BYTES = TC_BM * TC_BK * 2;  // one of hi / lo
+  constexpr int STAGE_BYTES = 2 * A_BYTES + BN * TC_BK * 2;
+  constexpr uint32_t IDESC = make_idesc(BN, 1, 1);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmHi);
+    prefetch_tmap(&tmLo);
+    prefetch_tmap(&tmX);
+  }
+  Bars b = setup_bars<STAGES>(smem + STAGES * STAGE_BYTES, 2 * BN, warp, lane);
+  const uint32_t tmem_base = *b.tmem;
+  const int MT = (p.n + TC_BM - 1) / TC_BM;
+  const int NT = p.d / BN;
+  const int total = p.splits * MT * NT;
+
+  auto decode = [&](int t, int& s, int& mt, int& nt) {
+    nt = t % NT;
+    int r = t / NT;
+    mt = r % MT;
+    s = r / MT;
+  };
+  auto krange = [&](int s, int& k0, int& nkb) {
+    k0 = s * p.chunk;
+    int k1 = min(p.T, k0 + p.chunk);
+    nkb = k1 > k0 ? (k1 - k0 + TC_BK - 1) / TC_BK : 0;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int s, mt, nt, k0, nkb;
+        decode(t, s, mt, nt);
+        krange(s, k0, nkb);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&b.empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&b.full[stage], STAGE_BYTES);
+          const int tk = k0 + kb * TC_BK;
+          tma_load_2d(sa, &tmHi, &b.full[stage], mt * TC_BM, tk);
+          tma_load_2d(sa + 8192, &tmHi, &b.full[stage], mt * TC_BM + 64, tk);
+          tma_load_2d(sa + A_BYTES, &tmLo, &b.full[stage], mt * TC_BM, tk);
+          tma_load_2d(sa + A_BYTES + 8192, &tmLo, &b.full[stage], mt * TC_BM + 64, tk);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j)
+            tma_load_2d(sa + 2 * A_BYTES + j * 8192, &tmX, &b.full[stage], nt * BN + j * 64, tk);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        int s, mt, nt, k0, nkb;
+        decode(t, s, mt, nt);
+        krange(s, k0, nkb);
+        const int acc = it & 1;
+        mbar_wait(&b.tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&b.full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + 2 * A_BYTES;
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            const uint64_t dbx = umma_desc(sb + k * 2048, 8192, 1024);
+            tc_mma(tmem_d, umma_desc(sa + k * 2048, 8192, 1024), dbx, IDESC, (kb | k) != 0);
+            tc_mma(tmem_d, umma_desc(sa + A_BYTES + k * 2048, 8192, 1024), dbx, IDESC, 1);
+          }
+          tc_commit(&b.empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&b.tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+      int s, mt, nt, k0, nkb;
+      decode(tile, s, mt, nt);
+      krange(s, k0, nkb);
+      const int acc = it & 1;
+      mbar_wait(&b.tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int m = mt * TC_BM + q * 32 + lane;  // expert row
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      float* prow = p.partial + ((size_t)s * p.n + m) * p.d;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r32[32];
+        if (nkb > 0) {
+          tmem_ld32(taddr + c * 32, r32);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r32[i] = 0u;
+        }
+        if (m >= p.n) continue;
+        const int col0 = nt * BN + c * 32;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          st_v4(prow + col0 + i, make_uint4(r32[i], r32[i + 1], r32[i + 2], r32[i + 3]));
+      }
+      tc_fence_before();
+      mbar_arrive(&b.tempty[acc]);
+    }
+  }
+  teardown(tmem_base, 2 * BN, warp);
+}
+
+// ------------------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
+static int g_sms = 148;
+
+static bool enc_init() {
+  if (g_enc) return true;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return false;
+  g_enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  return true;
+}
+
+static bool map2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                  uint32_t box_inner, uint32_t box_outer) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return g_enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename KF>
+static cudaError_t set_smem(KF kf, size_t smem) {
+  return cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+static size_t smem_for(int stage_bytes, int stages) {
+  return (size_t)stage_bytes * stages + 1024 + 256;
+}
+
+cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int d, int k,
+                               int renorm, const int32_t* cached, RouteBufs b, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  if (!enc_init()) return cudaErrorNotSupported;
+  CUtensorMap mx, mw;
+  const int bn = n <= 64 ? 64 : (n <= 128 ? 128 : 256);
+  if (!map2d(&mx, x, d, T, 64, 128) || !map2d(&mw, wg, d, n, 64, bn)) return cudaErrorInvalidValue;
+  GateFwdParams p{T, n, k, renorm, cached, b.logits, cached ? b.fresh_idx : b.idx, b.w,
+                  b.hit_count, b.flags};
+  const int MT = (T + 127) / 128;
+  const int grid = MT < g_sms ? MT : g_sms;
+#define GF(BN, ST)                                                                       \
+  {                                                                                      \
+    auto kf = gate_fwd_tc_kernel<BN, ST>;                                                \
+    size_t sm = smem_for((128 + BN) * 64 * 2, ST);                                       \
+    cudaError_t e = set_smem(kf, sm);                                                    \
+    if (e != cudaSuccess) return e;                                                      \
+    kf<<<grid, G_THREADS, sm, s>>>(mx, mw, p, d);                                        \
+  }
+  if (bn == 64) GF(64, 8) else if (bn == 128) GF(128, 6) else GF(256, 4)
+#undef GF
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb, int maxT,
+                              int n_pad, RouteBufs b, int T, int k, int n, int d,
+                              const CapTable& ct, void* dx, int accumulate, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  if (!enc_init()) return cudaErrorNotSupported;
+  CUtensorMap mhi, mlo, mw;
+  const __nv_bfloat16* hi = (const __nv_bfloat16*)dlb;
+  const __nv_bfloat16* lo = hi + (size_t)maxT * n_pad;
+  if (!map2d(&mhi, hi, n_pad, T, 64, 128) || !map2d(&mlo, lo, n_pad, T, 64, 128) ||
+      !map2d(&mw, wg, d, n, 64, 64))
+    return cudaErrorInvalidValue;
+  GateDxParams p{};
+  p.T = T; p.n_pad = n_pad; p.k = k; p.d = d; p.idx = b.idx; p.slot_of = b.slot_of;
+  p.dxbuf = (const __nv_bfloat16*)dxbuf; p.dx = (__nv_bfloat16*)dx; p.accumulate = accumulate;
+  p.ct = ct;
+  const int bn = d % 256 == 0 ? 256 : (d % 128 == 0 ? 128 : 64);
+  const int total = ((T + 127) / 128) * (d / bn);
+  const int grid = total < g_sms ? total : g_sms;
+  (void)n;
+#define GX(BN, ST)                                                                       \
+  {                                                                                      \
+    auto kf = gate_dx_tc_kernel<BN, ST>;                                                 \
+    size_t sm = smem_for((128 + BN) * 64 * 2, ST);                                       \
+    cudaError_t e = set_smem(kf, sm);                                                    \
+    if (e != cudaSuccess) return e;                                                      \
+    kf<<<grid, G_THREADS, sm, s>>>(mhi, mlo, mw, p);                                     \
+  }
+  if (bn == 256) GX(256, 4) else if (bn == 128) GX(128, 6) else GX(64, 8)
+#undef GX
+  return cudaGetLastError();
+}
+
+int gate_dw_tc_splits(int T, int n, int d) {
+  const int bn = d % 256 == 0 ? 256 : (d % 128 == 0 ? 128 : 64);
+  const int tiles = ((n + 127) / 128) * (d / bn);
+  int want = (g_sms + tiles - 1) / tiles;
+  int maxs = (T + 255) / 256;
+  if (want > maxs) want = maxs;
+  return want < 1 ? 1 : want;
+}
+
+cudaError_t launch_gate_dw_tc(const void* dlb, int maxT, int n_pad, const void* x, int T, int n,
+                              int d, float* partial, void* dwg, int accumulate, cudaStream_t s) {
+  const size_t count = (size_t)n * d;
+  if (T == 0) {
+    if (!accumulate) return cudaMemsetAsync(dwg, 0, count * 2, s);
+    return cudaSuccess;
+  }
+  if (!enc_init()) return cudaErrorNotSupported;
+  int splits = gate_dw_tc_splits(T, n, d);
+  int chunk = (T + splits - 1) / splits;
+  chunk = (chunk + 63) / 64 * 64;
+  splits = (T + chunk - 1) / chunk;
+  CUtensorMap mhi, mlo, mx;
+  const __nv_bfloat16* hi = (const __nv_bfloat16*)dlb;
+  const __nv_bfloat16* lo = hi + (size_t)maxT * n_pad;
+  if (!map2d(&mhi, hi, n_pad, T, 64, 64) || !map2d(&mlo, lo, n_pad, T, 64, 64) ||
+      !map2d(&mx, x, d, T, 64, 64))
+    return cudaErrorInvalidValue;
+  GateDwParams p{T, n, d, chunk, splits, partial};
+  const int bn = d % 256 == 0 ? 256 : (d % 128 == 0 ? 128 : 64);
+  const int total = splits * ((n + 127) / 128) * (d / bn);
+  const int grid = total < g_sms ? total : g_sms;
+#define GW(BN, ST)                                                                       \
+  {                                                                                      \
+    auto kf = gate_dw_tc_kernel<BN, ST>;                                                 \
+    size_t sm = smem_for((2 * 128 + BN) * 64 * 2, ST);                                   \
+    cudaError_t e = set_smem(kf, sm);                                                    \
+    if (e != cudaSuccess) return e;                                                      \
+    kf<<<grid, G_THREADS, sm, s>>>(mhi, mlo, mx, p);                                     \
+  }
+  if (bn == 256) GW(256, 3) else if (bn == 128) GW(128, 4) else GW(64, 5)
+#undef GW
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_reduce_partials(1, partial, splits, count, dwg, accumulate, s);
+}
+
+}  // namespace moe

@@ -1,0 +1,17 @@
+// gate_tc.h -- launchers of the tcgen05 gate kernels (bf16 layers), see gate_tc.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "common.cuh"
+#include "kernels.h"
+
+namespace moe {
+cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int d, int k,
+                               int renorm, const int32_t* cached, RouteBufs b, cudaStream_t s);
+cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb, int maxT,
+                              int n_pad, RouteBufs b, int T, int k, int n, int d,
+                              const CapTable& ct, void* dx, int accumulate, cudaStream_t s);
+cudaError_t launch_gate_dw_tc(const void* dlb, int maxT, int n_pad, const void* x, int T, int n,
+                              int d, float* partial, void* dwg, int accumulate, cudaStream_t s);
+int gate_dw_tc_splits(int T, int n, int d);
+}  // namespace moe

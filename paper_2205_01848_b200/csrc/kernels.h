@@ -44,7 +44,8 @@ cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, 
                                int d_out, const CapTable& ct, void* y, cudaStream_t s);
 cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, RouteBufs b,
                                int T, int k, int n, int d_out, int renorm,
-                               const CapTable& ct, void* dobuf, cudaStream_t s);
+                               const CapTable& ct, void* dobuf, void* dlb, int maxT, int n_pad,
+                               cudaStream_t s);
 cudaError_t launch_gate_dx(int dtype, const void* wg, const void* dxbuf, RouteBufs b, int T,
                            int k, int n, int d, const CapTable& ct, void* dx, int accumulate,
                            cudaStream_t s);
@@ -52,6 +53,8 @@ cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int
                            float* partial, int splits, void* dwg, int accumulate,
                            cudaStream_t s);
 int gate_dw_splits(int T, int d);
+cudaError_t launch_reduce_partials(int dtype, const float* partial, int splits, size_t count,
+                                   void* out, int accumulate, cudaStream_t s);
 cudaError_t launch_colsum(int dtype, const void* buf, int cols, const int32_t* kept, int n,
                           const CapTable& ct, void* out, int accumulate, cudaStream_t s);
 

@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "gemm_tc.h"
+#include "gate_tc.h"
 #include "prof.h"
 #include <map>
 
@@ -21,13 +22,13 @@ using namespace moe;
 
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
-      xbuf, hbuf, obuf, dobuf, dxbuf, partial, total;
+      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, total;
 };
 
 struct moe_ctx {
   moe_config_t cfg{};
   int n = 0, k = 0, d = 0, f = 0, dout = 0, maxT = 0, dtype = 0, renorm = 1, R = 1, rank = 0;
-  int n_local = 0, e_lo = 0;
+  int n_local = 0, e_lo = 0, n_pad = 64;
   size_t s = 4;  // bytes per element
   cudaStream_t stream = nullptr, side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -96,7 +97,9 @@ void compute_layout(moe_ctx* h) {
   L.obuf = take((size_t)h->rows * h->dout * h->s);
   L.dobuf = take((size_t)h->rows * h->dout * h->s);
   L.dxbuf = take((size_t)h->rows * h->d * h->s);
-  L.partial = take((size_t)gate_dw_splits(h->maxT, h->d) * n * h->d * 4 + 4096);
+  const size_t splits = std::max(gate_dw_splits(h->maxT, h->d), gate_dw_tc_splits(h->maxT, h->n, h->d));
+  L.partial = take(splits * n * h->d * 4 + 4096);
+  L.dlb = take(h->dtype == MOE_BF16 ? 2 * T * (size_t)h->n_pad * 2 : 0);
   L.total = o;
 }
 
@@ -182,6 +185,7 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
   h->maxT = c.max_tokens; h->dtype = c.dtype; h->renorm = c.renormalize ? 1 : 0;
   h->R = c.world_size; h->rank = c.rank;
   h->n_local = h->n / h->R; h->e_lo = h->rank * h->n_local;
+  h->n_pad = (h->n + 63) / 64 * 64;
   h->s = c.dtype == MOE_BF16 ? 2 : 4;
   h->stream = (cudaStream_t)c.stream;
   const char* fs = getenv("MOE_FORCE_SIMT");
@@ -303,7 +307,10 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     if (T > 0)
       CUDA_TRY(h, cudaMemcpyAsync(rb.idx, h->cached, (size_t)T * k * 4, cudaMemcpyDeviceToDevice, sd));
   } else {
-    KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, nullptr, rb, s0));
+    if (h->use_tc)
+      KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, nullptr, rb, s0));
+    else
+      KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, nullptr, rb, s0));
   }
   KL(h, T > 0, "route_hist", sd, launch_route_hist(rb.idx, T, k, n, rb.tile_hist, sd));
   KL(h, 1, "route_scan", sd, launch_route_scan(rb.tile_hist, ntiles, n, h->ct, rb, sd));
@@ -330,7 +337,10 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
                                      kept_local, nl, h->ct, h->max_cap_local, EPI_BIAS, sd));
   }
   if (cached) {
-    KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, h->cached, rb, s0));
+    if (h->use_tc)
+      KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, h->cached, rb, s0));
+    else
+      KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, h->cached, rb, s0));
     CUDA_TRY(h, cudaEventRecord(h->ev_join, sd));
     CUDA_TRY(h, cudaStreamWaitEvent(s0, h->ev_join, 0));
   }
@@ -361,7 +371,9 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   const int32_t* kept_local = rb.kept;
 
   // K6 combine backward -> dO rows (local or, in EP, returned to the expert owners), dw, dl
-  KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O, rb, T, k, n, dout, h->renorm, h->ct, dO, s0));
+  void* dlb = h->use_tc ? (void*)(ws + h->L.dlb) : nullptr;
+  KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O, rb, T, k, n, dout, h->renorm, h->ct, dO,
+                                                     dlb, h->maxT, h->n_pad, s0));
   KL(h, 1, "zero_pad", s0, launch_zero_pad(dt, dO, dout, kept_local, nl, h->ct, s0));
   const char* w1 = (const char*)fa.w1 + (size_t)h->e_lo * f * d * h->s;
   const char* w2 = (const char*)fa.w2 + (size_t)h->e_lo * dout * f * h->s;
@@ -391,12 +403,22 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                                      kept_local, nl, h->ct, h->max_cap_local, EPI_NONE, s0));
   }
   // B4: dx = gather(dX) + dl W_g ;  B5: dW_g = dl^T x
-  if (a->dx)
-    KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dXb, rb, T, k, n, d, h->ct, a->dx, acc, s0));
+  if (a->dx) {
+    if (h->use_tc)
+      KL(h, T > 0, "gate_dx", s0, launch_gate_dx_tc(fa.w_gate, dXb, dlb, h->maxT, h->n_pad, rb, T, k, n, d,
+                                                    h->ct, a->dx, acc, s0));
+    else
+      KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dXb, rb, T, k, n, d, h->ct, a->dx, acc, s0));
+  }
   if (a->dw_gate) {
-    int splits = gate_dw_splits(h->maxT, d);
-    KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw(dt, rb.dl, fa.x, T, n, d, (float*)(ws + h->L.partial),
-                                        splits, a->dw_gate, acc, s0));
+    if (h->use_tc) {
+      KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw_tc(dlb, h->maxT, h->n_pad, fa.x, T, n, d,
+                                                            (float*)(ws + h->L.partial), a->dw_gate, acc, s0));
+    } else {
+      int splits = gate_dw_splits(h->maxT, d);
+      KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw(dt, rb.dl, fa.x, T, n, d, (float*)(ws + h->L.partial),
+                                          splits, a->dw_gate, acc, s0));
+    }
   }
   h->have_fwd = 0;  // H has been consumed
   return MOE_OK;

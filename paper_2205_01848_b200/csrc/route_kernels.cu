@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(
           for (int q = 0; q < k; ++q) found |= (use[r] == sel[q]);
           same &= found;
         }
-        if (same) atomicAdd(hit, 1);
+        if (same && ok) atomicAdd(hit, 1);
       } else {
         for (int r = 0; r < k; ++r) use[r] = sel[r];
       }
@@ -446,7 +446,8 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
     const T* __restrict__ dy, const T* __restrict__ obuf, const float* __restrict__ w,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of,
     const float* __restrict__ logits, CapTable ct, int Tn, int k, int n, int dout, int renorm,
-    T* __restrict__ dobuf, float* __restrict__ dw, float* __restrict__ dl) {
+    T* __restrict__ dobuf, float* __restrict__ dw, float* __restrict__ dl,
+    __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
@@ -488,45 +489,56 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   }
   if (lane < k) dw[(size_t)t * k + lane] = dwr[0 + lane];  // note: lane < k <= 8
   float* dlrow = dl + (size_t)t * n;
-  if (renorm) {
-    for (int e = lane; e < n; e += 32) {
-      float v = 0.f;
-      for (int r = 0; r < k; ++r)
-        if (er[r] == e) v = wr[r] * (dwr[r] - c);
-      dlrow[e] = v;
-    }
-  } else {
-    const float* l = logits + (size_t)t * n;
-    float m = -INFINITY;
+  float m = -INFINITY, sp = 0.f;
+  const float* l = logits + (size_t)t * n;
+  if (!renorm) {
     for (int e = lane; e < n; e += 32) m = fmaxf(m, l[e]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    float sp = 0.f;
     for (int e = lane; e < n; e += 32) sp += expf(l[e] - m);
     sp = __shfl_sync(0xffffffffu, warp_sum(sp), 0);
-    for (int e = lane; e < n; e += 32) {
-      float p = expf(l[e] - m) / sp;
-      float dp = 0.f;
-      for (int r = 0; r < k; ++r)
-        if (er[r] == e) dp = dwr[r];
-      dlrow[e] = p * (dp - c);
+  }
+  const int ncols = dlb ? n_pad : n;
+  for (int e = lane; e < ncols; e += 32) {
+    float v = 0.f;
+    if (e < n) {
+      if (renorm) {
+        for (int r = 0; r < k; ++r)
+          if (er[r] == e) v = wr[r] * (dwr[r] - c);
+      } else {
+        const float p = expf(l[e] - m) / sp;
+        float dp = 0.f;
+        for (int r = 0; r < k; ++r)
+          if (er[r] == e) dp = dwr[r];
+        v = p * (dp - c);
+      }
+      dlrow[e] = v;
+    }
+    if (dlb) {  // exact-ish bf16 pair for the tensor-core gate gradients: v = hi + lo
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+      dlb[(size_t)t * n_pad + e] = hi;
+      dlb[((size_t)maxT + t) * n_pad + e] = lo;
     }
   }
 }
 
 cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, RouteBufs b,
                                int T, int k, int n, int d_out, int renorm,
-                               const CapTable& ct, void* dobuf, cudaStream_t s) {
+                               const CapTable& ct, void* dobuf, void* dlb, int maxT, int n_pad,
+                               cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   dim3 grid((T + 7) / 8);
   if (dtype == 1)
     combine_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
         (const __nv_bfloat16*)dy, (const __nv_bfloat16*)obuf, b.w, b.idx, b.slot_of, b.logits,
-        ct, T, k, n, d_out, renorm, (__nv_bfloat16*)dobuf, b.dw, b.dl);
+        ct, T, k, n, d_out, renorm, (__nv_bfloat16*)dobuf, b.dw, b.dl, (__nv_bfloat16*)dlb, maxT,
+        n_pad);
   else
     combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dy, (const float*)obuf, b.w,
                                                    b.idx, b.slot_of, b.logits, ct, T, k, n,
-                                                   d_out, renorm, (float*)dobuf, b.dw, b.dl);
+                                                   d_out, renorm, (float*)dobuf, b.dw, b.dl,
+                                                   (__nv_bfloat16*)dlb, maxT, n_pad);
   return cudaGetLastError();
 }
 
@@ -682,6 +694,18 @@ __global__ void reduce_partials_kernel(const float* __restrict__ partial, int sp
   for (int q = 0; q < splits; ++q) s += partial[(size_t)q * count + i];
   if (accumulate) s += to_f(out[i]);
   out[i] = from_f<T>(s);
+}
+
+cudaError_t launch_reduce_partials(int dtype, const float* partial, int splits, size_t count,
+                                   void* out, int accumulate, cudaStream_t s) {
+  int rb = (int)((count + 255) / 256);
+  if (dtype == 1)
+    reduce_partials_kernel<__nv_bfloat16><<<rb, 256, 0, s>>>(partial, splits, count,
+                                                             (__nv_bfloat16*)out, accumulate);
+  else
+    reduce_partials_kernel<float><<<rb, 256, 0, s>>>(partial, splits, count, (float*)out,
+                                                     accumulate);
+  return cudaGetLastError();
 }
 
 int gate_dw_splits(int T, int d) {

@@ -48,6 +48,9 @@ class MoELayer:
         self.dtype = dtype
         self.tdtype = _TORCH_DT[dtype]
         self.world_size, self.rank = world_size, rank
+        import os
+        # bf16 layers run the expert FFN and gate contractions on tcgen05 tensor cores
+        self.uses_tcgen05 = dtype == "bf16" and os.environ.get("MOE_FORCE_SIMT", "0") != "1"
         cfg = L.MoEConfig(n_experts, top_k, d_model, d_ff, d_out, max_tokens, L.DTYPES[dtype],
                           int(renormalize), world_size, rank, C.c_void_p(nccl_comm),
                           C.c_void_p(self._stream()))
