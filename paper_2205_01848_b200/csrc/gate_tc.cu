@@ -63,7 +63,8 @@ struct Bars {
 };
 
 template <int STAGES>
-__device__ __forceinline__ Bars setup_bars(uint8_t* after_stages, int ncols, int warp, int lane) {
+__device__ __forceinline__ Bars setup_bars(uint8_t* after_stages, int ncols, int warp, int lane,
+                                           int epi_threads = 128) {
   Bars b;
   b.full = reinterpret_cast<uint64_t*>(after_stages);
   b.empty = b.full + STAGES;
@@ -77,7 +78,7 @@ __device__ __forceinline__ Bars setup_bars(uint8_t* after_stages, int ncols, int
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&b.tfull[s], 1);
-      mbar_init(&b.tempty[s], 128);
+      mbar_init(&b.tempty[s], epi_threads);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -284,8 +285,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 // ======================================================================================
 // K9: dx = [hi | lo](dl) . [W_g ; W_g] + gather(dX)
 // ======================================================================================
+constexpr int GX_THREADS = 384;  // 4 control warps + 8 epilogue warps (gather-heavy epilogue)
+
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(G_THREADS, 1)
+__global__ void __launch_bounds__(GX_THREADS, 1)
     gate_dx_tc_kernel(const __grid_constant__ CUtensorMap tmHi,
                       const __grid_constant__ CUtensorMap tmLo,
                       const __grid_constant__ CUtensorMap tmW, GateDxParams p) {
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     prefetch_tmap(&tmLo);
     prefetch_tmap(&tmW);
   }
-  Bars b = setup_bars<STAGES>(smem + STAGES * STAGE_BYTES, 2 * BN, warp, lane);
+  Bars b = setup_bars<STAGES>(smem + STAGES * STAGE_BYTES, 2 * BN, warp, lane, 256);
   const uint32_t tmem_base = *b.tmem;
   const int MT = (p.T + TC_BM - 1) / TC_BM;
   const int NT = p.d / BN;
@@ -375,16 +378,44 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       }
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       __nv_bfloat16* drow = p.dx + (size_t)t * p.d;
+      const int half = (warp - 4) >> 2;
+      constexpr int CH = BN / 64;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r32[32];
-        tmem_ld32(taddr + c * 32, r32);
-        if (!valid) continue;
+      for (int c = half * CH; c < (half + 1) * CH; ++c) {
         const int col0 = nt * BN + c * 32;
+        // gather loads first (expert path, r order as the SIMT form); their latency overlaps
+        // the TMEM load below
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = 0.f;
-        for (int q2 = 0; q2 < nr; ++q2) {  // expert path first, r order (as the SIMT form)
+        uint4 g[2][4];
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2)
+          if (q2 < nr) {
+            const __nv_bfloat16* src = p.dxbuf + (size_t)rows[q2] * p.d + col0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) g[q2][i] = ld_nc_v4(src + 8 * i);
+          }
+        uint4 old[4];
+        if (valid && p.accumulate) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) old[i] = ld_v4(drow + col0 + 8 * i);
+        }
+        uint32_t r32[32];
+        tmem_ld32(taddr + c * 32, r32);
+        if (!valid) continue;
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2)
+          if (q2 < nr) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float xv[8];
+              unpack(g[q2][i], xv, __nv_bfloat16());
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[8 * i + j] += xv[j];
+            }
+          }
+        for (int q2 = 2; q2 < nr; ++q2) {  // k > 2 (rare): plain loads
           const __nv_bfloat16* src = p.dxbuf + (size_t)rows[q2] * p.d + col0;
 #pragma unroll
           for (int i = 0; i < 32; i += 8) {
@@ -398,11 +429,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r32[i]);
         if (p.accumulate) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
+          for (int i = 0; i < 4; ++i) {
             float o[8];
-            unpack(ld_v4(drow + col0 + i), o, __nv_bfloat16());
+            unpack(old[i], o, __nv_bfloat16());
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[i + j] += o[j];
+            for (int j = 0; j < 8; ++j) v[8 * i + j] += o[j];
           }
         }
 #pragma unroll
@@ -630,7 +661,7 @@ cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb
     size_t sm = smem_for((128 + BN) * 64 * 2, ST);                                       \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \
-    kf<<<grid, G_THREADS, sm, s>>>(mhi, mlo, mw, p);                                     \
+    kf<<<grid, GX_THREADS, sm, s>>>(mhi, mlo, mw, p);                                     \
   }
   if (bn == 256) GX(256, 4) else if (bn == 128) GX(128, 6) else GX(64, 8)
 #undef GX

@@ -32,61 +32,9 @@
 #include "kernels.h"
 #include "prof.h"
 #include "tc_common.cuh"
+#include "gemm_tc_impl.cuh"
 
 namespace moe {
-
-enum TcKind { TC_FWD1 = 0, TC_FWD2 = 1, TC_DGRAD_A = 2, TC_DGRAD_X = 3, TC_WGRAD = 4 };
-
-constexpr int TC_THREADS = 256;
-
-struct TcParams {
-  const int32_t* kept;          // [n_local] M_e (M-grouped) or K_e (WGRAD)
-  const int32_t* mtile_prefix;  // [n_local+1] prefix of ceil(kept/128) (M-grouped)
-  int n_local;
-  int M, N, K;                  // WGRAD: M, N output dims; M-grouped: N cols, K depth
-  const __nv_bfloat16* bias;    // FWD1/FWD2 bias [n_local, N]
-  __nv_bfloat16* C;             // output base (buffer or weight-gradient tensor)
-  int ldc;                      // leading dim of C (M-grouped buffers)
-  int accumulate;               // WGRAD
-  CapTable ct;                  // base rows of each local expert region
-};
-
-template <int KIND>
-struct KindTraits {
-  static constexpr bool kgroup = (KIND == TC_WGRAD);
-  static constexpr int a_mn = (KIND == TC_WGRAD) ? 1 : 0;
-  static constexpr int b_mn = (KIND == TC_DGRAD_A || KIND == TC_DGRAD_X || KIND == TC_WGRAD) ? 1 : 0;
-};
-
-// Decode a linear tile index into (expert, m0, n0).
-template <bool KG>
-__device__ __forceinline__ bool decode_tile(int t, const int32_t* s_prefix, int n_local, int MT,
-                                            int NT, int& e, int& mt, int& nt) {
-  if (KG) {
-    int per = MT * NT;
-    e = t / per;
-    if (e >= n_local) return false;
-    int r = t - e * per;
-    nt = r / MT;
-    mt = r - nt * MT;
-    return true;
-  } else {
-    // s_prefix[j] = sum_{e<j} mtiles(e); tiles of expert e: [prefix[e]*NT, prefix[e+1]*NT)
-    int total = s_prefix[n_local] * NT;
-    if (t >= total) return false;
-    int lo = 0, hi = n_local - 1;
-    while (lo < hi) {  // largest e with prefix[e]*NT <= t
-      int mid = (lo + hi + 1) >> 1;
-      if (s_prefix[mid] * NT <= t) lo = mid; else hi = mid - 1;
-    }
-    e = lo;
-    int r = t - s_prefix[e] * NT;
-    int mte = s_prefix[e + 1] - s_prefix[e];
-    nt = r / mte;
-    mt = r - nt * mte;
-    return true;
-  }
-}
 
 template <int KIND, int BN, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -115,11 +63,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     prefetch_tmap(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      // WGRAD with a fused bias gradient: the stage is released by the MMA commit AND the
+      // bias warp (warp 3), which row-sums the A^T tile straight from shared memory
+      mbar_init(&empty_bar[s], (Tr::kgroup && p.bias_out) ? 2 : 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 128);
+      mbar_init(&tempty_bar[s], TC_EPI_THREADS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -213,9 +163,59 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     __syncwarp();
+  } else if (warp == 3) {
+    if (Tr::kgroup && p.bias_out) {
+      // ============================ bias-gradient warp ============================
+      // db[e][m] = sum over kept tokens of A[t, m] (A = dO for db2, dA for db1): the A^T
+      // tile of every k-block is already in shared memory (MN-major, 128B swizzle: token row
+      // kk holds 64 m-values in 8 16-byte chunks, chunk c stored at c ^ (kk & 7)).  Lane l
+      // owns 4 consecutive m: box j = l/16, chunk c = (l%16)/2, half h = l%2.  Sequential
+      // fp32 sums over tokens in k order: deterministic.  Only the nt == 0 tile of each
+      // (e, mt) sums; other tiles just release the stage.
+      const int j = lane >> 4, c = (lane & 15) >> 1, hh = lane & 1;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x;; t += gridDim.x) {
+        int e, mt, nt;
+        if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+        const int nk = (p.kept[e] + TC_BK - 1) / TC_BK;
+        float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          if (nt == 0) {
+            const uint8_t* box = smem + stage * STAGE_BYTES + j * 8192;
+#pragma unroll 8
+            for (int kk = 0; kk < TC_BK; ++kk) {
+              const uint2 u = *reinterpret_cast<const uint2*>(box + kk * 128 + ((c ^ (kk & 7)) << 4) + hh * 8);
+              acc4[0] += __uint_as_float(u.x << 16);
+              acc4[1] += __uint_as_float(u.x & 0xffff0000u);
+              acc4[2] += __uint_as_float(u.y << 16);
+              acc4[3] += __uint_as_float(u.y & 0xffff0000u);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (nt == 0) {
+          const int m = mt * TC_BM + j * 64 + c * 8 + hh * 4;
+          if (m < p.M) {
+            __nv_bfloat16* dst = p.bias_out + (size_t)e * p.M + m;
+            if (p.accumulate) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc4[i] += __bfloat162float(dst[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = __float2bfloat16_rn(acc4[i]);
+          }
+        }
+      }
+    }
+    __syncwarp();
   } else if (warp >= 4) {
     // ============================ epilogue ============================
-    const int q = warp & 3;          // TMEM lane quarter
+    const int q = warp & 3;          // TMEM lane quarter (warp w may access lanes 32*(w%4)..)
+    const int half = (warp - 4) >> 2;  // which half of the BN columns this warp drains
     const int row_in_tile = q * 32 + lane;
     int it = 0;
     for (int t = blockIdx.x;; t += gridDim.x, ++it) {
@@ -236,9 +236,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       else
         crow = p.C + (size_t)(p.ct.base[e] + row) * p.ldc;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      constexpr int CH = BN / 64;      // 32-column chunks per warp half
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * CH; c < (half + 1) * CH; ++c) {
         const int col0 = n0 + c * 32;
+        // issue this chunk's side-input loads before the TMEM load so their latency overlaps
+        uint4 side[4];
+        const bool need_side = (KIND == TC_DGRAD_A && row_ok) ||
+                               (KIND == TC_WGRAD && row_ok && p.accumulate);
+        if (need_side) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) side[i] = ld_v4(crow + col0 + 8 * i);
+        }
         uint32_t r[32];
         if (!zero_acc) {
           tmem_ld32(taddr + c * 32, r);
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; i += 8) {
               float h[8];
-              unpack(ld_v4(crow + col0 + i), h, __nv_bfloat16());
+              unpack(side[i / 8], h, __nv_bfloat16());
 #pragma unroll
               for (int j = 0; j < 8; ++j) v[i + j] = h[j] > 0.f ? v[i + j] : 0.f;
             }
@@ -290,7 +299,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; i += 8) {
               float o[8];
-              unpack(ld_v4(crow + col0 + i), o, __nv_bfloat16());
+              unpack(side[i / 8], o, __nv_bfloat16());
 #pragma unroll
               for (int j = 0; j < 8; ++j) v[i + j] += o[j];
             }
@@ -372,6 +381,20 @@ static cudaError_t launch_tc_bn(int N, const CUtensorMap& a, const CUtensorMap& 
 
 static int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64); }
 
+cudaError_t launch_tc2_kind(int kind, int BN, const CUtensorMap& a, const CUtensorMap& b,
+                            const TcParams& p, int grid, cudaStream_t s);
+
+// 2-CTA (cta_group::2) kernels need BN in {128, 256}.  MOE_TC_1CTA=<bitmask of TcKind> forces
+// the 1-CTA form for those kinds (debug / A-B comparisons).
+static bool use_2cta(int N, int kind) {
+  static int mask = -1;
+  if (mask < 0) {
+    const char* v = getenv("MOE_TC_1CTA");
+    mask = v ? atoi(v) : 0;
+  }
+  return !((mask >> kind) & 1) && N % 128 == 0;
+}
+
 void tc_plan_free(TcPlan* p) { (void)p; }
 
 #define TC_TRY(expr)                                        \
@@ -395,29 +418,37 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
                            const int32_t* prefix, const CapTable& ct, cudaStream_t s) {
   CUtensorMap ma, mb;
   const int bn = pick_bn(N);
+  const bool two = use_2cta(N, KIND);
   TC_TRY(make_map(&ma, A, K, rows, 64, 128));
   if (KindTraits<KIND>::b_mn)
     TC_TRY(make_map(&mb, B, N, (uint64_t)n_local * K, 64, 64));
   else
-    TC_TRY(make_map(&mb, B, K, (uint64_t)n_local * N, 64, bn));
+    TC_TRY(make_map(&mb, B, K, (uint64_t)n_local * N, 64, two ? bn / 2 : bn));
   TcParams p{};
   p.kept = kept; p.mtile_prefix = prefix; p.n_local = n_local; p.M = 0; p.N = N; p.K = K;
   p.bias = (const __nv_bfloat16*)bias; p.C = (__nv_bfloat16*)C; p.ldc = ldc; p.ct = ct;
-  TC_CUDA(launch_tc_bn<KIND>(N, ma, mb, p, s));
+  if (two)
+    TC_CUDA(launch_tc2_kind(KIND, bn, ma, mb, p, g_num_sms & ~1, s));
+  else
+    TC_CUDA(launch_tc_bn<KIND>(N, ma, mb, p, s));
   return MOE_OK;
 }
 
 // WGRAD: Out_e[M x N] (+)= A_e^T B_e, A = Abuf[rows x M], B = Bbuf[rows x N] over kept_e rows.
 static moe_status_t wgrad(const void* Abuf, int M, const void* Bbuf, int N, int64_t rows,
-                          int n_local, void* Out, int accumulate, const int32_t* kept,
-                          const CapTable& ct, cudaStream_t s) {
+                          int n_local, void* Out, void* bias_out, int accumulate,
+                          const int32_t* kept, const CapTable& ct, cudaStream_t s) {
   CUtensorMap ma, mb;
   TC_TRY(make_map(&ma, Abuf, M, rows, 64, 64));
   TC_TRY(make_map(&mb, Bbuf, N, rows, 64, 64));
   TcParams p{};
   p.kept = kept; p.mtile_prefix = nullptr; p.n_local = n_local; p.M = M; p.N = N; p.K = 0;
-  p.C = (__nv_bfloat16*)Out; p.accumulate = accumulate; p.ct = ct;
-  TC_CUDA(launch_tc_bn<TC_WGRAD>(N, ma, mb, p, s));
+  p.C = (__nv_bfloat16*)Out; p.bias_out = (__nv_bfloat16*)bias_out; p.accumulate = accumulate;
+  p.ct = ct;
+  if (use_2cta(N, TC_WGRAD))
+    TC_CUDA(launch_tc2_kind(TC_WGRAD, pick_bn(N), ma, mb, p, g_num_sms & ~1, s));
+  else
+    TC_CUDA(launch_tc_bn<TC_WGRAD>(N, ma, mb, p, s));
   return MOE_OK;
 }
 
@@ -454,13 +485,12 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   int64_t nl = 0;
   if (rows == 0 || n_local == 0) { *nlaunch = 0; return MOE_OK; }
   moe_status_t st;
-  if (dw2) {  // dW2_e = dO_e^T H_e   (before H is overwritten)
+  if (dw2) {  // dW2_e = dO_e^T H_e (before H is overwritten), db2 = sum dO fused in
     ProfScope ps(prof, "wgrad_w2", s);
-    st = wgrad(dO, dout, H, f, rows, n_local, dw2, accumulate, kept, ct, s);
+    st = wgrad(dO, dout, H, f, rows, n_local, dw2, db2, accumulate, kept, ct, s);
     if (st != MOE_OK) return st;
     ++nl;
-  }
-  if (db2) {
+  } else if (db2) {
     ProfScope ps(prof, "bias_grad", s);
     TC_CUDA(launch_colsum(1, dO, dout, kept, n_local, ct, db2, accumulate, s));
     ++nl;
@@ -472,13 +502,12 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   }
   if (st != MOE_OK) return st;
   ++nl;
-  if (dw1) {  // dW1_e = dA_e^T X_e
+  if (dw1) {  // dW1_e = dA_e^T X_e, db1 = sum dA fused in
     ProfScope ps(prof, "wgrad_w1", s);
-    st = wgrad(H, f, X, d, rows, n_local, dw1, accumulate, kept, ct, s);
+    st = wgrad(H, f, X, d, rows, n_local, dw1, db1, accumulate, kept, ct, s);
     if (st != MOE_OK) return st;
     ++nl;
-  }
-  if (db1) {
+  } else if (db1) {
     ProfScope ps(prof, "bias_grad", s);
     TC_CUDA(launch_colsum(1, H, f, kept, n_local, ct, db1, accumulate, s));
     ++nl;

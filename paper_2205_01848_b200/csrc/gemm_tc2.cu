@@ -1,0 +1,436 @@
+// gemm_tc2.cu -- 2-CTA (cta_group::2) variant of the tcgen05 grouped GEMM (see gemm_tc.cu for
+// the GEMM table).  A CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile: CTA r holds
+// A rows [128r, 128r+128) and B columns [BN/2 r, BN/2 (r+1)) in its shared memory; the leader
+// (r = 0) issues tcgen05.mma.cta_group::2 (M = 256) which reads both CTAs' operands and writes
+// each CTA's 128 x BN accumulator into its own TMEM.  Per SM this halves the B bytes per MMA
+// (32 KB per 64-deep k-block instead of 48 KB), so the same shared memory holds 6 stages
+// instead of 4 -- the TMA-latency slack that the 1-CTA kernel lacks at K = 1024.
+//
+// Barriers: full[s] lives in the leader and collects both CTAs' TMA bytes (2-SM TMA form);
+// empty[s] and tfull[a] live in both CTAs and are signalled by multicast tcgen05.commit;
+// tempty[a] lives in the leader and collects one arrive per epilogue warp of both CTAs.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "gemm_tc_impl.cuh"
+#include "tc_common.cuh"
+
+namespace moe {
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+  uint32_t addr = smem_u32(b);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map,
+                                                uint32_t bar_cluster, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                        uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum), "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+// instruction descriptor for M = 256 (cta_group::2)
+__host__ __device__ constexpr uint32_t make_idesc2(int n, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+constexpr int TC2_M = 256;
+
+template <int KIND, int BN, int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    TcParams p) {
+  using Tr = KindTraits<KIND>;
+  constexpr int BNH = BN / 2;                    // B columns held by each CTA
+  constexpr int A_BYTES = TC_BM * TC_BK * 2;     // 16 KB: this CTA's 128 rows
+  constexpr int B_BYTES = BNH * TC_BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t IDESC = make_idesc2(BN, Tr::a_mn, Tr::b_mn);
+  constexpr int EPI_WARPS = TC_EPI_THREADS / 32;
+  const bool fuse_bias = Tr::kgroup && p.bias_out != nullptr;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint64_t* bias_bar = tempty_bar + 2;                             // [STAGES]
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bias_bar + STAGES);
+  int32_t* s_prefix = reinterpret_cast<int32_t*>(s_tmem + 4);        // [n_local + 1]
+  float* s_bias = reinterpret_cast<float*>(s_prefix + MOE_MAX_E + 4);  // [4][128]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int n_local = p.n_local;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 3 && !Tr::kgroup) {  // prefix of ceil(kept / 256) m-tiles (warp scan)
+    int carry = 0;
+    for (int base = 0; base < n_local; base += 32) {
+      const int e = base + lane;
+      int v = e < n_local ? (p.kept[e] + TC2_M - 1) / TC2_M : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (e < n_local) s_prefix[e] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_prefix[n_local] = carry;
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);   // multicast MMA commit
+      mbar_init(&bias_bar[s], 2);    // the 2 bias warps are done reading the stage
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 2 * EPI_WARPS);      // one arrive per epilogue warp, both CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(s_tmem)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *s_tmem;
+
+  const int NT = (p.N + BN - 1) / BN;
+  const int MT = Tr::kgroup ? (p.M + TC2_M - 1) / TC2_M : 0;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ============================ TMA producer (both CTAs) ============================
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair;; t += npairs) {
+        int e, mt, nt;
+        if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+        const int m0 = mt * TC2_M + (int)crank * TC_BM;   // this CTA's A rows
+        const int n0 = nt * BN + (int)crank * BNH;        // this CTA's B columns
+        const int base = p.ct.base[e];
+        const int nk = Tr::kgroup ? (p.kept[e] + TC_BK - 1) / TC_BK : p.K / TC_BK;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          // the bias warps observe every use of every stage (in lockstep with empty[s], so
+          // parities cannot alias); the stage is refilled only after they released it
+          if (fuse_bias) mbar_wait(&bias_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          const uint32_t fb = mapa_rank(smem_u32(&full_bar[stage]), 0);
+          if (leader) mbar_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
+          const int k0 = kb * TC_BK;
+          if (Tr::a_mn) {
+            tma_load_2d_2sm(sa, &tmA, fb, m0, base + k0);
+            tma_load_2d_2sm(sa + 8192, &tmA, fb, m0 + 64, base + k0);
+          } else {
+            tma_load_2d_2sm(sa, &tmA, fb, k0, base + m0);
+          }
+          if (Tr::b_mn) {
+            const int krow = Tr::kgroup ? base + k0 : e * p.K + k0;
+#pragma unroll
+            for (int j = 0; j < BNH / 64; ++j) tma_load_2d_2sm(sb + j * 8192, &tmB, fb, n0 + j * 64, krow);
+          } else {
+            tma_load_2d_2sm(sb, &tmB, fb, k0, e * p.N + n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ============================ MMA issuer (leader only) ============================
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair;; t += npairs, ++it) {
+        int e, mt, nt;
+        if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+        const int acc = it & 1;
+        const int nk = Tr::kgroup ? (p.kept[e] + TC_BK - 1) / TC_BK : p.K / TC_BK;
+        mbar_wait_cluster(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            uint64_t da = Tr::a_mn ? umma_desc(sa + k * 2048, 8192, 1024)
+                                   : umma_desc(sa + k * 32, 16, 1024);
+            uint64_t db = Tr::b_mn ? umma_desc(sb + k * 2048, 8192, 1024)
+                                   : umma_desc(sb + k * 32, 16, 1024);
+            tc_mma2(tmem_d, da, db, IDESC, (kb | k) != 0);
+          }
+          tc_commit2_mc(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit2_mc(&tfull_bar[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 2 || warp == 3) {
+    if (fuse_bias) {
+      // ====================== bias-gradient warps (WGRAD, nt == 0 tiles) ======================
+      // db[e][m] = sum over kept tokens of A[t, m]; this CTA's A^T tile (2 boxes of 64 m x 64
+      // tokens, 128B swizzle: chunk c of token row kk stored at c ^ (kk & 7)) is summed from
+      // shared memory after the MMA has consumed the stage (empty[s] completes in both CTAs
+      // via the multicast commit); the producer waits for bias_bar[s] before refilling it.
+      // Thread b (0..63): 16-byte chunk cb = b % 16 (box cb/8, chunk cb%8),
+      // token rows [16 g, 16 g + 16) with g = b / 16; fixed-order fp32 sums, then a fixed
+      // 4-way reduction over g through shared memory: deterministic.
+      const int b = (warp - 2) * 32 + lane;
+      const int cb = b & 15, g = b >> 4;
+      const int bj = cb >> 3, bc = cb & 7;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair;; t += npairs) {
+        int e, mt, nt;
+        if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+        const int nk = (p.kept[e] + TC_BK - 1) / TC_BK;
+        float a8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a8[i] = 0.f;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty_bar[stage], phase);
+          if (nt == 0) {
+            const uint8_t* box = smem + stage * STAGE_BYTES + bj * 8192;
+#pragma unroll 4
+            for (int kk = g * 16; kk < g * 16 + 16; ++kk) {
+              const uint4 u = *reinterpret_cast<const uint4*>(box + kk * 128 + ((bc ^ (kk & 7)) << 4));
+              float f8[8];
+              unpack(u, f8, __nv_bfloat16());
+#pragma unroll
+              for (int i = 0; i < 8; ++i) a8[i] += f8[i];
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bias_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (nt == 0) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) s_bias[g * 128 + cb * 8 + i] = a8[i];
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int ml = b * 2 + q;
+            float v = s_bias[ml] + s_bias[128 + ml] + s_bias[256 + ml] + s_bias[384 + ml];
+            const int m = mt * TC2_M + (int)crank * TC_BM + ml;
+            if (m < p.M) {
+              __nv_bfloat16* dst = p.bias_out + (size_t)e * p.M + m;
+              if (p.accumulate) v += __bfloat162float(*dst);
+              *dst = __float2bfloat16_rn(v);
+            }
+          }
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ============================ epilogue (both CTAs) ============================
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const int row_in_tile = (int)crank * TC_BM + q * 32 + lane;
+    const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty_bar[0]), 0);
+    int it = 0;
+    for (int t = pair;; t += npairs, ++it) {
+      int e, mt, nt;
+      if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+      const int acc = it & 1;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int m0 = mt * TC2_M, n0 = nt * BN;
+      const int row = m0 + row_in_tile;
+      const bool zero_acc = Tr::kgroup && p.kept[e] == 0;
+      const int Me = Tr::kgroup ? p.M : p.kept[e];
+      const bool row_ok = row < Me;
+      // padding rows written as zeros (token-K GEMMs read up to roundup(kept, 64))
+      const bool row_pad = !Tr::kgroup && !row_ok && row < ((Me + 63) & ~63);
+      __nv_bfloat16* crow;
+      if (Tr::kgroup)
+        crow = p.C + ((size_t)e * p.M + row) * p.N;
+      else
+        crow = p.C + (size_t)(p.ct.base[e] + row) * p.ldc;
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      constexpr int CH = BN / 64;
+#pragma unroll 1
+      for (int c = half * CH; c < (half + 1) * CH; ++c) {
+        const int col0 = n0 + c * 32;
+        uint4 side[4];
+        const bool need_side = (KIND == TC_DGRAD_A && row_ok) ||
+                               (KIND == TC_WGRAD && row_ok && p.accumulate);
+        if (need_side) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) side[i] = ld_v4(crow + col0 + 8 * i);
+        }
+        uint32_t r[32];
+        if (!zero_acc) {
+          tmem_ld32(taddr + c * 32, r);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (col0 >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        bool store = true;
+        if (KIND == TC_FWD1 || KIND == TC_FWD2) {
+          if (row_ok) {
+            const __nv_bfloat16* bp = p.bias + (size_t)e * p.N + col0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              float bb[8];
+              unpack(ld_v4(bp + i), bb, __nv_bfloat16());
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float x = v[i + j] + bb[j];
+                v[i + j] = (KIND == TC_FWD1) ? (x > 0.f ? x : 0.f) : x;
+              }
+            }
+          } else {
+            store = (KIND == TC_FWD1) && row_pad;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+        } else if (KIND == TC_DGRAD_A) {
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              float h[8];
+              unpack(side[i / 8], h, __nv_bfloat16());
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[i + j] = h[j] > 0.f ? v[i + j] : 0.f;
+            }
+          } else {
+            store = row_pad;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+        } else if (KIND == TC_DGRAD_X) {
+          store = row_ok;
+        } else {  // WGRAD
+          store = row_ok;
+          if (row_ok && p.accumulate) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              float o[8];
+              unpack(side[i / 8], o, __nv_bfloat16());
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[i + j] += o[j];
+            }
+          }
+        }
+        if (store) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) st_v4(crow + col0 + i, pack(v + i, __nv_bfloat16()));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(2 * BN));
+  }
+}
+
+// ------------------------------------------------------------------------------ host side
+template <int KIND, int BN>
+static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p,
+                           int grid, cudaStream_t s) {
+  constexpr int STAGES = (BN == 256) ? 6 : 8;
+  constexpr int STAGE_BYTES = (TC_BM + BN / 2) * TC_BK * 2;
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 512 + 4 * (MOE_MAX_E + 8) + 2048;
+  auto kf = tc_gemm2_kernel<KIND, BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kf<<<grid, TC_THREADS, smem, s>>>(a, b, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc2_kind(int kind, int BN, const CUtensorMap& a, const CUtensorMap& b,
+                            const TcParams& p, int grid, cudaStream_t s) {
+#define K2(KD)                                                               \
+  case KD:                                                                   \
+    return BN == 256 ? launch2<KD, 256>(a, b, p, grid, s) : launch2<KD, 128>(a, b, p, grid, s);
+  switch (kind) {
+    K2(TC_FWD1) K2(TC_FWD2) K2(TC_DGRAD_A) K2(TC_DGRAD_X) K2(TC_WGRAD)
+    default: return cudaErrorInvalidValue;
+  }
+#undef K2
+}
+
+}  // namespace moe

@@ -1,0 +1,67 @@
+// gemm_tc_impl.cuh -- definitions shared by the 1-CTA and 2-CTA tcgen05 grouped GEMMs.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace moe {
+
+enum TcKind { TC_FWD1 = 0, TC_FWD2 = 1, TC_DGRAD_A = 2, TC_DGRAD_X = 3, TC_WGRAD = 4 };
+
+constexpr int TC_THREADS = 384;     // 4 control warps + 8 epilogue warps
+constexpr int TC_EPI_THREADS = 256;
+
+struct TcParams {
+  const int32_t* kept;          // [n_local] M_e (M-grouped) or K_e (WGRAD)
+  const int32_t* mtile_prefix;  // [n_local+1] prefix of ceil(kept/128) (M-grouped)
+  int n_local;
+  int M, N, K;                  // WGRAD: M, N output dims; M-grouped: N cols, K depth
+  const __nv_bfloat16* bias;    // FWD1/FWD2 bias [n_local, N]
+  __nv_bfloat16* bias_out;      // WGRAD: fused bias gradient db[e][m] = sum_t A[t, m] (or null)
+  __nv_bfloat16* C;             // output base (buffer or weight-gradient tensor)
+  int ldc;                      // leading dim of C (M-grouped buffers)
+  int accumulate;               // WGRAD
+  CapTable ct;                  // base rows of each local expert region
+};
+
+template <int KIND>
+struct KindTraits {
+  static constexpr bool kgroup = (KIND == TC_WGRAD);
+  static constexpr int a_mn = (KIND == TC_WGRAD) ? 1 : 0;
+  static constexpr int b_mn = (KIND == TC_DGRAD_A || KIND == TC_DGRAD_X || KIND == TC_WGRAD) ? 1 : 0;
+};
+
+// Decode a linear tile index into (expert, m0, n0).
+template <bool KG>
+__device__ __forceinline__ bool decode_tile(int t, const int32_t* s_prefix, int n_local, int MT,
+                                            int NT, int& e, int& mt, int& nt) {
+  if (KG) {
+    int per = MT * NT;
+    e = t / per;
+    if (e >= n_local) return false;
+    int r = t - e * per;
+    nt = r / MT;
+    mt = r - nt * MT;
+    return true;
+  } else {
+    // s_prefix[j] = sum_{e<j} mtiles(e); tiles of expert e: [prefix[e]*NT, prefix[e+1]*NT)
+    int total = s_prefix[n_local] * NT;
+    if (t >= total) return false;
+    int lo = 0, hi = n_local - 1;
+    while (lo < hi) {  // largest e with prefix[e]*NT <= t
+      int mid = (lo + hi + 1) >> 1;
+      if (s_prefix[mid] * NT <= t) lo = mid; else hi = mid - 1;
+    }
+    e = lo;
+    int r = t - s_prefix[e] * NT;
+    int mte = s_prefix[e + 1] - s_prefix[e];
+    nt = r / mte;
+    mt = r - nt * mte;
+    return true;
+  }
+}
+
+
+}  // namespace moe

@@ -212,3 +212,15 @@ def test_autograd_function_matches_layer():
     y.square().sum().backward()
     assert x.grad is not None and m.w1.grad is not None and m.w_gate.grad is not None
     assert torch.isfinite(x.grad).all()
+
+
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("k,renorm", [(1, 0), (2, 1)])
+def test_multitile_stress_bf16(k, renorm):
+    """More tiles than SM pairs in every tcgen05 GEMM (persistent loops wrap, multi-k-block
+    weight-gradient tiles, fused bias warps): guards the pipeline/barrier protocols."""
+    n, T, d, f = 64, 8192, 256, 1024
+    caps = _caps(n, T, k, 1.0)
+    layer, gpu, st, gr, ol = run_pair(n, k, d, f, T, "bf16", caps, renorm)
+    assert_routing_exact(gpu, st, k)
+    assert_values(gpu, st, gr, ol, "bf16")

@@ -30,5 +30,5 @@ def test_tc_forward_buffers(n, k, d, f, T):
         O = r["o_buf"][b:b + m].float()
         err = (O - Oref).abs().max() / Oref.abs().max()
         assert err < 1e-2, (e, float(err))
-        pad = r["h_buf"][b + m: min(b + ((m + 127) // 128) * 128, r["base"][e + 1])]
+        pad = r["h_buf"][b + m: min(b + ((m + 63) // 64) * 64, r["base"][e + 1])]
         assert pad.abs().max().item() == 0.0 if pad.numel() else True
