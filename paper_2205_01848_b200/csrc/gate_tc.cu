@@ -364,8 +364,6 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
       const int acc = it & 1;
       const int mt = tile % MT, nt = tile / MT;
-      mbar_wait(&b.tfull[acc], (it >> 1) & 1);
-      tc_fence_after();
       const int t = mt * TC_BM + q * 32 + lane;
       const bool valid = t < p.T;
       int rows[MOE_MAX_K];
@@ -376,26 +374,26 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
           if (sl >= 0) rows[nr++] = p.ct.base[p.idx[(size_t)t * p.k + r]] + sl;
         }
       }
-      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
-      __nv_bfloat16* drow = p.dx + (size_t)t * p.d;
       const int half = (warp - 4) >> 2;
       constexpr int CH = BN / 64;
-#pragma unroll 1
-      for (int c = half * CH; c < (half + 1) * CH; ++c) {
+      // prefetch the first gathered dX row of every chunk before waiting for the MMA
+      uint4 pre[CH][4];
+      if (nr > 0) {
+#pragma unroll
+        for (int cc = 0; cc < CH; ++cc) {
+          const __nv_bfloat16* src = p.dxbuf + (size_t)rows[0] * p.d + nt * BN + (half * CH + cc) * 32;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pre[cc][i] = ld_nc_v4(src + 8 * i);
+        }
+      }
+      mbar_wait(&b.tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      __nv_bfloat16* drow = p.dx + (size_t)t * p.d;
+#pragma unroll
+      for (int cc = 0; cc < CH; ++cc) {
+        const int c = half * CH + cc;
         const int col0 = nt * BN + c * 32;
-        // gather loads first (expert path, r order as the SIMT form); their latency overlaps
-        // the TMEM load below
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-        uint4 g[2][4];
-#pragma unroll
-        for (int q2 = 0; q2 < 2; ++q2)
-          if (q2 < nr) {
-            const __nv_bfloat16* src = p.dxbuf + (size_t)rows[q2] * p.d + col0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) g[q2][i] = ld_nc_v4(src + 8 * i);
-          }
         uint4 old[4];
         if (valid && p.accumulate) {
 #pragma unroll
@@ -404,18 +402,19 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
         uint32_t r32[32];
         tmem_ld32(taddr + c * 32, r32);
         if (!valid) continue;
+        float v[32];
 #pragma unroll
-        for (int q2 = 0; q2 < 2; ++q2)
-          if (q2 < nr) {
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        if (nr > 0) {  // expert path first, r order (as the SIMT form)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              float xv[8];
-              unpack(g[q2][i], xv, __nv_bfloat16());
+          for (int i = 0; i < 4; ++i) {
+            float xv[8];
+            unpack(pre[cc][i], xv, __nv_bfloat16());
 #pragma unroll
-              for (int j = 0; j < 8; ++j) v[8 * i + j] += xv[j];
-            }
+            for (int j = 0; j < 8; ++j) v[8 * i + j] += xv[j];
           }
-        for (int q2 = 2; q2 < nr; ++q2) {  // k > 2 (rare): plain loads
+        }
+        for (int q2 = 1; q2 < nr; ++q2) {
           const __nv_bfloat16* src = p.dxbuf + (size_t)rows[q2] * p.d + col0;
 #pragma unroll
           for (int i = 0; i < 32; i += 8) {

@@ -300,8 +300,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       int e, mt, nt;
       if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
       const int acc = it & 1;
-      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
-      tc_fence_after();
       const int m0 = mt * TC2_M, n0 = nt * BN;
       const int row = m0 + row_in_tile;
       const bool zero_acc = Tr::kgroup && p.kept[e] == 0;
@@ -314,18 +312,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         crow = p.C + ((size_t)e * p.M + row) * p.N;
       else
         crow = p.C + (size_t)(p.ct.base[e] + row) * p.ldc;
-      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       constexpr int CH = BN / 64;
-#pragma unroll 1
-      for (int c = half * CH; c < (half + 1) * CH; ++c) {
-        const int col0 = n0 + c * 32;
-        uint4 side[4];
-        const bool need_side = (KIND == TC_DGRAD_A && row_ok) ||
-                               (KIND == TC_WGRAD && row_ok && p.accumulate);
-        if (need_side) {
+      // Side inputs of the whole tile (bias, H mask, old gradient) are fetched BEFORE waiting
+      // for the accumulator, so their DRAM/L2 latency overlaps this tile's MMAs.
+      uint4 pre[CH][4];
+      const bool need_side = ((KIND == TC_FWD1 || KIND == TC_FWD2 || KIND == TC_DGRAD_A) && row_ok) ||
+                             (KIND == TC_WGRAD && row_ok && p.accumulate);
+      if (need_side) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) side[i] = ld_v4(crow + col0 + 8 * i);
+        for (int cc = 0; cc < CH; ++cc) {
+          const int col0 = n0 + (half * CH + cc) * 32;
+          const __nv_bfloat16* src = (KIND == TC_FWD1 || KIND == TC_FWD2)
+                                         ? p.bias + (size_t)e * p.N + col0
+                                         : crow + col0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pre[cc][i] = ld_v4(src + 8 * i);
         }
+      }
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+      for (int cc = 0; cc < CH; ++cc) {
+        const int c = half * CH + cc;
+        const int col0 = n0 + c * 32;
+        uint4* side = pre[cc];
         uint32_t r[32];
         if (!zero_acc) {
           tmem_ld32(taddr + c * 32, r);
@@ -340,11 +351,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         bool store = true;
         if (KIND == TC_FWD1 || KIND == TC_FWD2) {
           if (row_ok) {
-            const __nv_bfloat16* bp = p.bias + (size_t)e * p.N + col0;
 #pragma unroll
             for (int i = 0; i < 32; i += 8) {
               float bb[8];
-              unpack(ld_v4(bp + i), bb, __nv_bfloat16());
+              unpack(side[i / 8], bb, __nv_bfloat16());
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 float x = v[i + j] + bb[j];
