@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1024)
+    ap.add_argument("--ep", action="store_true",
+                    help="force the expert-parallel (NCCL) path at N=1 (loopback)")
     return ap.parse_args()
 
 
@@ -116,9 +118,12 @@ def dist_setup(args):
 # ------------------------------------------------------------------------------------------
 # algorithmic work per kernel: bytes or FLOPs per launch
 # ------------------------------------------------------------------------------------------
-def kernel_work(cfg, T, A, s):
+def kernel_work(cfg, T, A, s, A_tok=None):
+    """A: kept rows of this GPU's experts (GEMM work); A_tok: kept pairs of this GPU's tokens
+    (dispatch / combine traffic).  Equal on one GPU."""
     n, k, d, f, do = cfg.n_experts, cfg.top_k, cfg.d_model, cfg.d_ff, cfg.d_out
     gf = 2.0 * A * d * f  # one expert GEMM (fwd or dgrad or wgrad) = 2*A*d*f FLOPs
+    A = A if A_tok is None else A_tok
     return {
         # name: (kind, amount)   kind "flop" (tensor/alu) or "byte" (hbm)
         "gate_topk": ("byte", T * d * s + n * d * s + 4 * T * n + 8 * T * k),
@@ -151,12 +156,26 @@ def run_ours(args):
     alpha = args.alpha if args.alpha is not None else cfg.alpha
     n, k, d, f, do = cfg.n_experts, cfg.top_k, cfg.d_model, cfg.d_ff, cfg.d_out
     s = 2 if cfg.dtype == "bf16" else 4
-    replicas = ws > 1  # expert parallelism not yet wired: independent replicas, labelled
-    # inputs resident in HBM (generated on the device from the seeded recipe)
-    g = make_layer(n, d, f, do, T, cfg.dtype, "uniform", device=dev, seed_offset=rank)
+    use_ep = ws > 1 or args.ep
+    comm = 0
+    if use_ep:
+        import torch.distributed as tdist
+        if not tdist.is_initialized():  # --ep at N = 1: a 1-rank NCCL group (loopback)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29555")
+            tdist.init_process_group("nccl", rank=0, world_size=1)
+            dist = tdist
+        from paper_2205_01848_b200.dist import nccl_comm_ptr
+        comm = nccl_comm_ptr(device=dev)
+    # inputs resident in HBM (generated on the device from the seeded recipe); the expert
+    # weights are the same on every rank (same seeds), each rank's tokens differ
+    g = make_layer(n, d, f, do, T, cfg.dtype, "uniform", device=dev)
+    if rank:
+        g["x"] = make_layer(n, d, 64, do, T, cfg.dtype, "uniform", device=dev, seed_offset=rank)["x"]
     dy = make_dy(T, do, cfg.dtype, device=dev, seed_offset=rank)
-    layer = MoELayer(n, k, d, f, do, T, cfg.dtype, cfg.renormalize, device=dev)
-    layer.set_capacity_factors([alpha] * n, T)
+    layer = MoELayer(n, k, d, f, do, T, cfg.dtype, cfg.renormalize, world_size=ws if use_ep else 1,
+                     rank=rank if use_ep else 0, nccl_comm=comm, device=dev)
+    layer.set_capacity_factors([alpha] * n, T * (ws if use_ep else 1))
     tdt = layer.tdtype
     grads = dict(dx=torch.empty(T, d, dtype=tdt, device=dev),
                  dw_gate=torch.empty(n, d, dtype=tdt, device=dev),
@@ -180,7 +199,14 @@ def run_ours(args):
         step()
     torch.cuda.synchronize(dev)
     stats = layer.stats()
-    A = sum(min(c, cap) for c, cap in zip(stats["counts"], layer.capacities))
+    nl = n // (ws if use_ep else 1)
+    e_lo = (rank if use_ep else 0) * nl
+    # A: kept rows this GPU's expert GEMMs run over; A_tok: kept pairs of this GPU's tokens
+    A = sum(min(c, cap) for c, cap in list(zip(stats["counts"], layer.capacities))[e_lo:e_lo + nl])
+    layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"], y=y)
+    A_tok = int((layer.routing(T)["slot_of"] >= 0).sum().item())
+    layer.backward(dy, grads=grads)
+    torch.cuda.synchronize(dev)
 
     def barrier():
         if dist is not None:
@@ -220,7 +246,7 @@ def run_ours(args):
 
     # ---------------- per-kernel rooflines ----------------
     pk = peaks()
-    work = kernel_work(cfg, T, A, s)
+    work = kernel_work(cfg, T, A, s, A_tok)
     sm_peak_tf = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
     kernels = {}
     for name, (cnt, tot) in ktimes.items():
@@ -301,7 +327,8 @@ def run_ours(args):
                                    + (", cached assignments" if args.cached else ""),
                        "tokens_per_gpu": T, "n_experts": n, "top_k": k, "d_model": d, "d_ff": f,
                        "capacity_factor": alpha, "renormalize": cfg.renormalize,
-                       "parallelism": (f"replicas{ws} (EP pending)" if replicas else "1 GPU"),
+                       "parallelism": (f"ep{ws} (experts sharded, tokens data-parallel, NCCL)"
+                                       if use_ep else "1 GPU"),
                        "l2": "inputs > L2 (x 134 MB + weights 1 GB), no flush",
                        "kept_assignments": A, "drops": stats["drops"],
                        "padding_flops_avoided": padded_flops},

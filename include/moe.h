@@ -79,9 +79,15 @@ typedef struct {
                            every accumulator are fp32 */
   int32_t renormalize;  /* 1: Alg. 1 normalize (sum-norm of selected probs);
                            0: raw softmax probability (Switch-style) */
-  int32_t world_size;   /* expert-parallel group size (1 = single GPU) */
+  int32_t world_size;   /* expert-parallel group size R (n % R == 0) */
   int32_t rank;         /* experts [rank*n/R, (rank+1)*n/R) are local */
-  void*   nccl_comm;    /* ncclComm_t of the EP group (torch's communicator); NULL iff R == 1 */
+  void*   nccl_comm;    /* ncclComm_t of the EP group (e.g. torch ProcessGroupNCCL._comm_ptr()).
+                           NULL: single-GPU path (R must be 1).  Non-NULL: expert-parallel path
+                           (S8(e)): tokens data-parallel, equal T on every rank, global token
+                           index t_g = rank*T + t, GLOBAL capacity (reading 12), exchanges by
+                           grouped ncclSend/ncclRecv; R = 1 runs the same path as a loopback.
+                           Expert parameter / gradient tensors keep the full [n, ...] shape;
+                           only the local experts' slices are read and written. */
   void*   stream;       /* cudaStream_t all work is ordered on (NULL = legacy default) */
 } moe_config_t;
 
@@ -188,6 +194,19 @@ MOE_API moe_status_t moe_get_stats_async(moe_handle_t h, const moe_stats_t* dst)
 /* Synchronises the stream and reports (then clears) the device error flags:
    bit 0 = NaN gate logit, bit 1 = invalid cached index.  flags_out may be NULL. */
 MOE_API moe_status_t moe_check_device_flags(moe_handle_t h, int32_t* flags_out);
+
+/* Expert-parallel exchange plan (host only, no GPU): from the all-gathered pre-drop counts
+   cnt_all [R x n] (row r = rank r's tokens) and the global capacities cap [n], fills
+   pre_out [R x n]  global slot of rank r's first pair of expert e (= sum of lower ranks),
+   kl_out  [R x n]  kept pairs of rank r for expert e (min(cnt, max(0, cap - pre))),
+   send_off_out [n] this rank's send-buffer row offset per expert (prefix of kl[rank]),
+   kept_local_out [n/R] global kept count of this rank's experts, drops_out [1].
+   Rank r sends kl[r][e] rows to owner(e) = e / (n/R); the owner receives them at rows
+   base_e + pre[r][e] of expert e's region.  Any output pointer may be NULL. */
+MOE_API moe_status_t moe_ep_plan(int32_t R, int32_t rank, int32_t n, const int32_t* cnt_all,
+                                 const int32_t* cap, int32_t* pre_out, int32_t* kl_out,
+                                 int32_t* send_off_out, int32_t* kept_local_out,
+                                 int64_t* drops_out);
 
 /* Number of kernels the library launched since the handle was created (for bench
    accounting of "our kernels in the timed region"). */

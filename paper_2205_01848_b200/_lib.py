@@ -82,6 +82,9 @@ EXPORTS = {
     "moe_profile_enable": ([C.c_void_p, C.c_int32], C.c_int),
     "moe_profile_read": ([C.c_void_p, C.POINTER(KernelTime), C.c_int32, C.POINTER(C.c_int32),
                           C.c_int32], C.c_int),
+    "moe_ep_plan": ([C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                     C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                     C.POINTER(C.c_int32), C.POINTER(C.c_int64)], C.c_int),
     "moe_policy_create": ([C.POINTER(PolicyConfig), C.POINTER(C.c_int32), C.POINTER(C.c_void_p)],
                           C.c_int),
     "moe_policy_update": ([C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),

@@ -16,7 +16,11 @@ namespace moe {
 // (moe_set_capacities) is stream-ordered without any copy (S4.1).
 struct CapTable {
   int32_t cap[MOE_MAX_E];       // C_e (global capacity, reading 12)
-  int32_t base[MOE_MAX_E + 1];  // row offset of each LOCAL expert's region in the buffers
+  int32_t base[MOE_MAX_E + 1];  // row offset of each expert's rows in the buffer it indexes:
+                                //  GEMM side: LOCAL expert regions of X/H/O/dO/dX;
+                                //  token side (dispatch/combine): per global expert e, the
+                                //  row of global slot 0 (EP: send-buffer offset - pre[e])
+  int32_t pre[MOE_MAX_E];       // token side: global slot of this rank's first pair of e
 };
 
 template <typename T> struct Vec;  // 16-byte vector of T

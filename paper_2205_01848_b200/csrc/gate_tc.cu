@@ -677,8 +677,10 @@ int gate_dw_tc_splits(int T, int n, int d) {
 }
 
 cudaError_t launch_gate_dw_tc(const void* dlb, int maxT, int n_pad, const void* x, int T, int n,
-                              int d, float* partial, void* dwg, int accumulate, cudaStream_t s) {
+                              int d, float* partial, void* dwg, int accumulate, cudaStream_t s,
+                              float* f32_out) {
   const size_t count = (size_t)n * d;
+  if (f32_out && T == 0) return cudaMemsetAsync(f32_out, 0, count * 4, s);
   if (T == 0) {
     if (!accumulate) return cudaMemsetAsync(dwg, 0, count * 2, s);
     return cudaSuccess;
@@ -710,6 +712,7 @@ cudaError_t launch_gate_dw_tc(const void* dlb, int maxT, int n_pad, const void* 
 #undef GW
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (f32_out) return launch_reduce_partials(0, partial, splits, count, f32_out, 0, s);
   return launch_reduce_partials(1, partial, splits, count, dwg, accumulate, s);
 }
 

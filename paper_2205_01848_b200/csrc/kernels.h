@@ -49,9 +49,12 @@ cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, Rout
 cudaError_t launch_gate_dx(int dtype, const void* wg, const void* dxbuf, RouteBufs b, int T,
                            int k, int n, int d, const CapTable& ct, void* dx, int accumulate,
                            cudaStream_t s);
+// f32_out != null: write the fp32 sum there instead (EP: all-reduced before rounding)
 cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int n, int d,
                            float* partial, int splits, void* dwg, int accumulate,
-                           cudaStream_t s);
+                           cudaStream_t s, float* f32_out = nullptr);
+cudaError_t launch_f32_to(int dtype, const float* in, size_t count, void* out, int accumulate,
+                          cudaStream_t s);
 int gate_dw_splits(int T, int d);
 cudaError_t launch_reduce_partials(int dtype, const float* partial, int splits, size_t count,
                                    void* out, int accumulate, cudaStream_t s);

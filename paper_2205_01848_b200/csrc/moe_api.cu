@@ -16,13 +16,14 @@
 #include "gemm_tc.h"
 #include "gate_tc.h"
 #include "prof.h"
+#include "ep.h"
 #include <map>
 
 using namespace moe;
 
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
-      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, total;
+      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, ep_all, sendbuf, oret, dwg32, total;
 };
 
 struct moe_ctx {
@@ -33,7 +34,8 @@ struct moe_ctx {
   cudaStream_t stream = nullptr, side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<int32_t> cap;   // global capacities C_e (all n)
-  CapTable ct{};              // cap (all n) + base (local experts)
+  CapTable ct{};              // GEMM side: cap (all n) + base of LOCAL expert regions
+  CapTable cts{};             // token side (dispatch/combine/gate_dx): base/pre per global e
   int64_t rows = 0;           // total local buffer rows
   int max_cap_local = 0;
   Layout L{};
@@ -48,6 +50,9 @@ struct moe_ctx {
   int use_tc = 0;             // tcgen05 path for bf16 (env MOE_FORCE_SIMT=1 disables)
   TcPlan tc{};
   Prof prof;
+  int use_ep = 0;             // expert-parallel path (nccl_comm given; R may be 1 = loopback)
+  EpState* ep = nullptr;
+  EpPlan plan;
   std::string err;
 };
 
@@ -91,7 +96,7 @@ void compute_layout(moe_ctx* h) {
   L.tile_hist = take(ntiles * n * 4);
   L.tile_off = take(ntiles * n * 4);
   L.meta = take(4096);
-  L.token_of_slot = take((size_t)h->rows * 4);
+  L.token_of_slot = take(std::max<size_t>((size_t)h->rows, T * k) * 4);
   L.xbuf = take((size_t)h->rows * h->d * h->s);
   L.hbuf = take((size_t)h->rows * h->f * h->s);
   L.obuf = take((size_t)h->rows * h->dout * h->s);
@@ -100,6 +105,11 @@ void compute_layout(moe_ctx* h) {
   const size_t splits = std::max(gate_dw_splits(h->maxT, h->d), gate_dw_tc_splits(h->maxT, h->n, h->d));
   L.partial = take(splits * n * h->d * 4 + 4096);
   L.dlb = take(h->dtype == MOE_BF16 ? 2 * T * (size_t)h->n_pad * 2 : 0);
+  const bool ep = h->use_ep;
+  L.ep_all = take(ep ? (size_t)h->R * n * 4 : 0);
+  L.sendbuf = take(ep ? T * k * (size_t)std::max(h->d, h->dout) * h->s : 0);
+  L.oret = take(ep ? T * k * (size_t)h->dout * h->s : 0);
+  L.dwg32 = take(ep ? n * (size_t)h->d * 4 : 0);
   L.total = o;
 }
 
@@ -140,6 +150,8 @@ void relayout(moe_ctx* h) {
   }
   h->ct.base[h->n_local] = (int32_t)base;
   h->rows = base;
+  h->cts = h->ct;  // single GPU: token side indexes the same regions, pre = 0
+  for (int e = 0; e < MOE_MAX_E; ++e) h->cts.pre[e] = 0;
   compute_layout(h);
 }
 
@@ -179,6 +191,7 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
   if (c.world_size < 1 || c.rank < 0 || c.rank >= c.world_size) return MOE_ERR_INVALID_ARG;
   if (c.n_experts % c.world_size) return MOE_ERR_CONFIG;
   if (c.world_size > 1 && !c.nccl_comm) return MOE_ERR_INVALID_ARG;
+  if (c.n_experts / c.world_size > MOE_MAX_E) return MOE_ERR_CONFIG;
   moe_ctx* h = new moe_ctx();
   h->cfg = c;
   h->n = c.n_experts; h->k = c.top_k; h->d = c.d_model; h->f = c.d_ff; h->dout = dout;
@@ -196,15 +209,20 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
     delete h;
     return MOE_ERR_CUDA;
   }
+  h->use_ep = c.nccl_comm ? 1 : 0;
   // default capacities: Eq. 4 with alpha = 1 over the global token count
   h->cap.assign(h->n, 1);
   std::vector<double> a(h->n, 1.0);
   moe_capacity_from_factors(h->n, tokens_global(h), h->k, a.data(), h->cap.data());
   for (auto& v : h->cap) v = (int32_t)std::min<int64_t>(v, std::max<int64_t>(1, tokens_global(h)));
   relayout(h);
-  if (h->R > 1) {  // expert parallelism lands in its own milestone
-    delete h;
-    return MOE_ERR_CONFIG;
+  if (c.nccl_comm) {
+    h->use_ep = 1;
+    moe_status_t st = ep_create(&h->ep, c.nccl_comm, h->R, h->rank, &h->err);
+    if (st != MOE_OK) {
+      delete h;
+      return st;
+    }
   }
   *out = h;
   return MOE_OK;
@@ -213,6 +231,7 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
 moe_status_t moe_destroy(moe_handle_t h) {
   if (!h) return MOE_ERR_INVALID_ARG;
   if (h->side) cudaStreamSynchronize(h->side);
+  if (h->ep) ep_destroy(h->ep);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->side) cudaStreamDestroy(h->side);
@@ -314,8 +333,34 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   }
   KL(h, T > 0, "route_hist", sd, launch_route_hist(rb.idx, T, k, n, rb.tile_hist, sd));
   KL(h, 1, "route_scan", sd, launch_route_scan(rb.tile_hist, ntiles, n, h->ct, rb, sd));
-  KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->ct, rb, X, sd));
-  KL(h, 1, "zero_pad", sd, launch_zero_pad(dt, X, d, rb.kept, n, h->ct, sd));
+  if (!h->use_ep) {
+    KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->cts, rb, X, sd));
+  } else {
+    // C1 + the single host sync of EP v1: all-gather the per-rank pre-drop counts, then every
+    // rank derives the same global slot offsets, kept counts and message sizes (reading 12).
+    std::string err;
+    moe_status_t st = ep_exchange_counts(h->ep, rb.counts, (int32_t*)(ws + h->L.ep_all), n,
+                                         h->cap.data(), sd, h->plan, &err);
+    if (st != MOE_OK) return fail(h, st, err);
+    const EpPlan& P = h->plan;
+    for (int e = 0; e < n; ++e) {
+      h->cts.pre[e] = P.pre[(size_t)h->rank * n + e];
+      h->cts.base[e] = P.send_off[e] - h->cts.pre[e];
+    }
+    // device copies of the global routing statistics and local GEMM tile tables
+    int64_t drops = P.drops;
+    CUDA_TRY(h, cudaMemcpyAsync(rb.counts, P.counts.data(), 4 * n, cudaMemcpyHostToDevice, sd));
+    CUDA_TRY(h, cudaMemcpyAsync(rb.kept, P.kept_local.data(), 4 * h->n_local, cudaMemcpyHostToDevice, sd));
+    CUDA_TRY(h, cudaMemcpyAsync(rb.mtile_prefix, P.mtile_prefix.data(), 4 * (h->n_local + 1),
+                                cudaMemcpyHostToDevice, sd));
+    CUDA_TRY(h, cudaMemcpyAsync(rb.drops, &drops, 8, cudaMemcpyHostToDevice, sd));
+    void* sendbuf = ws + h->L.sendbuf;
+    KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, (int64_t)h->rank * T,
+                                                 h->cts, rb, sendbuf, sd));
+    st = ep_to_experts(h->ep, P, sendbuf, X, h->ct, d, (int)h->s, sd, &err);   // C2
+    if (st != MOE_OK) return fail(h, st, err);
+  }
+  KL(h, 1, "zero_pad", sd, launch_zero_pad(dt, X, d, rb.kept, h->n_local, h->ct, sd));
   // expert FFN: H = relu(X W1^T + b1); O = H W2^T + b2 over kept_e rows per local expert
   const int nl = h->n_local;
   const char* w1 = (const char*)a->w1 + (size_t)h->e_lo * f * d * h->s;
@@ -336,6 +381,13 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     KL(h, 1, "ffn_gemm2", sd, launch_gemm_simt_mgroup(dt, H, f, w2, 1, (int64_t)dout * f, b2, O, dout, dout, f,
                                      kept_local, nl, h->ct, h->max_cap_local, EPI_BIAS, sd));
   }
+  void* O_tok = O;  // expert outputs as the token side indexes them
+  if (h->use_ep) {
+    std::string err;
+    O_tok = ws + h->L.oret;
+    moe_status_t st = ep_from_experts(h->ep, h->plan, O, O_tok, h->ct, dout, (int)h->s, sd, &err);  // C3
+    if (st != MOE_OK) return fail(h, st, err);
+  }
   if (cached) {
     if (h->use_tc)
       KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, h->cached, rb, s0));
@@ -344,7 +396,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     CUDA_TRY(h, cudaEventRecord(h->ev_join, sd));
     CUDA_TRY(h, cudaStreamWaitEvent(s0, h->ev_join, 0));
   }
-  KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O, rb, T, k, dout, h->ct, a->y, s0));
+  KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O_tok, rb, T, k, dout, h->cts, a->y, s0));
   h->fa = *a;
   h->T_last = T;
   h->have_fwd = 1;
@@ -372,8 +424,15 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
 
   // K6 combine backward -> dO rows (local or, in EP, returned to the expert owners), dw, dl
   void* dlb = h->use_tc ? (void*)(ws + h->L.dlb) : nullptr;
-  KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O, rb, T, k, n, dout, h->renorm, h->ct, dO,
-                                                     dlb, h->maxT, h->n_pad, s0));
+  void* O_tok = h->use_ep ? (void*)(ws + h->L.oret) : O;
+  void* dO_tok = h->use_ep ? (void*)(ws + h->L.sendbuf) : dO;
+  std::string err;
+  KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O_tok, rb, T, k, n, dout, h->renorm, h->cts,
+                                                     dO_tok, dlb, h->maxT, h->n_pad, s0));
+  if (h->use_ep) {  // C4: dO rows to the expert owners
+    moe_status_t st = ep_to_experts(h->ep, h->plan, dO_tok, dO, h->ct, dout, (int)h->s, s0, &err);
+    if (st != MOE_OK) return fail(h, st, err);
+  }
   KL(h, 1, "zero_pad", s0, launch_zero_pad(dt, dO, dout, kept_local, nl, h->ct, s0));
   const char* w1 = (const char*)fa.w1 + (size_t)h->e_lo * f * d * h->s;
   const char* w2 = (const char*)fa.w2 + (size_t)h->e_lo * dout * f * h->s;
@@ -403,21 +462,33 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                                      kept_local, nl, h->ct, h->max_cap_local, EPI_NONE, s0));
   }
   // B4: dx = gather(dX) + dl W_g ;  B5: dW_g = dl^T x
+  void* dX_tok = dXb;
+  if (h->use_ep) {  // C5: dX rows back to the token owners (send layout, reuses the send buffer)
+    dX_tok = ws + h->L.sendbuf;
+    moe_status_t st = ep_from_experts(h->ep, h->plan, dXb, dX_tok, h->ct, d, (int)h->s, s0, &err);
+    if (st != MOE_OK) return fail(h, st, err);
+  }
   if (a->dx) {
     if (h->use_tc)
-      KL(h, T > 0, "gate_dx", s0, launch_gate_dx_tc(fa.w_gate, dXb, dlb, h->maxT, h->n_pad, rb, T, k, n, d,
-                                                    h->ct, a->dx, acc, s0));
+      KL(h, T > 0, "gate_dx", s0, launch_gate_dx_tc(fa.w_gate, dX_tok, dlb, h->maxT, h->n_pad, rb, T, k, n, d,
+                                                    h->cts, a->dx, acc, s0));
     else
-      KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dXb, rb, T, k, n, d, h->ct, a->dx, acc, s0));
+      KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dX_tok, rb, T, k, n, d, h->cts, a->dx, acc, s0));
   }
   if (a->dw_gate) {
+    float* f32 = h->use_ep ? (float*)(ws + h->L.dwg32) : nullptr;  // EP: all-reduce in fp32
     if (h->use_tc) {
       KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw_tc(dlb, h->maxT, h->n_pad, fa.x, T, n, d,
-                                                            (float*)(ws + h->L.partial), a->dw_gate, acc, s0));
+                                                            (float*)(ws + h->L.partial), a->dw_gate, acc, s0, f32));
     } else {
       int splits = gate_dw_splits(h->maxT, d);
       KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw(dt, rb.dl, fa.x, T, n, d, (float*)(ws + h->L.partial),
-                                          splits, a->dw_gate, acc, s0));
+                                          splits, a->dw_gate, acc, s0, f32));
+    }
+    if (h->use_ep) {  // C6
+      moe_status_t st = ep_allreduce_f32(h->ep, f32, (size_t)n * d, s0, &err);
+      if (st != MOE_OK) return fail(h, st, err);
+      KL(h, 1, "gate_dw", s0, launch_f32_to(dt, f32, (size_t)n * d, a->dw_gate, acc, s0));
     }
   }
   h->have_fwd = 0;  // H has been consumed
@@ -510,6 +581,21 @@ moe_status_t moe_profile_read(moe_handle_t h, moe_kernel_time_t* out, int32_t ma
   }
   *count = c;
   if (reset) h->prof.reset();
+  return MOE_OK;
+}
+
+moe_status_t moe_ep_plan(int32_t R, int32_t rank, int32_t n, const int32_t* cnt_all,
+                         const int32_t* cap, int32_t* pre_out, int32_t* kl_out,
+                         int32_t* send_off_out, int32_t* kept_local_out, int64_t* drops_out) {
+  if (R < 1 || rank < 0 || rank >= R || n < 1 || n % R || !cnt_all || !cap)
+    return MOE_ERR_INVALID_ARG;
+  EpPlan P;
+  ep_make_plan(P, R, rank, n, cnt_all, cap);
+  if (pre_out) std::memcpy(pre_out, P.pre.data(), 4 * (size_t)R * n);
+  if (kl_out) std::memcpy(kl_out, P.kl.data(), 4 * (size_t)R * n);
+  if (send_off_out) std::memcpy(send_off_out, P.send_off.data(), 4 * (size_t)n);
+  if (kept_local_out) std::memcpy(kept_local_out, P.kept_local.data(), 4 * (size_t)P.n_local);
+  if (drops_out) *drops_out = P.drops;
   return MOE_OK;
 }
 

@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
         const int e = ev[r];
         int rank = __popc(masks[e][lt >> 5] & ((1u << (lt & 31)) - 1u));
         for (int q = 0; q < (lt >> 5); ++q) rank += __popc(masks[e][q]);
-        const int slot = tile_off[(size_t)tile * n + e] + rank;
+        const int slot = ct.pre[e] + tile_off[(size_t)tile * n + e] + rank;
         const bool keep = slot < ct.cap[e];
         slot_of[(size_t)t * k + r] = keep ? slot : -1;
         if (keep) {
@@ -717,8 +717,9 @@ int gate_dw_splits(int T, int d) {
 
 cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int n, int d,
                            float* partial, int splits, void* dwg, int accumulate,
-                           cudaStream_t s) {
+                           cudaStream_t s, float* f32_out) {
   size_t count = (size_t)n * d;
+  if (f32_out && T == 0) return cudaMemsetAsync(f32_out, 0, count * 4, s);
   if (T == 0) {
     if (!accumulate) return cudaMemsetAsync(dwg, 0, count * (dtype == 1 ? 2 : 4), s);
     return cudaSuccess;
@@ -746,13 +747,27 @@ cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int
 #undef GDW_CASE
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
+  if (f32_out) return launch_reduce_partials(0, partial, splits, count, f32_out, 0, s);
+  return launch_reduce_partials(dtype, partial, splits, count, dwg, accumulate, s);
+}
+
+template <typename T>
+__global__ void f32_to_kernel(const float* __restrict__ in, size_t count, T* __restrict__ out,
+                              int accumulate) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  float v = in[i];
+  if (accumulate) v += to_f(out[i]);
+  out[i] = from_f<T>(v);
+}
+
+cudaError_t launch_f32_to(int dtype, const float* in, size_t count, void* out, int accumulate,
+                          cudaStream_t s) {
   int rb = (int)((count + 255) / 256);
   if (dtype == 1)
-    reduce_partials_kernel<__nv_bfloat16><<<rb, 256, 0, s>>>(partial, splits, count,
-                                                             (__nv_bfloat16*)dwg, accumulate);
+    f32_to_kernel<__nv_bfloat16><<<rb, 256, 0, s>>>(in, count, (__nv_bfloat16*)out, accumulate);
   else
-    reduce_partials_kernel<float><<<rb, 256, 0, s>>>(partial, splits, count, (float*)dwg,
-                                                     accumulate);
+    f32_to_kernel<float><<<rb, 256, 0, s>>>(in, count, (float*)out, accumulate);
   return cudaGetLastError();
 }
 

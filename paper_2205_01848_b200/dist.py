@@ -1,0 +1,23 @@
+"""Process-group plumbing for expert parallelism: hand torch's NCCL communicator to the C ABI.
+
+torch creates NCCL communicators lazily; one small collective forces creation, after which
+ProcessGroupNCCL._comm_ptr() is the ncclComm_t the library enqueues its exchanges on.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def nccl_comm_ptr(group=None, device=None) -> int:
+    """ncclComm_t (as an int) of `group` (default: WORLD) for `device` (default: current)."""
+    group = group or dist.group.WORLD
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    t = torch.zeros(1, device=dev)
+    dist.all_reduce(t, group=group)          # forces communicator creation
+    torch.cuda.synchronize(dev)
+    backend = group._get_backend(dev)
+    ptr = backend._comm_ptr()
+    if not ptr:
+        raise RuntimeError("ProcessGroupNCCL returned a null communicator")
+    return int(ptr)
