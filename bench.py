@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--cached", action="store_true", help="sample-assignment caching (c5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1024)
+    ap.add_argument("--cpu-sample", type=int, default=8192)
     ap.add_argument("--ep", action="store_true",
                     help="force the expert-parallel (NCCL) path at N=1 (loopback)")
     return ap.parse_args()
