@@ -110,7 +110,7 @@ __device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
 // ======================================================================================
 // K1: gate forward + fused softmax / top-k / normalize epilogue
 // ======================================================================================
-template <int BN, int STAGES>
+template <int BN, int STAGES, int KM>
 __global__ void __launch_bounds__(G_THREADS, 1)
     gate_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmX,
                        const __grid_constant__ CUtensorMap tmW, GateFwdParams p, int K) {
@@ -180,21 +180,25 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       tc_fence_after();
       const int t = tile * TC_BM + q * 32 + lane;
       const bool valid = t < p.T;
-      float sel_v[MOE_MAX_K];
-      int sel_e[MOE_MAX_K];
-      int cidx[MOE_MAX_K];
-      float cval[MOE_MAX_K];
+      // KM = compile-time bound on k: every per-row array below is indexed with unrolled
+      // (constant) indices, so it lives in registers
+      float sel_v[KM];
+      int sel_e[KM];
+      int cidx[KM];
+      float cval[KM];
 #pragma unroll
-      for (int r = 0; r < MOE_MAX_K; ++r) {
+      for (int r = 0; r < KM; ++r) {
         sel_v[r] = 0.f;
         sel_e[r] = -1;
         cidx[r] = -1;
         cval[r] = 0.f;
       }
       if (valid && p.cached) {
-        for (int r = 0; r < k; ++r) cidx[r] = p.cached[(size_t)t * k + r];
+#pragma unroll
+        for (int r = 0; r < KM; ++r)
+          if (r < k) cidx[r] = p.cached[(size_t)t * k + r];
       }
-      float m_run = -INFINITY, s_run = 0.f;
+      float m_run = -INFINITY;
       bool nan_seen = false;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       float* lrow = p.logits + (size_t)t * n;
@@ -204,78 +208,108 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         uint32_t r32[32];
         tmem_ld32(taddr + c * 32, r32);
         if (!valid) continue;
+        if ((n & 3) == 0 && c * 32 + 32 <= n) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<uint4*>(lrow + c * 32 + j) = make_uint4(r32[j], r32[j + 1], r32[j + 2], r32[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j < n) lrow[c * 32 + j] = __uint_as_float(r32[j]);
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int e = c * 32 + j;
-          if (e >= n) break;
+          if (e < n) {
           const float v = __uint_as_float(r32[j]);
-          lrow[e] = v;
           nan_seen |= (v != v);
-          // streaming top-k, strict '>' keeps the lower index first among equals
-          if (sel_e[k - 1] < 0 || v > sel_v[k - 1]) {
-            int pos = k - 1;
-            while (pos > 0 && (sel_e[pos - 1] < 0 || v > sel_v[pos - 1])) {
-              sel_v[pos] = sel_v[pos - 1];
-              sel_e[pos] = sel_e[pos - 1];
-              --pos;
+          // streaming top-k in ascending expert order: a strictly larger value displaces and
+          // the displaced entry bubbles down, so equal values keep the lower index first
+          // (once inserted, every later entry shifts down by one: the displaced entry ranks
+          // above all entries after it, ties included)
+          float cv = v;
+          int ce = e;
+          bool ins = false;
+#pragma unroll
+          for (int pos = 0; pos < KM; ++pos) {
+            if (pos < k && (ins || sel_e[pos] < 0 || cv > sel_v[pos])) {
+              ins = true;
+              const float tv = sel_v[pos];
+              const int te = sel_e[pos];
+              sel_v[pos] = cv;
+              sel_e[pos] = ce;
+              cv = tv;
+              ce = te;
             }
-            sel_v[pos] = v;
-            sel_e[pos] = e;
           }
-          // online softmax denominator
-          if (v > m_run) {
-            s_run = s_run * expf(m_run - v) + 1.f;
-            m_run = v;
-          } else {
-            s_run += expf(v - m_run);
-          }
-          for (int r = 0; r < k; ++r)
+          m_run = fmaxf(m_run, v);  // row max for the raw-probability denominator
+#pragma unroll
+          for (int r = 0; r < KM; ++r)
             if (cidx[r] == e) cval[r] = v;
+          }
         }
       }
       tc_fence_before();
       mbar_arrive(&b.tempty[acc]);
       if (valid) {
         if (nan_seen) atomicOr(p.flags, 1);
-        int use[MOE_MAX_K];
-        float lv[MOE_MAX_K];
+        float lv[KM];
+        int use[KM];
         if (p.cached) {
           bool ok = true;
-          for (int r = 0; r < k; ++r) {
+#pragma unroll
+          for (int r = 0; r < KM; ++r) {
+            if (r >= k) break;
             ok &= (cidx[r] >= 0 && cidx[r] < n);
+#pragma unroll
             for (int q2 = 0; q2 < r; ++q2) ok &= (cidx[q2] != cidx[r]);
           }
           if (!ok) atomicOr(p.flags, 2);
           bool same = true;
-          for (int r = 0; r < k; ++r) {
+#pragma unroll
+          for (int r = 0; r < KM; ++r) {
+            if (r >= k) break;
             bool found = false;
-            for (int q2 = 0; q2 < k; ++q2) found |= (cidx[r] == sel_e[q2]);
+#pragma unroll
+            for (int q2 = 0; q2 < KM; ++q2) found |= (q2 < k && cidx[r] == sel_e[q2]);
             same &= found;
           }
           if (same && ok) atomicAdd(p.hit, 1);
-          for (int r = 0; r < k; ++r) {
+#pragma unroll
+          for (int r = 0; r < KM; ++r) {
             use[r] = ok ? cidx[r] : sel_e[r];
             lv[r] = ok ? cval[r] : sel_v[r];
           }
         } else {
-          for (int r = 0; r < k; ++r) {
+#pragma unroll
+          for (int r = 0; r < KM; ++r) {
             use[r] = sel_e[r];
             lv[r] = sel_v[r];
           }
         }
+        (void)use;
         int32_t* orow = p.idx_out + (size_t)t * k;
-        for (int r = 0; r < k; ++r) orow[r] = sel_e[r];
         float* wrow = p.w_out + (size_t)t * k;
+        // raw mode: p_i = exp(l_i - max) / sum_e exp(l_e - max), the row re-read from L1/L2
         if (p.renorm) {
           float m = lv[0];
-          for (int r = 1; r < k; ++r) m = fmaxf(m, lv[r]);
-          float ev[MOE_MAX_K], s = 0.f;
-          for (int r = 0; r < k; ++r) { ev[r] = expf(lv[r] - m); s += ev[r]; }
-          for (int r = 0; r < k; ++r) wrow[r] = ev[r] / s;
+#pragma unroll
+          for (int r = 1; r < KM; ++r)
+            if (r < k) m = fmaxf(m, lv[r]);
+          float ev[KM], ssum = 0.f;
+#pragma unroll
+          for (int r = 0; r < KM; ++r)
+            if (r < k) { ev[r] = expf(lv[r] - m); ssum += ev[r]; }
+#pragma unroll
+          for (int r = 0; r < KM; ++r)
+            if (r < k) { wrow[r] = ev[r] / ssum; orow[r] = sel_e[r]; }
         } else {
-          for (int r = 0; r < k; ++r) wrow[r] = expf(lv[r] - m_run) / s_run;
+          float ssum = 0.f;
+          for (int e = 0; e < n; ++e) ssum += expf(lrow[e] - m_run);
+#pragma unroll
+          for (int r = 0; r < KM; ++r)
+            if (r < k) { wrow[r] = expf(lv[r] - m_run) / ssum; orow[r] = sel_e[r]; }
         }
-        (void)use;
       }
     }
   }
@@ -624,7 +658,10 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
   const int grid = MT < g_sms ? MT : g_sms;
 #define GF(BN, ST)                                                                       \
   {                                                                                      \
-    auto kf = gate_fwd_tc_kernel<BN, ST>;                                                \
+    auto kf = k == 1 ? gate_fwd_tc_kernel<BN, ST, 1>                                     \
+                     : (k == 2 ? gate_fwd_tc_kernel<BN, ST, 2>                           \
+                               : (k <= 4 ? gate_fwd_tc_kernel<BN, ST, 4>                 \
+                                         : gate_fwd_tc_kernel<BN, ST, 8>));              \
     size_t sm = smem_for((128 + BN) * 64 * 2, ST);                                       \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \

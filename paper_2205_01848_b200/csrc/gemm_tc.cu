@@ -306,8 +306,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         if (store) {
+          uint32_t bits = 0;
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) st_v4(crow + col0 + i, pack(v + i, __nv_bfloat16()));
+          for (int i = 0; i < 32; i += 8) {
+            const uint4 pk = pack(v + i, __nv_bfloat16());
+            st_v4(crow + col0 + i, pk);
+            const uint32_t w4[4] = {pk.x, pk.y, pk.z, pk.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              bits |= ((w4[j] & 0xffffu) != 0u ? 1u : 0u) << (i + 2 * j);
+              bits |= ((w4[j] >> 16) != 0u ? 1u : 0u) << (i + 2 * j + 1);
+            }
+          }
+          if (KIND == TC_FWD1 && p.mask)  // relu' bits for the 2-CTA DGRAD_A epilogue
+            p.mask[(size_t)(p.ct.base[e] + row) * (p.N >> 5) + (col0 >> 5)] = bits;
         }
       }
       tc_fence_before();
@@ -415,7 +427,8 @@ void tc_plan_free(TcPlan* p) { (void)p; }
 template <int KIND>
 static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, int N,
                            int n_local, const void* bias, void* C, int ldc, const int32_t* kept,
-                           const int32_t* prefix, const CapTable& ct, cudaStream_t s) {
+                           const int32_t* prefix, const CapTable& ct, cudaStream_t s,
+                           uint32_t* mask = nullptr) {
   CUtensorMap ma, mb;
   const int bn = pick_bn(N);
   const bool two = use_2cta(N, KIND);
@@ -427,6 +440,7 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   TcParams p{};
   p.kept = kept; p.mtile_prefix = prefix; p.n_local = n_local; p.M = 0; p.N = N; p.K = K;
   p.bias = (const __nv_bfloat16*)bias; p.C = (__nv_bfloat16*)C; p.ldc = ldc; p.ct = ct;
+  p.mask = mask;
   if (two)
     TC_CUDA(launch_tc2_kind(KIND, bn, ma, mb, p, g_num_sms & ~1, s));
   else
@@ -456,14 +470,15 @@ moe_status_t tc_ffn_forward(TcPlan* plan, void* X, const void* w1, const void* b
                             const void* w2, const void* b2, void* H, void* O, int64_t rows,
                             int d, int f, int dout, const int32_t* kept,
                             const int32_t* mtile_prefix, int n_local, const CapTable& ct,
-                            int max_cap, cudaStream_t s, int64_t* nlaunch, Prof* prof) {
+                            int max_cap, cudaStream_t s, int64_t* nlaunch, Prof* prof,
+                            uint32_t* mask) {
   (void)plan; (void)max_cap;
   if (!ensure_encode()) return MOE_ERR_CUDA;
   if (rows == 0 || n_local == 0) { *nlaunch = 0; return MOE_OK; }
   moe_status_t st;
   {
     ProfScope ps(prof, "ffn_gemm1", s);
-    st = mgroup<TC_FWD1>(X, rows, d, w1, f, n_local, b1, H, f, kept, mtile_prefix, ct, s);
+    st = mgroup<TC_FWD1>(X, rows, d, w1, f, n_local, b1, H, f, kept, mtile_prefix, ct, s, mask);
   }
   if (st != MOE_OK) return st;
   {
@@ -479,7 +494,7 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
                              int accumulate, int64_t rows, int d, int f, int dout,
                              const int32_t* kept, const int32_t* mtile_prefix, int n_local,
                              const CapTable& ct, int max_cap, cudaStream_t s,
-                             int64_t* nlaunch, Prof* prof) {
+                             int64_t* nlaunch, Prof* prof, uint32_t* mask) {
   (void)plan; (void)max_cap;
   if (!ensure_encode()) return MOE_ERR_CUDA;
   int64_t nl = 0;
@@ -498,7 +513,8 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   // dA = (dO W2_e) * 1[H > 0], W2_e stored [d_out x f] = [K x N]
   {
     ProfScope ps(prof, "dgrad_dA", s);
-    st = mgroup<TC_DGRAD_A>(dO, rows, dout, w2, f, n_local, nullptr, H, f, kept, mtile_prefix, ct, s);
+    st = mgroup<TC_DGRAD_A>(dO, rows, dout, w2, f, n_local, nullptr, H, f, kept, mtile_prefix, ct, s,
+                            mask);
   }
   if (st != MOE_OK) return st;
   ++nl;

@@ -20,7 +20,8 @@ moe_status_t tc_ffn_forward(TcPlan* p, void* X, const void* w1, const void* b1,
                             const void* w2, const void* b2, void* H, void* O, int64_t rows,
                             int d, int f, int dout, const int32_t* kept,
                             const int32_t* mtile_prefix, int n_local, const CapTable& ct,
-                            int max_cap, cudaStream_t s, int64_t* nlaunch, Prof* prof);
+                            int max_cap, cudaStream_t s, int64_t* nlaunch, Prof* prof,
+                            uint32_t* mask);
 // Backward: dW2 = dO^T H, db2 = sum dO; dA = (dO W2) * 1[H>0] (into H);
 // dW1 = dA^T X, db1 = sum dA; dX = dA W1.
 moe_status_t tc_ffn_backward(TcPlan* p, void* X, void* H, void* dO, void* dX, const void* w1,
@@ -28,6 +29,6 @@ moe_status_t tc_ffn_backward(TcPlan* p, void* X, void* H, void* dO, void* dX, co
                              int accumulate, int64_t rows, int d, int f, int dout,
                              const int32_t* kept, const int32_t* mtile_prefix, int n_local,
                              const CapTable& ct, int max_cap, cudaStream_t s,
-                             int64_t* nlaunch, Prof* prof);
+                             int64_t* nlaunch, Prof* prof, uint32_t* mask);
 
 }  // namespace moe

@@ -33,7 +33,7 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
@@ -42,7 +42,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) 
       "{\n"
       ".reg .pred p;\n"
       "WAITC_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAITC_%=;\n"
       "}\n" ::"r"(addr),
       "r"(parity)
@@ -316,7 +316,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       // Side inputs of the whole tile (bias, H mask, old gradient) are fetched BEFORE waiting
       // for the accumulator, so their DRAM/L2 latency overlaps this tile's MMAs.
       uint4 pre[CH][4];
-      const bool need_side = ((KIND == TC_FWD1 || KIND == TC_FWD2 || KIND == TC_DGRAD_A) && row_ok) ||
+      uint32_t mbits[CH];
+      uint32_t mout[CH];
+#pragma unroll
+      for (int cc = 0; cc < CH; ++cc) mout[cc] = 0u;
+      const int mask_ld = p.N >> 5;
+      uint32_t* mrow = p.mask ? p.mask + (size_t)(p.ct.base[e] + row) * mask_ld : nullptr;
+      if (KIND == TC_DGRAD_A && row_ok) {  // relu' mask bits written by FWD1 (not H itself)
+#pragma unroll
+        for (int cc = 0; cc < CH; ++cc) mbits[cc] = mrow[(n0 >> 5) + half * CH + cc];
+      }
+      const bool need_side = ((KIND == TC_FWD1 || KIND == TC_FWD2) && row_ok) ||
                              (KIND == TC_WGRAD && row_ok && p.accumulate);
       if (need_side) {
 #pragma unroll
@@ -368,13 +378,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           }
         } else if (KIND == TC_DGRAD_A) {
           if (row_ok) {
+            const uint32_t mb = mbits[cc];
 #pragma unroll
-            for (int i = 0; i < 32; i += 8) {
-              float h[8];
-              unpack(side[i / 8], h, __nv_bfloat16());
-#pragma unroll
-              for (int j = 0; j < 8; ++j) v[i + j] = h[j] > 0.f ? v[i + j] : 0.f;
-            }
+            for (int i = 0; i < 32; ++i) v[i] = ((mb >> i) & 1u) ? v[i] : 0.f;
           } else {
             store = row_pad;
 #pragma unroll
@@ -395,9 +401,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           }
         }
         if (store) {
+          uint4 pk[4];
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) st_v4(crow + col0 + i, pack(v + i, __nv_bfloat16()));
+          for (int i = 0; i < 4; ++i) {
+            pk[i] = pack(v + 8 * i, __nv_bfloat16());
+            st_v4(crow + col0 + 8 * i, pk[i]);
+          }
+          if (KIND == TC_FWD1) {  // bit j: the stored bf16 H is > 0 (relu output >= 0)
+            uint32_t bits = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t w4[4] = {pk[i].x, pk[i].y, pk[i].z, pk[i].w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t ne = __vsetne2(w4[j], 0u);  // 0x0001 per nonzero half
+                bits |= ((ne & 1u) | ((ne >> 15) & 2u)) << (8 * i + 2 * j);
+              }
+            }
+            mout[cc] = bits;
+          }
         }
+      }
+      if (KIND == TC_FWD1 && mrow && (row_ok || row_pad)) {  // one vector store per thread
+        uint32_t* mdst = mrow + (n0 >> 5) + half * CH;
+        if (CH == 4)
+          *reinterpret_cast<uint4*>(mdst) = make_uint4(mout[0], mout[1 % CH], mout[2 % CH], mout[3 % CH]);
+        else
+#pragma unroll
+          for (int cc = 0; cc < CH; ++cc) mdst[cc] = mout[cc];
       }
       tc_fence_before();
       __syncwarp();

@@ -23,6 +23,8 @@ struct TcParams {
   __nv_bfloat16* C;             // output base (buffer or weight-gradient tensor)
   int ldc;                      // leading dim of C (M-grouped buffers)
   int accumulate;               // WGRAD
+  uint32_t* mask;               // FWD1 writes / DGRAD_A reads: bit j of word [row][c] = (H > 0)
+                                // for column 32c + j (relu' mask, 16x fewer bytes than H)
   CapTable ct;                  // base rows of each local expert region
 };
 
