@@ -61,10 +61,11 @@ __device__ __forceinline__ uint4 pack(const float* f, __nv_bfloat16) {
                     pack_bf16x2(f[6], f[7]));
 }
 
+// streaming read-only load (not volatile: the compiler may batch and reorder these)
 __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
 __device__ __forceinline__ uint4 ld_v4(const void* p) {

@@ -384,10 +384,67 @@ cudaError_t launch_zero_pad(int dtype, void* buf, int cols, const int32_t* kept,
 
 // =====================================================================================
 // K5: combine (Alg. 1 l.8, Aggregate P:408): y[t] = sum_r [kept] w[t,r] O[row(t,r)],
-// r ascending, fp32 accumulate; warp per token, 16-byte vectors.
+// r ascending, fp32 accumulate; warp per token, 16-byte vectors.  VPL = 16-byte vectors per
+// lane per row (d_out*s/512), KM = compile-time bound on k: all of a token's row loads are
+// issued before the first use (two memory round trips per token: indices, then rows).
 // =====================================================================================
-template <typename T>
+template <typename T, int VPL, int KM>
 __global__ void __launch_bounds__(256) combine_fwd_kernel(
+    const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
+    const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
+    T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= Tn) return;
+  constexpr int VE = Vec<T>::N;
+  const int nvec = dout / VE;
+  int rows[KM];
+  float wr[KM];
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    rows[r] = -1;
+    wr[r] = 0.f;
+    if (r < k) {
+      const int sl = slot_of[(size_t)t * k + r];
+      if (sl >= 0) {
+        rows[r] = ct.base[idx[(size_t)t * k + r]] + sl;
+        wr[r] = w[(size_t)t * k + r];
+      }
+    }
+  }
+  T* yrow = y + (size_t)t * dout;
+  for (int vb = 0; vb < nvec; vb += VPL * 32) {
+  uint4 u[KM][VPL];
+#pragma unroll
+  for (int r = 0; r < KM; ++r)
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int v = vb + j * 32 + lane;
+      if (rows[r] >= 0 && v < nvec) u[r][j] = ld_nc_v4(obuf + (size_t)rows[r] * dout + (size_t)v * VE);
+    }
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int v = vb + j * 32 + lane;
+    if (v >= nvec) continue;
+    float acc[VE];
+#pragma unroll
+    for (int i = 0; i < VE; ++i) acc[i] = 0.f;
+#pragma unroll
+    for (int r = 0; r < KM; ++r) {
+      if (rows[r] < 0) continue;
+      float o[VE];
+      unpack(u[r][j], o, T());
+#pragma unroll
+      for (int i = 0; i < VE; ++i) acc[i] = fmaf(wr[r], o[i], acc[i]);
+    }
+    st_v4(yrow + (size_t)v * VE, pack(acc, T()));
+  }
+  }
+}
+
+// generic fallback (any d_out, any k): row loop
+template <typename T>
+__global__ void __launch_bounds__(256) combine_fwd_generic_kernel(
     const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
     T* __restrict__ y) {
@@ -423,25 +480,40 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
   }
 }
 
+template <typename T>
+static cudaError_t combine_fwd_t(const void* obuf, RouteBufs b, int T_, int k, int d_out,
+                                 const CapTable& ct, void* y, cudaStream_t s) {
+  dim3 grid((T_ + 7) / 8);
+  const int vpl = (d_out / Vec<T>::N + 31) / 32;
+#define CF(V, K)                                                                            \
+  combine_fwd_kernel<T, V, K><<<grid, 256, 0, s>>>((const T*)obuf, b.w, b.idx, b.slot_of, ct, \
+                                                   T_, k, d_out, (T*)y)
+  if (k <= 2) {
+    if (vpl <= 2) { if (k == 1) CF(2, 1); else CF(2, 2); }
+    else if (vpl <= 4) { if (k == 1) CF(4, 1); else CF(4, 2); }
+    else { if (k == 1) CF(8, 1); else CF(8, 2); }
+  } else {
+    combine_fwd_generic_kernel<T><<<grid, 256, 0, s>>>((const T*)obuf, b.w, b.idx, b.slot_of, ct,
+                                                       T_, k, d_out, (T*)y);
+  }
+#undef CF
+  return cudaGetLastError();
+}
+
 cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, int k,
                                int d_out, const CapTable& ct, void* y, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  dim3 grid((T + 7) / 8);
-  if (dtype == 1)
-    combine_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
-        (const __nv_bfloat16*)obuf, b.w, b.idx, b.slot_of, ct, T, k, d_out, (__nv_bfloat16*)y);
-  else
-    combine_fwd_kernel<float><<<grid, 256, 0, s>>>((const float*)obuf, b.w, b.idx, b.slot_of,
-                                                   ct, T, k, d_out, (float*)y);
-  return cudaGetLastError();
+  if (dtype == 1) return combine_fwd_t<__nv_bfloat16>(obuf, b, T, k, d_out, ct, y, s);
+  return combine_fwd_t<float>(obuf, b, T, k, d_out, ct, y, s);
 }
 
 // =====================================================================================
 // K6: combine backward.  dO[row] = w dy[t]; dw[t,r] = <dy[t], O[row]> (0 if dropped);
 // dl[t,:] closed form: renorm dl[i_r] = w_r (dw_r - sum w dw), 0 elsewhere;
-// raw dl_j = p_j (dp_j - sum_r w_r dw_r) with dp_j = dw_r at j = i_r.  Warp per token.
+// raw dl_j = p_j (dp_j - sum_r w_r dw_r) with dp_j = dw_r at j = i_r.  Warp per token; the
+// logits, dy and O rows are all requested before the first use.
 // =====================================================================================
-template <typename T>
+template <typename T, int VPL, int KM>
 __global__ void __launch_bounds__(256) combine_bwd_kernel(
     const T* __restrict__ dy, const T* __restrict__ obuf, const float* __restrict__ w,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of,
@@ -451,76 +523,147 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
-  int rows[MOE_MAX_K];
-  float wr[MOE_MAX_K], part[MOE_MAX_K];
-  int er[MOE_MAX_K];
-  for (int r = 0; r < k; ++r) {
-    int sl = slot_of[(size_t)t * k + r];
-    er[r] = idx[(size_t)t * k + r];
-    rows[r] = sl >= 0 ? ct.base[er[r]] + sl : -1;
-    wr[r] = w[(size_t)t * k + r];
-    part[r] = 0.f;
-  }
   constexpr int VE = Vec<T>::N;
+  constexpr int NL = MOE_MAX_E / 64;  // expert pairs per lane (n <= 256)
   const int nvec = dout / VE;
+  int rows[KM], er[KM];
+  float wr[KM], part[KM];
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    rows[r] = -1; er[r] = -1; wr[r] = 0.f; part[r] = 0.f;
+    if (r < k) {
+      const int sl = slot_of[(size_t)t * k + r];
+      er[r] = idx[(size_t)t * k + r];
+      rows[r] = sl >= 0 ? ct.base[er[r]] + sl : -1;
+      wr[r] = w[(size_t)t * k + r];
+    }
+  }
+  // this lane's experts: pairs e = 2*lane + 64*j (+1)
+  float lg[NL][2];
+  const float* l = logits + (size_t)t * n;
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const int e = 2 * lane + 64 * j;
+    lg[j][0] = (!renorm && e < n) ? l[e] : -INFINITY;
+    lg[j][1] = (!renorm && e + 1 < n) ? l[e + 1] : -INFINITY;
+  }
   const T* dyrow = dy + (size_t)t * dout;
-  for (int v = lane; v < nvec; v += 32) {
-    float g[VE];
-    unpack(ld_nc_v4(dyrow + (size_t)v * VE), g, T());
-    for (int r = 0; r < k; ++r) {
+  for (int vb = 0; vb < nvec; vb += VPL * 32) {  // one pass for d_out*s <= 512*VPL bytes
+  uint4 g[VPL];
+  uint4 u[KM][VPL];
+#pragma unroll
+  for (int jv = 0; jv < VPL; ++jv) {
+    const int v = vb + jv * 32 + lane;
+    if (v < nvec) g[jv] = ld_nc_v4(dyrow + (size_t)v * VE);
+  }
+#pragma unroll
+  for (int r = 0; r < KM; ++r)
+#pragma unroll
+    for (int jv = 0; jv < VPL; ++jv) {
+      const int v = vb + jv * 32 + lane;
+      if (rows[r] >= 0 && v < nvec) u[r][jv] = ld_nc_v4(obuf + (size_t)rows[r] * dout + (size_t)v * VE);
+    }
+#pragma unroll
+  for (int jv = 0; jv < VPL; ++jv) {
+    const int v = vb + jv * 32 + lane;
+    if (v >= nvec) continue;
+    float gv[VE];
+    unpack(g[jv], gv, T());
+#pragma unroll
+    for (int r = 0; r < KM; ++r) {
       if (rows[r] < 0) continue;
       float o[VE], dov[VE];
-      unpack(ld_nc_v4(obuf + (size_t)rows[r] * dout + (size_t)v * VE), o, T());
+      unpack(u[r][jv], o, T());
 #pragma unroll
       for (int i = 0; i < VE; ++i) {
-        part[r] = fmaf(g[i], o[i], part[r]);
-        dov[i] = wr[r] * g[i];
+        part[r] = fmaf(gv[i], o[i], part[r]);
+        dov[i] = wr[r] * gv[i];
       }
       st_v4(dobuf + (size_t)rows[r] * dout + (size_t)v * VE, pack(dov, T()));
     }
   }
-  float dwr[MOE_MAX_K];
+  }
+  float dwr[KM];
   float c = 0.f;
-  for (int r = 0; r < k; ++r) {
-    float s = warp_sum(part[r]);
-    s = __shfl_sync(0xffffffffu, s, 0);
-    dwr[r] = rows[r] >= 0 ? s : 0.f;
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    float sr = warp_sum(part[r]);
+    sr = __shfl_sync(0xffffffffu, sr, 0);
+    dwr[r] = rows[r] >= 0 ? sr : 0.f;
     c = fmaf(wr[r], dwr[r], c);
   }
-  if (lane < k) dw[(size_t)t * k + lane] = dwr[0 + lane];  // note: lane < k <= 8
-  float* dlrow = dl + (size_t)t * n;
+#pragma unroll
+  for (int r = 0; r < KM; ++r)
+    if (r < k && lane == r) dw[(size_t)t * k + r] = dwr[r];
   float m = -INFINITY, sp = 0.f;
-  const float* l = logits + (size_t)t * n;
   if (!renorm) {
-    for (int e = lane; e < n; e += 32) m = fmaxf(m, l[e]);
+#pragma unroll
+    for (int j = 0; j < NL; ++j) m = fmaxf(m, fmaxf(lg[j][0], lg[j][1]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    for (int e = lane; e < n; e += 32) sp += expf(l[e] - m);
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int e = 2 * lane + 64 * j;
+      if (e < n) sp += expf(lg[j][0] - m);
+      if (e + 1 < n) sp += expf(lg[j][1] - m);
+    }
     sp = __shfl_sync(0xffffffffu, warp_sum(sp), 0);
   }
+  float* dlrow = dl + (size_t)t * n;
   const int ncols = dlb ? n_pad : n;
-  for (int e = lane; e < ncols; e += 32) {
-    float v = 0.f;
-    if (e < n) {
-      if (renorm) {
-        for (int r = 0; r < k; ++r)
-          if (er[r] == e) v = wr[r] * (dwr[r] - c);
-      } else {
-        const float p = expf(l[e] - m) / sp;
-        float dp = 0.f;
-        for (int r = 0; r < k; ++r)
-          if (er[r] == e) dp = dwr[r];
-        v = p * (dp - c);
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const int e0 = 2 * lane + 64 * j;
+    if (e0 >= ncols) continue;
+    float v2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = e0 + h;
+      float v = 0.f;
+      if (e < n) {
+        if (renorm) {
+#pragma unroll
+          for (int r = 0; r < KM; ++r)
+            if (er[r] == e) v = wr[r] * (dwr[r] - c);
+        } else {
+          const float p = expf(lg[j][h] - m) / sp;
+          float dp = 0.f;
+#pragma unroll
+          for (int r = 0; r < KM; ++r)
+            if (er[r] == e) dp = dwr[r];
+          v = p * (dp - c);
+        }
+        dlrow[e] = v;
       }
-      dlrow[e] = v;
+      v2[h] = v;
     }
     if (dlb) {  // exact-ish bf16 pair for the tensor-core gate gradients: v = hi + lo
-      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-      const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-      dlb[(size_t)t * n_pad + e] = hi;
-      dlb[((size_t)maxT + t) * n_pad + e] = lo;
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(v2[0], v2[1]);
+      const __nv_bfloat162 lo =
+          __floats2bfloat162_rn(v2[0] - __low2float(hi), v2[1] - __high2float(hi));
+      *reinterpret_cast<__nv_bfloat162*>(dlb + (size_t)t * n_pad + e0) = hi;
+      *reinterpret_cast<__nv_bfloat162*>(dlb + ((size_t)maxT + t) * n_pad + e0) = lo;
     }
   }
+}
+
+template <typename T>
+static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, int T_, int k,
+                                 int n, int d_out, int renorm, const CapTable& ct, void* dobuf,
+                                 void* dlb, int maxT, int n_pad, cudaStream_t s) {
+  dim3 grid((T_ + 7) / 8);
+  const int vpl = (d_out / Vec<T>::N + 31) / 32;  // > 8: the kernel loops over 4 KB blocks
+#define CB(V, K)                                                                               \
+  combine_bwd_kernel<T, V, K><<<grid, 256, 0, s>>>((const T*)dy, (const T*)obuf, b.w, b.idx,   \
+                                                   b.slot_of, b.logits, ct, T_, k, n, d_out,   \
+                                                   renorm, (T*)dobuf, b.dw, b.dl,              \
+                                                   (__nv_bfloat16*)dlb, maxT, n_pad)
+  const int km = k == 1 ? 1 : (k == 2 ? 2 : 8);
+  if (vpl <= 2) { if (km == 1) CB(2, 1); else if (km == 2) CB(2, 2); else CB(2, 8); }
+  else if (vpl <= 4) { if (km == 1) CB(4, 1); else if (km == 2) CB(4, 2); else CB(4, 8); }
+  else { if (km == 1) CB(8, 1); else if (km == 2) CB(8, 2); else CB(8, 8); }
+#undef CB
+  return cudaGetLastError();
 }
 
 cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, RouteBufs b,
@@ -528,18 +671,10 @@ cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, Rout
                                const CapTable& ct, void* dobuf, void* dlb, int maxT, int n_pad,
                                cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  dim3 grid((T + 7) / 8);
   if (dtype == 1)
-    combine_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
-        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)obuf, b.w, b.idx, b.slot_of, b.logits,
-        ct, T, k, n, d_out, renorm, (__nv_bfloat16*)dobuf, b.dw, b.dl, (__nv_bfloat16*)dlb, maxT,
-        n_pad);
-  else
-    combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dy, (const float*)obuf, b.w,
-                                                   b.idx, b.slot_of, b.logits, ct, T, k, n,
-                                                   d_out, renorm, (float*)dobuf, b.dw, b.dl,
-                                                   (__nv_bfloat16*)dlb, maxT, n_pad);
-  return cudaGetLastError();
+    return combine_bwd_t<__nv_bfloat16>(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf, dlb,
+                                        maxT, n_pad, s);
+  return combine_bwd_t<float>(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf, dlb, maxT, n_pad, s);
 }
 
 // =====================================================================================
