@@ -393,12 +393,24 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
     }
     __syncwarp();
   } else if (warp >= 4) {
-    const int q = warp & 3;
+    // Epilogue: warp (q, half) owns token rows 32q..32q+31 (its TMEM lanes) x HC columns.
+    // The gathered dX rows and the dx output go through a per-warp shared-memory staging
+    // buffer so every global access is a coalesced 16-byte-per-lane row segment
+    // (a thread-per-row access pattern would touch 32 rows per instruction).
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    constexpr int HC = BN / 2;    // columns per warp
+    constexpr int RB = HC * 2;    // bytes of one row segment
+    constexpr int RS = RB + 16;   // padded staging stride (conflict-free 16-B row reads)
+    constexpr int LPR = RB / 16;  // lanes per row segment
+    constexpr int RPI = 32 / LPR; // rows per cooperative instruction
+    uint8_t* stg = smem + STAGES * STAGE_BYTES + 256 + (warp - 4) * 32 * RS;
+    const int sub = lane / LPR, seg = lane % LPR;
     int it = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
       const int acc = it & 1;
       const int mt = tile % MT, nt = tile / MT;
-      const int t = mt * TC_BM + q * 32 + lane;
+      const int t0w = mt * TC_BM + q * 32;
+      const int t = t0w + lane;
       const bool valid = t < p.T;
       int rows[MOE_MAX_K];
       int nr = 0;
@@ -408,72 +420,70 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
           if (sl >= 0) rows[nr++] = p.ct.base[p.idx[(size_t)t * p.k + r]] + sl;
         }
       }
-      const int half = (warp - 4) >> 2;
-      constexpr int CH = BN / 64;
-      // prefetch the first gathered dX row of every chunk before waiting for the MMA
-      uint4 pre[CH][4];
-      if (nr > 0) {
+      const int maxnr = __reduce_max_sync(0xffffffffu, nr);
+      const int col_base = nt * BN + half * HC;
+      float v[HC];
 #pragma unroll
-        for (int cc = 0; cc < CH; ++cc) {
-          const __nv_bfloat16* src = p.dxbuf + (size_t)rows[0] * p.d + nt * BN + (half * CH + cc) * 32;
+      for (int i = 0; i < HC; ++i) v[i] = 0.f;
+      for (int r = 0; r < maxnr; ++r) {  // expert path first, r order (as the SIMT form)
+        int rr = -1;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) pre[cc][i] = ld_nc_v4(src + 8 * i);
+        for (int q2 = 0; q2 < MOE_MAX_K; ++q2)
+          if (q2 == r && q2 < nr) rr = rows[q2];
+#pragma unroll
+        for (int i = 0; i < 32; i += RPI) {
+          const int rowid = __shfl_sync(0xffffffffu, rr, i + sub);
+          if (rowid >= 0) {
+            const uint4 val = ld_nc_v4(p.dxbuf + (size_t)rowid * p.d + col_base + seg * 8);
+            *reinterpret_cast<uint4*>(stg + (i + sub) * RS + seg * 16) = val;
+          }
         }
+        __syncwarp();
+        if (rr >= 0) {
+#pragma unroll
+          for (int c = 0; c < HC / 8; ++c) {
+            float xv[8];
+            unpack(*reinterpret_cast<const uint4*>(stg + lane * RS + c * 16), xv, __nv_bfloat16());
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[8 * c + j] += xv[j];
+          }
+        }
+        __syncwarp();
       }
       mbar_wait(&b.tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
-      __nv_bfloat16* drow = p.dx + (size_t)t * p.d;
 #pragma unroll
-      for (int cc = 0; cc < CH; ++cc) {
-        const int c = half * CH + cc;
-        const int col0 = nt * BN + c * 32;
-        uint4 old[4];
-        if (valid && p.accumulate) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) old[i] = ld_v4(drow + col0 + 8 * i);
-        }
+      for (int c = 0; c < HC / 32; ++c) {
         uint32_t r32[32];
-        tmem_ld32(taddr + c * 32, r32);
-        if (!valid) continue;
-        float v[32];
+        tmem_ld32(taddr + half * HC + c * 32, r32);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-        if (nr > 0) {  // expert path first, r order (as the SIMT form)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float xv[8];
-            unpack(pre[cc][i], xv, __nv_bfloat16());
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[8 * i + j] += xv[j];
-          }
-        }
-        for (int q2 = 1; q2 < nr; ++q2) {
-          const __nv_bfloat16* src = p.dxbuf + (size_t)rows[q2] * p.d + col0;
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            float xv[8];
-            unpack(ld_nc_v4(src + i), xv, __nv_bfloat16());
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[i + j] += xv[j];
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r32[i]);
-        if (p.accumulate) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float o[8];
-            unpack(old[i], o, __nv_bfloat16());
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[8 * i + j] += o[j];
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) st_v4(drow + col0 + i, pack(v + i, __nv_bfloat16()));
+        for (int i = 0; i < 32; ++i) v[32 * c + i] += __uint_as_float(r32[i]);
       }
       tc_fence_before();
-      mbar_arrive(&b.tempty[acc]);
+      mbar_arrive(&b.tempty[acc]);  // TMEM drained: the next tile's MMAs may start
+      __nv_bfloat16* drow = p.dx + (size_t)t * p.d + col_base;
+      if (valid && p.accumulate) {
+#pragma unroll
+        for (int c = 0; c < HC / 8; ++c) {
+          float o[8];
+          unpack(ld_v4(drow + 8 * c), o, __nv_bfloat16());
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[8 * c + j] += o[j];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < HC / 8; ++c)
+        *reinterpret_cast<uint4*>(stg + lane * RS + c * 16) = pack(v + 8 * c, __nv_bfloat16());
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 32; i += RPI) {
+        const int tok = t0w + i + sub;
+        if (tok < p.T)
+          st_v4(p.dx + (size_t)tok * p.d + col_base + seg * 8,
+                *reinterpret_cast<const uint4*>(stg + (i + sub) * RS + seg * 16));
+      }
+      __syncwarp();
     }
   }
   teardown(tmem_base, 2 * BN, warp);
@@ -687,19 +697,19 @@ cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb
   p.T = T; p.n_pad = n_pad; p.k = k; p.d = d; p.idx = b.idx; p.slot_of = b.slot_of;
   p.dxbuf = (const __nv_bfloat16*)dxbuf; p.dx = (__nv_bfloat16*)dx; p.accumulate = accumulate;
   p.ct = ct;
-  const int bn = d % 256 == 0 ? 256 : (d % 128 == 0 ? 128 : 64);
+  const int bn = d % 128 == 0 ? 128 : 64;
   const int total = ((T + 127) / 128) * (d / bn);
   const int grid = total < g_sms ? total : g_sms;
   (void)n;
 #define GX(BN, ST)                                                                       \
   {                                                                                      \
     auto kf = gate_dx_tc_kernel<BN, ST>;                                                 \
-    size_t sm = smem_for((128 + BN) * 64 * 2, ST);                                       \
+    size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 8 * 32 * (BN + 16);                  \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \
     kf<<<grid, GX_THREADS, sm, s>>>(mhi, mlo, mw, p);                                     \
   }
-  if (bn == 256) GX(256, 4) else if (bn == 128) GX(128, 6) else GX(64, 8)
+  if (bn == 128) GX(128, 4) else GX(64, 6)
 #undef GX
   return cudaGetLastError();
 }
