@@ -136,7 +136,8 @@ def kernel_work(cfg, T, A, s, A_tok=None):
         "combine_bwd": ("byte", (T + 2 * A) * do * s + 12 * T * k + 8 * T * n),
         "wgrad_w2": ("flop", gf), "dgrad_dA": ("flop", gf),
         "wgrad_w1": ("flop", gf), "dgrad_dX": ("flop", gf),
-        "bias_grad": ("byte", A * (f + do) * s),
+        # db1 partial reduction (fixed order over 8 partial rows per 256-row m-tile)
+        "bias_grad": ("byte", ((A // 256) + n) * 8 * f * 4 + n * f * s),
         "gate_dx": ("byte", (A + T) * d * s + 4 * T * n + 8 * T * k),
         "gate_dw": ("byte", T * d * s + 4 * T * n),
     }

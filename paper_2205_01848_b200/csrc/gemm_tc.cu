@@ -409,6 +409,32 @@ static bool use_2cta(int N, int kind) {
 
 void tc_plan_free(TcPlan* p) { (void)p; }
 
+// db[e][c] = sum of the DGRAD_A column-sum partials of expert e, fixed order (deterministic).
+__global__ void bias_part_reduce_kernel(const float* __restrict__ part,
+                                        const int32_t* __restrict__ kept, int N,
+                                        __nv_bfloat16* __restrict__ db, int accumulate) {
+  const int e = blockIdx.y;
+  __shared__ int s_pre, s_mt;
+  if (threadIdx.x < 32) {
+    int acc = 0;
+    for (int j = threadIdx.x; j < e; j += 32) acc += (kept[j] + 255) / 256;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) {
+      s_pre = acc;
+      s_mt = (kept[e] + 255) / 256;
+    }
+  }
+  __syncthreads();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  const float* pp = part + (size_t)s_pre * 8 * N + c;
+  float v = 0.f;
+  for (int j = 0; j < s_mt * 8; ++j) v += pp[(size_t)j * N];
+  if (accumulate) v += __bfloat162float(db[(size_t)e * N + c]);
+  db[(size_t)e * N + c] = __float2bfloat16_rn(v);
+}
+
 #define TC_TRY(expr)                                        \
   do {                                                      \
     if (!(expr)) return MOE_ERR_CUDA;                       \
@@ -428,7 +454,7 @@ template <int KIND>
 static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, int N,
                            int n_local, const void* bias, void* C, int ldc, const int32_t* kept,
                            const int32_t* prefix, const CapTable& ct, cudaStream_t s,
-                           uint32_t* mask = nullptr) {
+                           uint32_t* mask = nullptr, float* bias_part = nullptr) {
   CUtensorMap ma, mb;
   const int bn = pick_bn(N);
   const bool two = use_2cta(N, KIND);
@@ -441,6 +467,7 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   p.kept = kept; p.mtile_prefix = prefix; p.n_local = n_local; p.M = 0; p.N = N; p.K = K;
   p.bias = (const __nv_bfloat16*)bias; p.C = (__nv_bfloat16*)C; p.ldc = ldc; p.ct = ct;
   p.mask = mask;
+  p.bias_part = two ? bias_part : nullptr;
   if (two)
     TC_CUDA(launch_tc2_kind(KIND, bn, ma, mb, p, g_num_sms & ~1, s));
   else
@@ -494,8 +521,10 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
                              int accumulate, int64_t rows, int d, int f, int dout,
                              const int32_t* kept, const int32_t* mtile_prefix, int n_local,
                              const CapTable& ct, int max_cap, cudaStream_t s,
-                             int64_t* nlaunch, Prof* prof, uint32_t* mask) {
+                             int64_t* nlaunch, Prof* prof, uint32_t* mask, float* bias_part) {
   (void)plan; (void)max_cap;
+  // db1 from the DGRAD_A epilogue (2-CTA) instead of the weight-gradient bias warps
+  const bool db1_in_dgrad = db1 && bias_part && use_2cta(f, TC_DGRAD_A);
   if (!ensure_encode()) return MOE_ERR_CUDA;
   int64_t nl = 0;
   if (rows == 0 || n_local == 0) { *nlaunch = 0; return MOE_OK; }
@@ -514,16 +543,23 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   {
     ProfScope ps(prof, "dgrad_dA", s);
     st = mgroup<TC_DGRAD_A>(dO, rows, dout, w2, f, n_local, nullptr, H, f, kept, mtile_prefix, ct, s,
-                            mask);
+                            mask, db1_in_dgrad ? bias_part : nullptr);
   }
   if (st != MOE_OK) return st;
   ++nl;
-  if (dw1) {  // dW1_e = dA_e^T X_e, db1 = sum dA fused in
+  if (db1_in_dgrad) {
+    ProfScope ps(prof, "bias_grad", s);
+    bias_part_reduce_kernel<<<dim3((f + 255) / 256, n_local), 256, 0, s>>>(
+        bias_part, kept, f, (__nv_bfloat16*)db1, accumulate);
+    TC_CUDA(cudaGetLastError());
+    ++nl;
+  }
+  if (dw1) {  // dW1_e = dA_e^T X_e (db1 fused here only when not produced by DGRAD_A)
     ProfScope ps(prof, "wgrad_w1", s);
-    st = wgrad(H, f, X, d, rows, n_local, dw1, db1, accumulate, kept, ct, s);
+    st = wgrad(H, f, X, d, rows, n_local, dw1, db1_in_dgrad ? nullptr : db1, accumulate, kept, ct, s);
     if (st != MOE_OK) return st;
     ++nl;
-  } else if (db1) {
+  } else if (db1 && !db1_in_dgrad) {
     ProfScope ps(prof, "bias_grad", s);
     TC_CUDA(launch_colsum(1, H, f, kept, n_local, ct, db1, accumulate, s));
     ++nl;

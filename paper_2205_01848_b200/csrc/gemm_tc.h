@@ -29,6 +29,6 @@ moe_status_t tc_ffn_backward(TcPlan* p, void* X, void* H, void* dO, void* dX, co
                              int accumulate, int64_t rows, int d, int f, int dout,
                              const int32_t* kept, const int32_t* mtile_prefix, int n_local,
                              const CapTable& ct, int max_cap, cudaStream_t s,
-                             int64_t* nlaunch, Prof* prof, uint32_t* mask);
+                             int64_t* nlaunch, Prof* prof, uint32_t* mask, float* bias_part);
 
 }  // namespace moe

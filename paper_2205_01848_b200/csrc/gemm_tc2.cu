@@ -386,6 +386,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.f;
           }
+          if (p.bias_part) {
+            // db1 = sum over kept tokens of dA (the stored bf16 values): column sums of this
+            // warp's 32 rows by a transpose-reduce over the lanes (31 shuffles; lane j ends
+            // with column j), written as a per-(m-tile, CTA, quarter) partial row that a
+            // fixed-order kernel reduces per expert: deterministic, no atomics.
+            float cs[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) cs[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+              const bool up = (lane & off) != 0;
+#pragma unroll
+              for (int i = 0; i < off; ++i) {
+                const float send = up ? cs[i] : cs[i + off];
+                const float keep = up ? cs[i + off] : cs[i];
+                cs[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+              }
+            }
+            const size_t prow = ((size_t)(s_prefix[e] + mt) * 2 + crank) * 4 + q;
+            p.bias_part[prow * p.N + col0 + lane] = cs[0];
+          }
         } else if (KIND == TC_DGRAD_X) {
           store = row_ok;
         } else {  // WGRAD

@@ -23,7 +23,7 @@ using namespace moe;
 
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
-      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, ep_all, sendbuf, oret, dwg32, total;
+      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, ep_all, sendbuf, oret, dwg32, total;
 };
 
 struct moe_ctx {
@@ -106,6 +106,8 @@ void compute_layout(moe_ctx* h) {
   L.partial = take(splits * n * h->d * 4 + 4096);
   L.dlb = take(h->dtype == MOE_BF16 ? 2 * T * (size_t)h->n_pad * 2 : 0);
   L.mask = take(h->dtype == MOE_BF16 ? (size_t)h->rows * (h->f / 32) * 4 : 0);
+  // db1 partials: sum_e ceil(kept_e/256) <= rows/256 + n_local tiles x 8 rows x f
+  L.bpart = take(h->dtype == MOE_BF16 ? ((size_t)h->rows / 256 + h->n_local) * 8 * h->f * 4 : 0);
   const bool ep = h->use_ep;
   L.ep_all = take(ep ? (size_t)h->R * n * 4 : 0);
   L.sendbuf = take(ep ? T * k * (size_t)std::max(h->d, h->dout) * h->s : 0);
@@ -446,7 +448,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
     moe_status_t st = tc_ffn_backward(&h->tc, X, H, dO, dXb, w1, w2, dw1, db1, dw2, db2, acc,
                                       h->rows, d, f, dout, kept_local, rb.mtile_prefix, nl,
                                       h->ct, h->max_cap_local, s0, &nk, &h->prof,
-                                      (uint32_t*)(ws + h->L.mask));
+                                      (uint32_t*)(ws + h->L.mask), (float*)(ws + h->L.bpart));
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 backward failed");
   } else {
