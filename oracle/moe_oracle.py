@@ -225,9 +225,43 @@ class FwdState:
     extra: dict = field(default_factory=dict)
 
 
+# --------------------------------------------------------------------------- #
+# Eq. 3 balance term and the AggregateSpec output (App. A)
+# --------------------------------------------------------------------------- #
+def balance_term(T_frac, G_frac, lam: float) -> float:
+    """Eq. 3: B = lambda * n * sum_i T_i * G_i (n = len(T_frac))."""
+    T_frac = np.asarray(T_frac, np.float64)
+    return float(lam * len(T_frac) * np.sum(T_frac * np.asarray(G_frac, np.float64)))
+
+
+def balance_fractions(counts_pre, p, k: int):
+    """T_i: fraction of the (token, slot) assignments routed to expert i, PRE-drop counts
+    (S:347-348), normalised over the batch's T*k assignments (S:186 'count_i / (batch*k)');
+    G_i: mean gate probability of expert i over the batch."""
+    p = np.asarray(p, np.float64)
+    return np.asarray(counts_pre, np.float64) / (p.shape[0] * k), p.mean(axis=0)
+
+
+def aggregate_spec(O, idx, slot_of):
+    """AggregateSpec (App. A): row t*k + r holds O_{idx[t,r]}[slot] -- the
+    prediction of the r-th chosen expert for sample t -- or zeros with valid = 0 when the
+    pair was dropped."""
+    T, k = idx.shape
+    d_out = next((o.shape[1] for o in O if o.ndim == 2), 0)
+    out = np.zeros((T * k, d_out))
+    valid = np.zeros(T * k, np.uint8)
+    for t in range(T):
+        for r in range(k):
+            s = slot_of[t, r]
+            if s >= 0:
+                out[t * k + r] = O[idx[t, r]][s]
+                valid[t * k + r] = 1
+    return out, valid
+
+
 def moe_forward(x, params, k: int, capacities, renormalize: int = 1, cached_idx=None,
                 logits=None, emulate_bf16: bool = False, token_offset: int = 0,
-                prior_counts=None) -> FwdState:
+                prior_counts=None, balance_lambda: float = 0.0) -> FwdState:
     """One MoE layer forward.
 
     params: w_gate [n,d], w1 [n,f,d], b1 [n,f], w2 [n,d_out,f], b2 [n,d_out] (fp64 arrays).
@@ -276,21 +310,34 @@ def moe_forward(x, params, k: int, capacities, renormalize: int = 1, cached_idx=
             s = rt.slot_of[t, r]
             if s >= 0:
                 y[t] += w[t, r] * O[idx[t, r]][s]
-    return FwdState(x, params, k, n, list(capacities), renormalize, l, p, idx, fresh, w,
-                    rt, X, A, H, O, y, hit, emulate_bf16, token_offset)
+    st = FwdState(x, params, k, n, list(capacities), renormalize, l, p, idx, fresh, w,
+                  rt, X, A, H, O, y, hit, emulate_bf16, token_offset)
+    st.extra["balance_lambda"] = float(balance_lambda)
+    if balance_lambda:
+        Tf, Gf = balance_fractions(rt.counts, p, k)
+        st.extra["aux_loss"] = balance_term(Tf, Gf, balance_lambda)
+        st.extra["T_frac"] = Tf
+    st.extra["spec"], st.extra["spec_valid"] = aggregate_spec(O, idx, rt.slot_of)
+    return st
 
 
 # --------------------------------------------------------------------------- #
 # Backward: exact chain rule of the forward above
 # --------------------------------------------------------------------------- #
-def moe_backward(st: FwdState, dy: np.ndarray) -> dict:
+def moe_backward(st: FwdState, dy: np.ndarray, dspec=None, dw_ext=None) -> dict:
     """Gradients of sum(dy * y) w.r.t. x, w_gate, w1, b1, w2, b2 (and the logits, dl).
 
     P:225: dropped samples are ignored in back propagation -> dropped pairs get dw = 0 and
     no expert-gradient rows (reading 8).  Renorm mode: dl[t,i_r] = w_r (dw_r - sum w dw),
     zero for unselected experts; the dropped expert's logit still gets gradient through
     the renorm denominator.  Raw mode: dp_j = dw_r at j = i_r; dl = p (dp - <p,dp>).
-    relu'(0) = 0 (reading 9)."""
+    relu'(0) = 0 (reading 9).
+
+    Optional loss variants (N3): dspec [T*k, d_out] is the gradient w.r.t. the AggregateSpec
+    rows (specification loss, Eq. 2; rows of dropped pairs are ignored) and dw_ext
+    [T, k] the caller's direct gradient w.r.t. the gate weights w (e.g. L_i of Eq. 2); the
+    balance term (Eq. 3) adds dB/dl with T_i held constant (stop-gradient):
+    dB/dp[t,i] = lambda n T_i / T."""
     dy = np.asarray(dy, np.float64)
     k, n = st.k, st.n
     T = st.x.shape[0]
@@ -305,6 +352,10 @@ def moe_backward(st: FwdState, dy: np.ndarray) -> dict:
                 e = idx[t, r]
                 dO[e][s] = w[t, r] * dy[t]
                 dw[t, r] = float(dy[t] @ st.O[e][s])
+                if dspec is not None:
+                    dO[e][s] = dO[e][s] + np.asarray(dspec, np.float64)[t * k + r]
+                if dw_ext is not None:
+                    dw[t, r] += float(dw_ext[t, r])
     if st.emulate_bf16:
         dO = [round_bf16(a) for a in dO]
     dW1 = np.zeros_like(np.asarray(st.params["w1"], np.float64))
@@ -336,6 +387,11 @@ def moe_backward(st: FwdState, dy: np.ndarray) -> dict:
             for r in range(k):
                 dp[idx[t, r]] = dw[t, r]
             dl[t] = st.p[t] * (dp - float(np.dot(st.p[t], dp)))
+    lam = st.extra.get("balance_lambda", 0.0)
+    if lam:
+        g = lam * n * st.extra["T_frac"] / T
+        for t in range(T):
+            dl[t] += st.p[t] * (g - float(np.dot(st.p[t], g)))
     wg = np.asarray(st.params["w_gate"], np.float64)
     dW_g = dl.T @ st.x
     dx = dl @ wg

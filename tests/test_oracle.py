@@ -409,3 +409,74 @@ def test_round_bf16_matches_torch():
                         np.array([0.0, -0.0, 1.0, 1.00390625, 1.01171875])])
     ref = torch.tensor(a, dtype=torch.float32).to(torch.bfloat16).to(torch.float64).numpy()
     assert np.array_equal(O.round_bf16(a), ref)
+
+
+# ----------------------------------------------------------------------------- N3: loss variants
+def test_balance_term_spec_examples():
+    # S:329-332 (Eq. 3)
+    lam = 0.37
+    n = 4
+    assert abs(O.balance_term([1 / n] * n, [1 / n] * n, lam) - lam) < 1e-15      # uniform -> lambda
+    assert abs(O.balance_term([1, 0, 0, 0], [1, 0, 0, 0], lam) - 4 * lam) < 1e-15  # collapse -> n lambda
+    assert abs(O.balance_term([0.5, 0.5], [0.6, 0.4], 0.01) - 0.01) < 1e-15
+    # fractions: T sums to 1 over the T*k assignments, G sums to 1
+    rng = np.random.default_rng(11)
+    l = rng.standard_normal((50, 6))
+    idx = O.topk(l, 2)
+    Tf, Gf = O.balance_fractions(O.route(idx, [50] * 6, 6).counts, O.softmax(l), 2)
+    assert abs(Tf.sum() - 1) < 1e-12 and abs(Gf.sum() - 1) < 1e-12
+
+
+def test_aggregate_spec_special_cases():
+    rng = np.random.default_rng(12)
+    n, T, d, f = 3, 12, 4, 5
+    x = rng.standard_normal((T, d))
+    p = _params(rng, n, d, f, d)
+    st = O.moe_forward(x, p, 1, [T] * n, 1)
+    spec, valid = st.extra["spec"], st.extra["spec_valid"]
+    # k = 1, no drops: spec rows are the de-grouped expert predictions; with w = 1 == y
+    assert valid.all() and np.allclose(spec, st.y, atol=1e-12)
+    st2 = O.moe_forward(x, p, 2, [2] * n, 1)                   # drops -> invalid zero rows
+    sp2, v2 = st2.extra["spec"], st2.extra["spec_valid"]
+    assert (v2 == (st2.routing.slot_of.reshape(-1) >= 0)).all()
+    assert np.abs(sp2[v2 == 0]).max() == 0.0
+    # weighted sum of the valid spec rows reproduces y (Eq. 1 inner sum vs Eq. 2 rows)
+    w = st2.w.reshape(-1, 1)
+    assert np.allclose((sp2 * w).reshape(T, 2, d).sum(1), st2.y, atol=1e-12)
+
+
+@pytest.mark.parametrize("renorm", [0, 1])
+def test_loss_variants_finite_differences(renorm):
+    """L = sum(dy*y) + sum(c*spec) + sum(cw*w) + B(lambda): analytic vs central differences."""
+    n, k, lam = 4, 2, 0.3
+    x, p, st, dy = _fd_case(n, k, renorm, 1.0, seed=77)
+    rng = np.random.default_rng(78)
+    T = x.shape[0]
+    cs = rng.standard_normal((T * k, dy.shape[1]))
+    cw = rng.standard_normal((T, k))
+    caps = st.capacities
+
+    def full(xx, pp):
+        s2 = O.moe_forward(xx, pp, k, caps, renorm, balance_lambda=lam)
+        assert (s2.idx == st.idx).all()
+        return s2, float((s2.y * dy).sum() + (s2.extra["spec"] * cs).sum() + (s2.w * cw).sum()
+                         + s2.extra["aux_loss"])
+
+    s0, _ = full(x, p)
+    gr = O.moe_backward(s0, dy, dspec=cs, dw_ext=cw)
+    h = 1e-6
+    for key, gk in (("w_gate", "dw_gate"), ("w1", "dw1"), ("b2", "db2")):
+        base = p[key]
+        for fi in np.random.default_rng(5).choice(base.size, 5, replace=False):
+            ii = np.unravel_index(fi, base.shape)
+            pp = dict(p); pl = base.copy(); pl[ii] += h; pp[key] = pl
+            pm = dict(p); mi = base.copy(); mi[ii] -= h; pm[key] = mi
+            num = (full(x, pp)[1] - full(x, pm)[1]) / (2 * h)
+            ana = gr[gk][ii]
+            assert abs(num - ana) <= 1e-4 * max(1.0, np.abs(gr[gk]).max()), (key, num, ana)
+    for fi in range(0, x.size, 7):
+        ii = np.unravel_index(fi, x.shape)
+        xp = x.copy(); xp[ii] += h
+        xm = x.copy(); xm[ii] -= h
+        num = (full(xp, p)[1] - full(xm, p)[1]) / (2 * h)
+        assert abs(num - gr["dx"][ii]) <= 1e-4 * max(1.0, np.abs(gr["dx"]).max())
