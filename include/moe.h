@@ -195,6 +195,27 @@ MOE_API moe_status_t moe_get_stats_async(moe_handle_t h, const moe_stats_t* dst)
    bit 0 = NaN gate logit, bit 1 = invalid cached index.  flags_out may be NULL. */
 MOE_API moe_status_t moe_check_device_flags(moe_handle_t h, int32_t* flags_out);
 
+/* ----------------------------------------------------------------------------------- *
+ * Loss variants
+ * ----------------------------------------------------------------------------------- */
+/* Eq. 3 balance term: B = lambda * n * sum_i T_i G_i with T_i = cnt_i/(T_g k)
+   (pre-drop counts, held constant in the backward: stop-gradient) and
+   G_i = mean_t p[t,i].  lambda = 0 turns it off.  When on, every forward computes B
+   (read with moe_get_aux_loss_async into host fp32 [1]) and the next backward adds dB/dl
+   = p (g - <p,g>), g_i = lambda n T_i / T_g, to the gate gradient (i.e. the layer's backward
+   returns the gradients of sum(dy * y) + B).  In EP the G sums are all-reduced (fp32). */
+MOE_API moe_status_t moe_set_balance_loss(moe_handle_t h, float lambda);
+MOE_API moe_status_t moe_get_aux_loss_async(moe_handle_t h, float* host_dst);
+/* AggregateSpec (App. A): when set, forwards also write spec [T*k x d_out]
+   (layer dtype; row t*k + r = the prediction of the r-th chosen expert for token t, zeros if
+   the pair was dropped) and valid [T*k] (uint8, 1 = kept).  Device pointers, caller-owned,
+   sized for max_tokens; both NULL = off.  Used with the specification loss (Eq. 2). */
+MOE_API moe_status_t moe_set_spec_outputs(moe_handle_t h, void* spec, uint8_t* valid);
+/* Extra gradients consumed by the next moe_backward: dspec [T*k x d_out] (layer dtype) w.r.t.
+   the spec rows (rows of dropped pairs are ignored) and dw_ext [T x k] fp32 w.r.t. the gate
+   weights w (e.g. L(y_hat, O_i) of Eq. 2).  Device pointers or NULL; they persist until reset. */
+MOE_API moe_status_t moe_set_spec_grads(moe_handle_t h, const void* dspec, const float* dw_ext);
+
 /* Expert-parallel exchange plan (host only, no GPU): from the all-gathered pre-drop counts
    cnt_all [R x n] (row r = rank r's tokens) and the global capacities cap [n], fills
    pre_out [R x n]  global slot of rank r's first pair of expert e (= sum of lower ranks),

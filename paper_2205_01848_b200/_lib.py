@@ -82,6 +82,10 @@ EXPORTS = {
     "moe_profile_enable": ([C.c_void_p, C.c_int32], C.c_int),
     "moe_profile_read": ([C.c_void_p, C.POINTER(KernelTime), C.c_int32, C.POINTER(C.c_int32),
                           C.c_int32], C.c_int),
+    "moe_set_balance_loss": ([C.c_void_p, C.c_float], C.c_int),
+    "moe_get_aux_loss_async": ([C.c_void_p, C.POINTER(C.c_float)], C.c_int),
+    "moe_set_spec_outputs": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "moe_set_spec_grads": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "moe_ep_plan": ([C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                      C.POINTER(C.c_int32), C.POINTER(C.c_int64)], C.c_int),

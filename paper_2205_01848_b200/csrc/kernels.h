@@ -25,6 +25,12 @@ struct RouteBufs {
   uint32_t* ticket;       // [1] last-block ticket of route_scan (self-resetting)
   float* dw;              // [T x k]
   float* dl;              // [T x n]
+  // optional loss variants (N3); null = off
+  void* spec;             // [T*k x d_out] AggregateSpec rows (forward output)
+  uint8_t* spec_valid;    // [T*k]
+  const void* dspec;      // [T*k x d_out] gradient w.r.t. the spec rows (backward input)
+  const float* dw_ext;    // [T x k] extra gradient w.r.t. the gate weights (backward input)
+  const float* bal_g;     // [n] balance-term coefficients lambda*n*T_i/T_g (backward)
 };
 
 // dtype: 0 = fp32, 1 = bf16 for every templated launcher below.
@@ -60,6 +66,13 @@ cudaError_t launch_reduce_partials(int dtype, const float* partial, int splits, 
                                    void* out, int accumulate, cudaStream_t s);
 cudaError_t launch_colsum(int dtype, const void* buf, int cols, const int32_t* kept, int n,
                           const CapTable& ct, void* out, int accumulate, cudaStream_t s);
+
+// Eq. 3 balance term (aux_kernels.cu)
+cudaError_t launch_balance_partial(const float* logits, int T, int n, float* partial,
+                                   float* gsum, cudaStream_t s);
+cudaError_t launch_balance_final(const float* gsum, const int32_t* counts, int n, int k,
+                                 int64_t Tg, float lam, float* g_out, float* aux_out,
+                                 cudaStream_t s);
 
 // Grouped GEMMs of the expert FFN (SIMT fp32/bf16 path, gemm_simt.cu).
 enum EpiKind { EPI_BIAS_RELU = 0, EPI_BIAS = 1, EPI_RELU_MASK = 2, EPI_NONE = 3 };

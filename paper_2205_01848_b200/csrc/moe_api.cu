@@ -23,7 +23,7 @@ using namespace moe;
 
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
-      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, ep_all, sendbuf, oret, dwg32, total;
+      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, ep_all, sendbuf, oret, dwg32, total;
 };
 
 struct moe_ctx {
@@ -50,6 +50,11 @@ struct moe_ctx {
   int use_tc = 0;             // tcgen05 path for bf16 (env MOE_FORCE_SIMT=1 disables)
   TcPlan tc{};
   Prof prof;
+  float balance_lambda = 0.f; // Eq. 3 balance term weight (0 = off)
+  void* spec = nullptr;       // AggregateSpec outputs of the next forward (N3)
+  uint8_t* spec_valid = nullptr;
+  const void* dspec = nullptr;   // extra gradients for the next backward (N3)
+  const float* dw_ext = nullptr;
   int use_ep = 0;             // expert-parallel path (nccl_comm given; R may be 1 = loopback)
   EpState* ep = nullptr;
   EpPlan plan;
@@ -107,6 +112,8 @@ void compute_layout(moe_ctx* h) {
   L.dlb = take(h->dtype == MOE_BF16 ? 2 * T * (size_t)h->n_pad * 2 : 0);
   L.mask = take(h->dtype == MOE_BF16 ? (size_t)h->rows * (h->f / 32) * 4 : 0);
   // db1 partials: sum_e ceil(kept_e/256) <= rows/256 + n_local tiles x 8 rows x f
+  // balance term: partial column sums [ceil(T/64) x n], gsum [n], g [n], aux [1]
+  L.bal = take(((T + 63) / 64 + 3) * n * 4 + 256);
   L.bpart = take(h->dtype == MOE_BF16 ? ((size_t)h->rows / 256 + h->n_local) * 8 * h->f * 4 : 0);
   const bool ep = h->use_ep;
   L.ep_all = take(ep ? (size_t)h->R * n * 4 : 0);
@@ -399,7 +406,23 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     CUDA_TRY(h, cudaEventRecord(h->ev_join, sd));
     CUDA_TRY(h, cudaStreamWaitEvent(s0, h->ev_join, 0));
   }
+  if (h->balance_lambda != 0.f) {  // Eq. 3 balance term (N3)
+    float* bal = (float*)(ws + h->L.bal);
+    float* gsum = bal + (size_t)((h->maxT + 63) / 64) * n;
+    KL(h, T > 0 ? 2 : 1, "balance", s0, launch_balance_partial(rb.logits, T, n, bal, gsum, s0));
+    if (h->use_ep) {
+      std::string err;
+      moe_status_t st = ep_allreduce_f32(h->ep, gsum, (size_t)n, s0, &err);
+      if (st != MOE_OK) return fail(h, st, err);
+    }
+    KL(h, 1, "balance", s0, launch_balance_final(gsum, rb.counts, n, k, (int64_t)T * h->R,
+                                                 h->balance_lambda, gsum + n, gsum + 2 * n, s0));
+  }
+  rb.spec = h->spec;
+  rb.spec_valid = h->spec_valid;
   KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O_tok, rb, T, k, dout, h->cts, a->y, s0));
+  rb.spec = nullptr;
+  rb.spec_valid = nullptr;
   h->fa = *a;
   h->T_last = T;
   h->have_fwd = 1;
@@ -430,8 +453,16 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   void* O_tok = h->use_ep ? (void*)(ws + h->L.oret) : O;
   void* dO_tok = h->use_ep ? (void*)(ws + h->L.sendbuf) : dO;
   std::string err;
+  rb.dspec = h->dspec;
+  rb.dw_ext = h->dw_ext;
+  rb.bal_g = h->balance_lambda != 0.f
+                 ? (const float*)(ws + h->L.bal) + (size_t)((h->maxT + 63) / 64) * n + n
+                 : nullptr;
   KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O_tok, rb, T, k, n, dout, h->renorm, h->cts,
                                                      dO_tok, dlb, h->maxT, h->n_pad, s0));
+  rb.dspec = nullptr;
+  rb.dw_ext = nullptr;
+  rb.bal_g = nullptr;
   if (h->use_ep) {  // C4: dO rows to the expert owners
     moe_status_t st = ep_to_experts(h->ep, h->plan, dO_tok, dO, h->ct, dout, (int)h->s, s0, &err);
     if (st != MOE_OK) return fail(h, st, err);
@@ -600,6 +631,38 @@ moe_status_t moe_ep_plan(int32_t R, int32_t rank, int32_t n, const int32_t* cnt_
   if (send_off_out) std::memcpy(send_off_out, P.send_off.data(), 4 * (size_t)n);
   if (kept_local_out) std::memcpy(kept_local_out, P.kept_local.data(), 4 * (size_t)P.n_local);
   if (drops_out) *drops_out = P.drops;
+  return MOE_OK;
+}
+
+moe_status_t moe_set_balance_loss(moe_handle_t h, float lambda) {
+  if (!h || !(lambda >= 0.f)) return MOE_ERR_INVALID_ARG;
+  h->balance_lambda = lambda;
+  return MOE_OK;
+}
+
+moe_status_t moe_get_aux_loss_async(moe_handle_t h, float* host_dst) {
+  if (!h || !host_dst) return MOE_ERR_INVALID_ARG;
+  if (!h->ws) return fail(h, MOE_ERR_STATE, "workspace not set");
+  if (h->balance_lambda == 0.f) {
+    *host_dst = 0.f;
+    return MOE_OK;
+  }
+  const float* aux = (const float*)(h->ws + h->L.bal) + (size_t)((h->maxT + 63) / 64) * h->n + 2 * h->n;
+  CUDA_TRY(h, cudaMemcpyAsync(host_dst, aux, 4, cudaMemcpyDeviceToHost, h->stream));
+  return MOE_OK;
+}
+
+moe_status_t moe_set_spec_outputs(moe_handle_t h, void* spec, uint8_t* valid) {
+  if (!h || (!spec != !valid)) return MOE_ERR_INVALID_ARG;
+  h->spec = spec;
+  h->spec_valid = valid;
+  return MOE_OK;
+}
+
+moe_status_t moe_set_spec_grads(moe_handle_t h, const void* dspec, const float* dw_ext) {
+  if (!h) return MOE_ERR_INVALID_ARG;
+  h->dspec = dspec;
+  h->dw_ext = dw_ext;
   return MOE_OK;
 }
 

@@ -392,7 +392,7 @@ template <typename T, int VPL, int KM>
 __global__ void __launch_bounds__(256) combine_fwd_kernel(
     const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
-    T* __restrict__ y) {
+    T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
@@ -422,6 +422,19 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
       const int v = vb + j * 32 + lane;
       if (rows[r] >= 0 && v < nvec) u[r][j] = ld_nc_v4(obuf + (size_t)rows[r] * dout + (size_t)v * VE);
     }
+  if (spec) {  // AggregateSpec (App. A): the chosen experts' rows, zeros if dropped
+#pragma unroll
+    for (int r = 0; r < KM; ++r) {
+      if (r >= k) break;
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int v = vb + j * 32 + lane;
+        if (v < nvec)
+          st_v4(spec + ((size_t)t * k + r) * dout + (size_t)v * VE,
+                rows[r] >= 0 ? u[r][j] : make_uint4(0, 0, 0, 0));
+      }
+    }
+  }
 #pragma unroll
   for (int j = 0; j < VPL; ++j) {
     const int v = vb + j * 32 + lane;
@@ -440,6 +453,11 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
     st_v4(yrow + (size_t)v * VE, pack(acc, T()));
   }
   }
+  if (valid && lane < k) {
+#pragma unroll
+    for (int r = 0; r < KM; ++r)
+      if (r == lane) valid[(size_t)t * k + r] = rows[r] >= 0 ? 1 : 0;
+  }
 }
 
 // generic fallback (any d_out, any k): row loop
@@ -447,17 +465,20 @@ template <typename T>
 __global__ void __launch_bounds__(256) combine_fwd_generic_kernel(
     const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
-    T* __restrict__ y) {
+    T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
   int rows[MOE_MAX_K];
   float wr[MOE_MAX_K];
   int nk = 0;
+  int rsel[MOE_MAX_K];
   for (int r = 0; r < k; ++r) {
     int sl = slot_of[(size_t)t * k + r];
+    rsel[r] = -1;
     if (sl >= 0) {
       rows[nk] = ct.base[idx[(size_t)t * k + r]] + sl;
+      rsel[r] = rows[nk];
       wr[nk] = w[(size_t)t * k + r];
       ++nk;
     }
@@ -477,24 +498,32 @@ __global__ void __launch_bounds__(256) combine_fwd_generic_kernel(
       for (int i = 0; i < VE; ++i) acc[i] = fmaf(wr[q], o[i], acc[i]);
     }
     st_v4(yrow + (size_t)v * VE, pack(acc, T()));
+    if (spec)
+      for (int r = 0; r < k; ++r)
+        st_v4(spec + ((size_t)t * k + r) * dout + (size_t)v * VE,
+              rsel[r] >= 0 ? ld_nc_v4(obuf + (size_t)rsel[r] * dout + (size_t)v * VE)
+                           : make_uint4(0, 0, 0, 0));
   }
+  if (valid && lane < k) valid[(size_t)t * k + lane] = slot_of[(size_t)t * k + lane] >= 0 ? 1 : 0;
 }
 
 template <typename T>
 static cudaError_t combine_fwd_t(const void* obuf, RouteBufs b, int T_, int k, int d_out,
                                  const CapTable& ct, void* y, cudaStream_t s) {
+  T* spec = (T*)b.spec;
+  uint8_t* valid = b.spec_valid;
   dim3 grid((T_ + 7) / 8);
   const int vpl = (d_out / Vec<T>::N + 31) / 32;
 #define CF(V, K)                                                                            \
   combine_fwd_kernel<T, V, K><<<grid, 256, 0, s>>>((const T*)obuf, b.w, b.idx, b.slot_of, ct, \
-                                                   T_, k, d_out, (T*)y)
+                                                   T_, k, d_out, (T*)y, spec, valid)
   if (k <= 2) {
     if (vpl <= 2) { if (k == 1) CF(2, 1); else CF(2, 2); }
     else if (vpl <= 4) { if (k == 1) CF(4, 1); else CF(4, 2); }
     else { if (k == 1) CF(8, 1); else CF(8, 2); }
   } else {
     combine_fwd_generic_kernel<T><<<grid, 256, 0, s>>>((const T*)obuf, b.w, b.idx, b.slot_of, ct,
-                                                       T_, k, d_out, (T*)y);
+                                                       T_, k, d_out, (T*)y, spec, valid);
   }
 #undef CF
   return cudaGetLastError();
@@ -519,12 +548,14 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
     const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of,
     const float* __restrict__ logits, CapTable ct, int Tn, int k, int n, int dout, int renorm,
     T* __restrict__ dobuf, float* __restrict__ dw, float* __restrict__ dl,
-    __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad) {
+    __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad, const T* __restrict__ dspec,
+    const float* __restrict__ dw_ext, const float* __restrict__ bal_g) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
   constexpr int VE = Vec<T>::N;
   constexpr int NL = MOE_MAX_E / 64;  // expert pairs per lane (n <= 256)
+  const bool need_p = !renorm || bal_g != nullptr;  // full softmax row needed
   const int nvec = dout / VE;
   int rows[KM], er[KM];
   float wr[KM], part[KM];
@@ -544,8 +575,8 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
 #pragma unroll
   for (int j = 0; j < NL; ++j) {
     const int e = 2 * lane + 64 * j;
-    lg[j][0] = (!renorm && e < n) ? l[e] : -INFINITY;
-    lg[j][1] = (!renorm && e + 1 < n) ? l[e + 1] : -INFINITY;
+    lg[j][0] = (need_p && e < n) ? l[e] : -INFINITY;
+    lg[j][1] = (need_p && e + 1 < n) ? l[e + 1] : -INFINITY;
   }
   const T* dyrow = dy + (size_t)t * dout;
   for (int vb = 0; vb < nvec; vb += VPL * 32) {  // one pass for d_out*s <= 512*VPL bytes
@@ -572,12 +603,18 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
 #pragma unroll
     for (int r = 0; r < KM; ++r) {
       if (rows[r] < 0) continue;
-      float o[VE], dov[VE];
+      float o[VE], dov[VE], ds[VE];
       unpack(u[r][jv], o, T());
+      if (dspec) {  // specification-loss gradient of this (token, expert) row
+        unpack(ld_nc_v4(dspec + ((size_t)t * k + r) * dout + (size_t)v * VE), ds, T());
+      } else {
+#pragma unroll
+        for (int i = 0; i < VE; ++i) ds[i] = 0.f;
+      }
 #pragma unroll
       for (int i = 0; i < VE; ++i) {
         part[r] = fmaf(gv[i], o[i], part[r]);
-        dov[i] = wr[r] * gv[i];
+        dov[i] = fmaf(wr[r], gv[i], ds[i]);
       }
       st_v4(dobuf + (size_t)rows[r] * dout + (size_t)v * VE, pack(dov, T()));
     }
@@ -589,14 +626,14 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   for (int r = 0; r < KM; ++r) {
     float sr = warp_sum(part[r]);
     sr = __shfl_sync(0xffffffffu, sr, 0);
-    dwr[r] = rows[r] >= 0 ? sr : 0.f;
+    dwr[r] = rows[r] >= 0 ? sr + (dw_ext ? dw_ext[(size_t)t * k + r] : 0.f) : 0.f;
     c = fmaf(wr[r], dwr[r], c);
   }
 #pragma unroll
   for (int r = 0; r < KM; ++r)
     if (r < k && lane == r) dw[(size_t)t * k + r] = dwr[r];
-  float m = -INFINITY, sp = 0.f;
-  if (!renorm) {
+  float m = -INFINITY, sp = 0.f, cb = 0.f;
+  if (need_p) {
 #pragma unroll
     for (int j = 0; j < NL; ++j) m = fmaxf(m, fmaxf(lg[j][0], lg[j][1]));
 #pragma unroll
@@ -608,6 +645,15 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
       if (e + 1 < n) sp += expf(lg[j][1] - m);
     }
     sp = __shfl_sync(0xffffffffu, warp_sum(sp), 0);
+    if (bal_g) {  // Eq. 3 balance term: dB/dl = p (g - <p, g>), g_i = lambda n T_i / T_g
+#pragma unroll
+      for (int j = 0; j < NL; ++j) {
+        const int e = 2 * lane + 64 * j;
+        if (e < n) cb = fmaf(expf(lg[j][0] - m) / sp, bal_g[e], cb);
+        if (e + 1 < n) cb = fmaf(expf(lg[j][1] - m) / sp, bal_g[e + 1], cb);
+      }
+      cb = __shfl_sync(0xffffffffu, warp_sum(cb), 0);
+    }
   }
   float* dlrow = dl + (size_t)t * n;
   const int ncols = dlb ? n_pad : n;
@@ -633,6 +679,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
             if (er[r] == e) dp = dwr[r];
           v = p * (dp - c);
         }
+        if (bal_g) v = fmaf(expf(lg[j][h] - m) / sp, bal_g[e] - cb, v);
         dlrow[e] = v;
       }
       v2[h] = v;
@@ -657,7 +704,8 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
   combine_bwd_kernel<T, V, K><<<grid, 256, 0, s>>>((const T*)dy, (const T*)obuf, b.w, b.idx,   \
                                                    b.slot_of, b.logits, ct, T_, k, n, d_out,   \
                                                    renorm, (T*)dobuf, b.dw, b.dl,              \
-                                                   (__nv_bfloat16*)dlb, maxT, n_pad)
+                                                   (__nv_bfloat16*)dlb, maxT, n_pad,           \
+                                                   (const T*)b.dspec, b.dw_ext, b.bal_g)
   const int km = k == 1 ? 1 : (k == 2 ? 2 : 8);
   if (vpl <= 2) { if (km == 1) CB(2, 1); else if (km == 2) CB(2, 2); else CB(2, 8); }
   else if (vpl <= 4) { if (km == 1) CB(4, 1); else if (km == 2) CB(4, 2); else CB(4, 8); }

@@ -119,6 +119,39 @@ class MoELayer:
         self._cached_ref = idx
         L.check(self.lib.moe_set_cached_assignment(self.h, _ptr(idx)), self.h)
 
+    # -- loss variants (N3) -----------------------------------------------------------
+    def set_balance_loss(self, lam: float):
+        """Eq. 3 balance term weight (0 = off); the backward then includes dB/dl."""
+        L.check(self.lib.moe_set_balance_loss(self.h, float(lam)), self.h)
+        self._lam = float(lam)
+
+    def aux_loss(self) -> float:
+        """B of the last forward (synchronises)."""
+        v = C.c_float()
+        self._sync_stream()
+        L.check(self.lib.moe_get_aux_loss_async(self.h, C.byref(v)), self.h)
+        torch.cuda.current_stream(self.device).synchronize()
+        return float(v.value)
+
+    def enable_spec(self, on: bool = True):
+        """AggregateSpec outputs for the following forwards (self.spec, self.spec_valid)."""
+        if on:
+            self.spec = torch.empty(self.max_tokens * self.k, self.d_out, dtype=self.tdtype,
+                                    device=self.device)
+            self.spec_valid = torch.empty(self.max_tokens * self.k, dtype=torch.uint8,
+                                          device=self.device)
+            L.check(self.lib.moe_set_spec_outputs(self.h, _ptr(self.spec), _ptr(self.spec_valid)),
+                    self.h)
+        else:
+            self.spec = self.spec_valid = None
+            L.check(self.lib.moe_set_spec_outputs(self.h, None, None), self.h)
+
+    def set_spec_grads(self, dspec=None, dw_ext=None):
+        """Gradients w.r.t. the spec rows ([T*k, d_out], layer dtype) and the gate weights
+        ([T, k] fp32) consumed by the following backwards (None = none)."""
+        self._spec_grads = (dspec, dw_ext)
+        L.check(self.lib.moe_set_spec_grads(self.h, _ptr(dspec), _ptr(dw_ext)), self.h)
+
     # -- hot path -------------------------------------------------------------------
     def _check(self, t, shape, name):
         if t.dtype != self.tdtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous() \
