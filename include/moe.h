@@ -216,6 +216,35 @@ MOE_API moe_status_t moe_set_spec_outputs(moe_handle_t h, void* spec, uint8_t* v
    weights w (e.g. L(y_hat, O_i) of Eq. 2).  Device pointers or NULL; they persist until reset. */
 MOE_API moe_status_t moe_set_spec_grads(moe_handle_t h, const void* dspec, const float* dw_ext);
 
+/* ----------------------------------------------------------------------------------- *
+ * Recompile runtime pieces
+ * ----------------------------------------------------------------------------------- */
+/* Model-metric future queue: App. B pushes one future per launched iteration into a queue
+   per metric; its length is the number of launched-but-unexecuted iterations and recompile
+   triggers run when it equals Delta_launch.  With depth > 0 every moe_forward appends one
+   entry (async D2H into pinned memory + an event, no sync); moe_metrics_pop returns the
+   oldest entry once the GPU produced it (block = 1 waits for it) and removes it.  A forward
+   issued while `depth` entries are pending fails with MOE_ERR_STATE (the caller must pop:
+   this bounds the launch frontier).  depth = 0 disables and clears the queue. */
+typedef struct {
+  int64_t iteration;      /* forward index since moe_metrics_enable */
+  int32_t T;              /* tokens of that forward */
+  int32_t hit_count;      /* cached mode: rows whose fresh top-k set equals the cached set */
+  int64_t drops;          /* pairs dropped by the capacities */
+  float aux_loss;         /* Eq. 3 balance term (0 when off) */
+  int32_t counts[256];    /* pre-drop per-expert counts (global in EP), n entries used */
+} moe_metrics_t;
+MOE_API moe_status_t moe_metrics_enable(moe_handle_t h, int32_t depth);
+MOE_API moe_status_t moe_metrics_pending(moe_handle_t h, int32_t* n);
+MOE_API moe_status_t moe_metrics_pop(moe_handle_t h, int32_t block, moe_metrics_t* out,
+                                     int32_t* got);
+/* Caching trigger: switch sample-assignment caching on when hit_fraction >=
+   enable_at (paper: 0.96), off when it drops below disable_below (0.90), never before epoch
+   warmup_epochs (10).  Host only. */
+MOE_API moe_status_t moe_caching_trigger(double hit_fraction, int32_t epoch, int32_t enabled,
+                                         double enable_at, double disable_below,
+                                         int32_t warmup_epochs, int32_t* new_enabled);
+
 /* Expert-parallel exchange plan (host only, no GPU): from the all-gathered pre-drop counts
    cnt_all [R x n] (row r = rank r's tokens) and the global capacities cap [n], fills
    pre_out [R x n]  global slot of rank r's first pair of expert e (= sum of lower ranks),

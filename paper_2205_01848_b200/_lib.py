@@ -55,6 +55,11 @@ class KernelTime(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("total_ms", C.c_double)]
 
 
+class Metrics(C.Structure):
+    _fields_ = [("iteration", C.c_int64), ("T", C.c_int32), ("hit_count", C.c_int32),
+                ("drops", C.c_int64), ("aux_loss", C.c_float), ("counts", C.c_int32 * 256)]
+
+
 class PolicyConfig(C.Structure):
     _fields_ = [("n_experts", C.c_int32), ("top_k", C.c_int32), ("tokens_global", C.c_int64),
                 ("window", C.c_int32), ("headroom", C.c_double), ("shrink_util", C.c_double),
@@ -86,6 +91,11 @@ EXPORTS = {
     "moe_get_aux_loss_async": ([C.c_void_p, C.POINTER(C.c_float)], C.c_int),
     "moe_set_spec_outputs": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "moe_set_spec_grads": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "moe_metrics_enable": ([C.c_void_p, C.c_int32], C.c_int),
+    "moe_metrics_pending": ([C.c_void_p, C.POINTER(C.c_int32)], C.c_int),
+    "moe_metrics_pop": ([C.c_void_p, C.c_int32, C.POINTER(Metrics), C.POINTER(C.c_int32)], C.c_int),
+    "moe_caching_trigger": ([C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_int32,
+                             C.POINTER(C.c_int32)], C.c_int),
     "moe_ep_plan": ([C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                      C.POINTER(C.c_int32), C.POINTER(C.c_int64)], C.c_int),

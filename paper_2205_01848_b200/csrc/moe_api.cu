@@ -55,6 +55,14 @@ struct moe_ctx {
   uint8_t* spec_valid = nullptr;
   const void* dspec = nullptr;   // extra gradients for the next backward (N3)
   const float* dw_ext = nullptr;
+  // model-metric future queue (App. B)
+  struct MetricSlot {
+    moe_metrics_t* host = nullptr;  // pinned
+    cudaEvent_t ev = nullptr;
+  };
+  std::vector<MetricSlot> mq;
+  int mq_head = 0, mq_count = 0;
+  int64_t mq_iter = 0;
   int use_ep = 0;             // expert-parallel path (nccl_comm given; R may be 1 = loopback)
   EpState* ep = nullptr;
   EpPlan plan;
@@ -247,6 +255,10 @@ moe_status_t moe_destroy(moe_handle_t h) {
   if (h->side) cudaStreamDestroy(h->side);
   tc_plan_free(&h->tc);
   h->prof.destroy();
+  for (auto& sl : h->mq) {
+    if (sl.host) cudaFreeHost(sl.host);
+    if (sl.ev) cudaEventDestroy(sl.ev);
+  }
   delete h;
   return MOE_OK;
 }
@@ -312,6 +324,8 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   if (a->T < 0 || a->T > h->maxT) return fail(h, MOE_ERR_INVALID_ARG, "T out of range");
   if (a->T > 0 && (!a->x || !a->w_gate || !a->w1 || !a->b1 || !a->w2 || !a->b2 || !a->y))
     return fail(h, MOE_ERR_INVALID_ARG, "null tensor");
+  if (!h->mq.empty() && h->mq_count == (int)h->mq.size())
+    return fail(h, MOE_ERR_STATE, "metrics queue full: pop before launching more iterations");
   const int T = a->T, n = h->n, k = h->k, d = h->d, f = h->f, dout = h->dout, dt = h->dtype;
   cudaStream_t s0 = h->stream;
   RouteBufs& rb = h->rb;
@@ -423,6 +437,23 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O_tok, rb, T, k, dout, h->cts, a->y, s0));
   rb.spec = nullptr;
   rb.spec_valid = nullptr;
+  if (!h->mq.empty()) {  // push this iteration's metric futures (App. B)
+    auto& sl = h->mq[(h->mq_head + h->mq_count) % h->mq.size()];
+    sl.host->iteration = h->mq_iter;
+    sl.host->T = T;
+    CUDA_TRY(h, cudaMemcpyAsync(sl.host->counts, rb.counts, 4 * n, cudaMemcpyDeviceToHost, s0));
+    CUDA_TRY(h, cudaMemcpyAsync(&sl.host->drops, rb.drops, 8, cudaMemcpyDeviceToHost, s0));
+    CUDA_TRY(h, cudaMemcpyAsync(&sl.host->hit_count, rb.hit_count, 4, cudaMemcpyDeviceToHost, s0));
+    if (h->balance_lambda != 0.f) {
+      const float* aux = (const float*)(ws + h->L.bal) + (size_t)((h->maxT + 63) / 64) * n + 2 * n;
+      CUDA_TRY(h, cudaMemcpyAsync(&sl.host->aux_loss, aux, 4, cudaMemcpyDeviceToHost, s0));
+    } else {
+      sl.host->aux_loss = 0.f;
+    }
+    CUDA_TRY(h, cudaEventRecord(sl.ev, s0));
+    ++h->mq_count;
+  }
+  ++h->mq_iter;
   h->fa = *a;
   h->T_last = T;
   h->have_fwd = 1;
@@ -631,6 +662,62 @@ moe_status_t moe_ep_plan(int32_t R, int32_t rank, int32_t n, const int32_t* cnt_
   if (send_off_out) std::memcpy(send_off_out, P.send_off.data(), 4 * (size_t)n);
   if (kept_local_out) std::memcpy(kept_local_out, P.kept_local.data(), 4 * (size_t)P.n_local);
   if (drops_out) *drops_out = P.drops;
+  return MOE_OK;
+}
+
+moe_status_t moe_metrics_enable(moe_handle_t h, int32_t depth) {
+  if (!h || depth < 0) return MOE_ERR_INVALID_ARG;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  for (auto& sl : h->mq) {
+    if (sl.host) cudaFreeHost(sl.host);
+    if (sl.ev) cudaEventDestroy(sl.ev);
+  }
+  h->mq.assign(depth, {});
+  for (auto& sl : h->mq) {
+    CUDA_TRY(h, cudaMallocHost(&sl.host, sizeof(moe_metrics_t)));
+    std::memset(sl.host, 0, sizeof(moe_metrics_t));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
+  }
+  h->mq_head = h->mq_count = 0;
+  h->mq_iter = 0;
+  return MOE_OK;
+}
+
+moe_status_t moe_metrics_pending(moe_handle_t h, int32_t* n) {
+  if (!h || !n) return MOE_ERR_INVALID_ARG;
+  *n = h->mq_count;
+  return MOE_OK;
+}
+
+moe_status_t moe_metrics_pop(moe_handle_t h, int32_t block, moe_metrics_t* out, int32_t* got) {
+  if (!h || !out || !got) return MOE_ERR_INVALID_ARG;
+  *got = 0;
+  if (h->mq_count == 0) return MOE_OK;
+  auto& sl = h->mq[h->mq_head];
+  if (block) {
+    CUDA_TRY(h, cudaEventSynchronize(sl.ev));
+  } else {
+    cudaError_t q = cudaEventQuery(sl.ev);
+    if (q == cudaErrorNotReady) return MOE_OK;
+    CUDA_TRY(h, q);
+  }
+  std::memcpy(out, sl.host, sizeof(moe_metrics_t));
+  h->mq_head = (h->mq_head + 1) % (int)h->mq.size();
+  --h->mq_count;
+  *got = 1;
+  return MOE_OK;
+}
+
+moe_status_t moe_caching_trigger(double hit_fraction, int32_t epoch, int32_t enabled,
+                                 double enable_at, double disable_below, int32_t warmup_epochs,
+                                 int32_t* new_enabled) {
+  if (!new_enabled || disable_below > enable_at) return MOE_ERR_INVALID_ARG;
+  int32_t e = enabled ? 1 : 0;
+  if (epoch >= warmup_epochs) {
+    if (!e && hit_fraction >= enable_at) e = 1;
+    else if (e && hit_fraction < disable_below) e = 0;
+  }
+  *new_enabled = e;
   return MOE_OK;
 }
 

@@ -58,6 +58,7 @@ class MoELayer:
         with torch.cuda.device(self.device):
             L.check(self.lib.moe_init(C.byref(cfg), C.byref(h)), None, "moe_init")
         self.h = h
+        self.layout_generation = 0   # bumped by every recompile (capacity change)
         self.ws = None
         self._cached_ref = None
         self._alloc_workspace()
@@ -100,6 +101,7 @@ class MoELayer:
     def set_capacities(self, caps):
         """Dynamic capacity factors (S4.1): new per-expert capacities, stream-ordered."""
         arr = (C.c_int32 * self.n)(*[int(c) for c in caps])
+        self.layout_generation += 1
         st = self.lib.moe_set_capacities(self.h, arr)
         if st == L.MOE_ERR_WORKSPACE_TOO_SMALL:
             self._alloc_workspace()
@@ -254,6 +256,10 @@ class MoELayer:
         cnt = C.c_int32()
         L.check(self.lib.moe_profile_read(self.h, buf, 64, C.byref(cnt), int(reset)), self.h)
         return {buf[i].name.decode(): (buf[i].launches, buf[i].total_ms) for i in range(cnt.value)}
+
+    def metrics_queue(self, depth: int):
+        from .runtime import MetricQueue
+        return MetricQueue(self, depth)
 
     def launch_count(self):
         v = C.c_int64()

@@ -1,0 +1,143 @@
+"""Recompile runtime around one MoE layer (PAPER App. B).
+
+* The model-metric future queue lives in the C library (moe_metrics_*): every forward pushes
+  its routing statistics asynchronously; the queue length is the number of launched but not
+  yet consumed iterations.
+* RecompileRuntime keeps that length at Delta_launch: after each launch it pops the oldest
+  metric (waiting for the GPU only when the queue is longer than Delta_launch), runs the
+  user's triggers on the CPU while the GPU keeps executing the already-launched iterations,
+  and applies their decisions at the launch frontier (the next launched iteration) -- the
+  paper's "graph adjustments take effect at the launch frontier".
+* GraphedStep captures one forward+backward of the layer into a CUDA graph; a capacity change
+  (a recompile) re-instantiates it, exactly the paper's recompile of a static graph.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib as L
+
+
+def caching_trigger(hit_fraction, epoch, enabled, enable_at=0.96, disable_below=0.90,
+                    warmup_epochs=10) -> bool:
+    """P:353 switching rule (library host helper)."""
+    out = C.c_int32()
+    L.check(L.load().moe_caching_trigger(float(hit_fraction), int(epoch), int(bool(enabled)),
+                                         float(enable_at), float(disable_below),
+                                         int(warmup_epochs), C.byref(out)))
+    return bool(out.value)
+
+
+class MetricQueue:
+    """Python view of the library's per-iteration metric queue of one layer."""
+
+    def __init__(self, layer, depth: int):
+        self.layer = layer
+        self.lib = layer.lib
+        L.check(self.lib.moe_metrics_enable(layer.h, int(depth)), layer.h)
+        self.depth = depth
+
+    def pending(self) -> int:
+        n = C.c_int32()
+        L.check(self.lib.moe_metrics_pending(self.layer.h, C.byref(n)), self.layer.h)
+        return n.value
+
+    def pop(self, block: bool = True):
+        m = L.Metrics()
+        got = C.c_int32()
+        L.check(self.lib.moe_metrics_pop(self.layer.h, int(block), C.byref(m), C.byref(got)),
+                self.layer.h)
+        if not got.value:
+            return None
+        return dict(iteration=m.iteration, T=m.T, hit_count=m.hit_count, drops=m.drops,
+                    aux_loss=m.aux_loss, counts=list(m.counts[: self.layer.n]))
+
+
+class RecompileRuntime:
+    """Delta_launch-delayed triggers over one layer's metric queue (App. B).
+
+    triggers: callables f(metrics, runtime) returning None or a dict with optional keys
+    'capacities' (list) and 'cached' (tensor or None); decisions apply to the next launch."""
+
+    def __init__(self, layer, delta_launch: int = 1, triggers=()):
+        self.layer = layer
+        self.delta = int(delta_launch)
+        self.queue = MetricQueue(layer, self.delta + 1)
+        self.triggers = list(triggers)
+        self.log = []            # (metric iteration, launch iteration it takes effect at, decision)
+        self.launched = 0
+
+    def before_launch(self):
+        """Make room in the queue (the launch frontier may run Delta_launch ahead)."""
+        while self.queue.pending() > self.delta:
+            self._consume(self.queue.pop(block=True))
+
+    def after_launch(self):
+        self.launched += 1
+        while self.queue.pending() > self.delta:
+            self._consume(self.queue.pop(block=True))
+
+    def _consume(self, m):
+        for trig in self.triggers:
+            dec = trig(m, self)
+            if not dec:
+                continue
+            if "capacities" in dec:
+                self.layer.set_capacities(dec["capacities"])
+            if "cached" in dec:
+                self.layer.set_cached_assignment(dec["cached"])
+            self.log.append((m["iteration"], self.launched, dec))
+
+    def drain(self):
+        while self.queue.pending():
+            self._consume(self.queue.pop(block=True))
+
+
+def capacity_trigger(policy):
+    """Adapter: the library's dynamic-capacity policy (moe_policy_*) as a runtime trigger."""
+    def trig(m, rt):
+        new = policy.update(m["counts"])
+        return {"capacities": new} if new is not None else None
+    return trig
+
+
+class GraphedStep:
+    """forward + backward of a layer captured into one CUDA graph over static tensors.
+
+    A recompile (capacities changed) invalidates the captured kernel arguments; call
+    `recapture()` (done automatically when `layer.layout_generation` changed)."""
+
+    def __init__(self, layer, x, params, dy, grads, y=None):
+        self.layer = layer
+        self.x, self.params, self.dy, self.grads = x, params, dy, grads
+        self.y = y if y is not None else torch.empty(x.shape[0], layer.d_out, dtype=layer.tdtype,
+                                                     device=layer.device)
+        self.graph = None
+        self.gen = None
+        self.recapture()
+
+    def _body(self):
+        p = self.params
+        self.layer.forward(self.x, p["w_gate"], p["w1"], p["b1"], p["w2"], p["b2"], y=self.y)
+        self.layer.backward(self.dy, grads=self.grads)
+
+    def recapture(self):
+        s = torch.cuda.Stream(self.layer.device)
+        s.wait_stream(torch.cuda.current_stream(self.layer.device))
+        with torch.cuda.stream(s):
+            self._body()                   # warm-up outside capture (attributes, maps)
+        torch.cuda.current_stream(self.layer.device).wait_stream(s)
+        torch.cuda.synchronize(self.layer.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._body()
+        self.graph = g
+        self.gen = self.layer.layout_generation
+
+    def replay(self):
+        if self.gen != self.layer.layout_generation:
+            self.recapture()
+        self.graph.replay()
+        return self.y

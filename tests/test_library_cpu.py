@@ -71,3 +71,15 @@ def test_config_validation_before_cuda(lib):
     for cfg in bad:
         assert lib.moe_init(C.byref(cfg), C.byref(h)) == 2
     assert lib.moe_init(None, C.byref(h)) == 1
+
+
+def test_caching_trigger_matches_oracle_and_spec(lib):
+    from paper_2205_01848_b200 import caching_trigger
+    # S:461-464
+    assert caching_trigger(0.99, 5, False) is False
+    assert caching_trigger(0.97, 12, False) is True
+    assert caching_trigger(0.88, 48, True) is False
+    for h in np.linspace(0.0, 1.0, 41):
+        for ep in (0, 9, 10, 50):
+            for en in (False, True):
+                assert caching_trigger(h, ep, en) == O.caching_trigger(h, ep, en)
