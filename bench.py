@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=8192)
+    ap.add_argument("--graph", action="store_true",
+                    help="also time the step replayed from a CUDA graph (reported as graph_*)")
     ap.add_argument("--ep", action="store_true",
                     help="force the expert-parallel (NCCL) path at N=1 (loopback)")
     return ap.parse_args()
@@ -210,6 +212,9 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
 
     def barrier():
+        # drain our stream first: the layer's NCCL exchanges share torch's communicator, and
+        # a torch collective must not overlap them on another stream
+        torch.cuda.synchronize(dev)
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize(dev)
@@ -244,6 +249,21 @@ def run_ours(args):
     ms = max_over_ranks(ms)
     ms_step = ms / args.steps
     value = T * ws * args.steps / (ms / 1e3)
+
+    graph_ms = None
+    if args.graph and not use_ep:   # EP has a host sync per forward: not capturable
+        from paper_2205_01848_b200 import GraphedStep
+        gs = GraphedStep(layer, g["x"], g, dy, grads, y=y)
+        for _ in range(3):
+            gs.replay()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            gs.replay()
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        graph_ms = max_over_ranks(g0.elapsed_time(g1)) / args.steps
 
     # ---------------- per-kernel rooflines ----------------
     pk = peaks()
@@ -368,6 +388,9 @@ def run_ours(args):
             "cpu_baseline": cpu_base,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "graph": (None if graph_ms is None else
+                      {"ms_per_step": round(graph_ms, 4),
+                       "value": round(T * ws / (graph_ms / 1e3), 1)}),
             "clocks": clocks,
         }
         print(json.dumps(out), flush=True)
