@@ -258,6 +258,14 @@ MOE_API moe_status_t moe_ep_plan(int32_t R, int32_t rank, int32_t n, const int32
                                  int32_t* send_off_out, int32_t* kept_local_out,
                                  int64_t* drops_out);
 
+/* Virtual communicator for testing the expert-parallel path on ONE GPU: R ranks run as R
+   host threads of one process (one handle per thread, moe_config_t.nccl_comm = *comm_out,
+   world_size = R, rank = r); exchanges are device-to-device copies with an event rendezvous
+   that reproduces NCCL's grouped send/recv matching, all-gather and (fixed rank order)
+   all-reduce semantics.  Every rank must issue the same sequence of layer calls. */
+MOE_API moe_status_t moe_vcomm_create(int32_t R, void** comm_out);
+MOE_API moe_status_t moe_vcomm_destroy(void* comm);
+
 /* Number of kernels the library launched since the handle was created (for bench
    accounting of "our kernels in the timed region"). */
 MOE_API moe_status_t moe_launch_count(moe_handle_t h, int64_t* out);

@@ -96,6 +96,8 @@ EXPORTS = {
     "moe_metrics_pop": ([C.c_void_p, C.c_int32, C.POINTER(Metrics), C.POINTER(C.c_int32)], C.c_int),
     "moe_caching_trigger": ([C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_int32,
                              C.POINTER(C.c_int32)], C.c_int),
+    "moe_vcomm_create": ([C.c_int32, C.POINTER(C.c_void_p)], C.c_int),
+    "moe_vcomm_destroy": ([C.c_void_p], C.c_int),
     "moe_ep_plan": ([C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                      C.POINTER(C.c_int32), C.POINTER(C.c_int64)], C.c_int),

@@ -51,4 +51,8 @@ moe_status_t ep_from_experts(EpState* s, const EpPlan& P, const void* src, void*
 moe_status_t ep_allreduce_f32(EpState* s, float* buf, size_t count, cudaStream_t st,
                               std::string* err);
 
+// Virtual communicator (R ranks as threads of one process on one GPU; test transport).
+moe_status_t vcomm_create(int R, void** out);
+moe_status_t vcomm_destroy(void* p);
+
 }  // namespace moe

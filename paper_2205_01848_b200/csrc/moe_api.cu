@@ -753,6 +753,9 @@ moe_status_t moe_set_spec_grads(moe_handle_t h, const void* dspec, const float* 
   return MOE_OK;
 }
 
+moe_status_t moe_vcomm_create(int32_t R, void** comm_out) { return vcomm_create(R, comm_out); }
+moe_status_t moe_vcomm_destroy(void* comm) { return vcomm_destroy(comm); }
+
 moe_status_t moe_launch_count(moe_handle_t h, int64_t* out) {
   if (!h || !out) return MOE_ERR_INVALID_ARG;
   *out = h->launches;

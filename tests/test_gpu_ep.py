@@ -58,3 +58,105 @@ def test_ep_loopback_cached(comm):
                                       cached=lambda fresh: perturb_cached(fresh, n, 0.03))
     assert_routing_exact(gpu, st, k, check_token_of_slot=False)
     assert_values(gpu, st, gr, ol, "bf16")
+
+
+def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0):
+    """R expert-parallel ranks as threads on one GPU over the library's virtual communicator,
+    against the single-GPU layer on the concatenated batch."""
+    import ctypes as C
+    import threading
+    from paper_2205_01848_b200 import MoELayer, _lib
+    from synth import make_dy, make_layer
+    lib = _lib.load()
+    comm = C.c_void_p()
+    assert lib.moe_vcomm_create(R, C.byref(comm)) == 0
+    Tg = R * T
+    cpu = make_layer(n, d, f, d, Tg, dtype)
+    g = {kk: v.cuda() for kk, v in cpu.items()}
+    dy = make_dy(Tg, d, dtype).cuda()
+    caps = O.capacities_from_factors([1.0] * n, Tg, k)
+    cached = None
+    if cached_frac is not None:
+        from synth import perturb_cached
+        fresh = O.topk_sorted(O.gate_logits(to_np(cpu["x"]), to_np(cpu["w_gate"])), k)
+        cached = torch.from_numpy(perturb_cached(fresh, n, cached_frac)).cuda()
+    layers = [MoELayer(n, k, d, f, 0, T, dtype, renorm, world_size=R, rank=r,
+                       nccl_comm=comm.value, device="cuda") for r in range(R)]
+    out = [None] * R
+    errs = []
+
+    def work(r):
+        try:
+            L = layers[r]
+            L.set_capacities(caps)
+            L.set_balance_loss(lam)
+            if cached is not None:
+                L.set_cached_assignment(cached[r * T:(r + 1) * T].contiguous())
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                xs = g["x"][r * T:(r + 1) * T]
+                y = L.forward(xs, g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+                gr = L.backward(dy[r * T:(r + 1) * T].contiguous())
+                rt = L.routing(T)
+                s.synchronize()
+            out[r] = (y, gr, rt, L.stats())
+        except Exception as ex:  # surfaced in the main thread
+            errs.append(ex)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    ref = MoELayer(n, k, d, f, 0, Tg, dtype, renorm, device="cuda")
+    ref.set_capacities(caps)
+    ref.set_balance_loss(lam)
+    if cached is not None:
+        ref.set_cached_assignment(cached)
+    y_ref = ref.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+    st_ref = ref.stats()
+    gr_ref = ref.backward(dy)
+    rt_ref = ref.routing(Tg)
+    torch.cuda.synchronize()
+    lib.moe_vcomm_destroy(comm)
+    return out, (y_ref, gr_ref, rt_ref, st_ref)
+
+
+def to_np(t):
+    return t.detach().float().cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("R", [2, 4])
+@pytest.mark.parametrize("dtype,k,renorm", [("bf16", 2, 1), ("bf16", 1, 0), ("f32", 2, 0)])
+def test_ep_virtual_ranks_match_single_gpu(R, dtype, k, renorm):
+    n, T, d, f = 16, 512, 64, 128
+    out, (y_ref, gr_ref, rt_ref, st_ref) = _run_virtual(R, n, k, T, d, f, dtype, renorm)
+    nl = n // R
+    # routing: global slots, counts and drops are independent of R (reading 12)
+    assert np.array_equal(np.concatenate([o[2]["slot_of"].cpu().numpy() for o in out]),
+                          rt_ref["slot_of"].cpu().numpy())
+    for o in out:
+        assert o[3]["counts"] == st_ref["counts"] and o[3]["drops"] == st_ref["drops"]
+    # token-side outputs bit-identical; expert gradients of each rank's experts bit-identical
+    assert torch.equal(torch.cat([o[0] for o in out]), y_ref)
+    assert torch.equal(torch.cat([o[1]["dx"] for o in out]), gr_ref["dx"])
+    for r, o in enumerate(out):
+        sl = slice(r * nl, (r + 1) * nl)
+        for key in ("dw1", "db1", "dw2", "db2"):
+            assert torch.equal(o[1][key][sl], gr_ref[key][sl]), (r, key)
+        # dW_g: per-rank partials all-reduced in fp32 (a different summation split)
+        a, b = to_np(o[1]["dw_gate"]), to_np(gr_ref["dw_gate"])
+        assert np.abs(a - b).max() <= (1e-5 if dtype == "f32" else 1e-2) * np.abs(b).max()
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_ep_virtual_ranks_cached_and_balance():
+    n, T, d, f, R = 16, 512, 64, 128, 2
+    out, (y_ref, gr_ref, rt_ref, st_ref) = _run_virtual(R, n, 2, T, d, f, "bf16", 1,
+                                                        cached_frac=0.03, lam=0.2)
+    assert torch.equal(torch.cat([o[0] for o in out]), y_ref)
+    assert sum(o[3]["hit_count"] for o in out) == st_ref["hit_count"]
+    assert np.allclose(np.concatenate([o[2]["dl"].cpu().numpy() for o in out]),
+                       rt_ref["dl"].cpu().numpy(), rtol=1e-5, atol=1e-7)
