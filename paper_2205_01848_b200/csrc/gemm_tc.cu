@@ -396,6 +396,24 @@ static int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64
 cudaError_t launch_tc2_kind(int kind, int BN, const CUtensorMap& a, const CUtensorMap& b,
                             const TcParams& p, int grid, cudaStream_t s);
 
+static int tc_pf() {  // MOE_TC_PF: k-blocks of B prefetched to L2 for the next wave
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_TC_PF");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+static int tc_sched() {  // MOE_TC_SCHED: 2-CTA tile schedule (see TcParams::sched)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_TC_SCHED");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 // 2-CTA (cta_group::2) kernels need BN in {128, 256}.  MOE_TC_1CTA=<bitmask of TcKind> forces
 // the 1-CTA form for those kinds (debug / A-B comparisons).
 static bool use_2cta(int N, int kind) {
@@ -468,6 +486,8 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   p.bias = (const __nv_bfloat16*)bias; p.C = (__nv_bfloat16*)C; p.ldc = ldc; p.ct = ct;
   p.mask = mask;
   p.bias_part = two ? bias_part : nullptr;
+  p.sched = tc_sched();
+  p.pf_kb = tc_pf();
   if (two)
     TC_CUDA(launch_tc2_kind(KIND, bn, ma, mb, p, g_num_sms & ~1, s));
   else
@@ -486,6 +506,8 @@ static moe_status_t wgrad(const void* Abuf, int M, const void* Bbuf, int N, int6
   p.kept = kept; p.mtile_prefix = nullptr; p.n_local = n_local; p.M = M; p.N = N; p.K = 0;
   p.C = (__nv_bfloat16*)Out; p.bias_out = (__nv_bfloat16*)bias_out; p.accumulate = accumulate;
   p.ct = ct;
+  p.sched = tc_sched();
+  p.pf_kb = tc_pf();
   if (use_2cta(N, TC_WGRAD))
     TC_CUDA(launch_tc2_kind(TC_WGRAD, pick_bn(N), ma, mb, p, g_num_sms & ~1, s));
   else

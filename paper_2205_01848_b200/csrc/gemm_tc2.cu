@@ -56,6 +56,12 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
       : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                         uint32_t accum) {
   asm volatile(
@@ -155,19 +161,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 
   const int NT = (p.N + BN - 1) / BN;
   const int MT = Tr::kgroup ? (p.M + TC2_M - 1) / TC2_M : 0;
+  // tile schedule (identical in every role): round-robin or a contiguous chunk per pair
+  int t_begin = pair, t_step = npairs, t_end = 0x7fffffff;
+  if (p.sched != 0) {
+    const int total = total_tiles<Tr::kgroup>(s_prefix, n_local, MT, NT);
+    const int chunk = (total + npairs - 1) / npairs;
+    t_begin = pair * chunk;
+    t_end = min(total, t_begin + chunk);
+    t_step = 1;
+  }
+  const bool nfast = p.sched == 1;
 
   if (warp == 0) {
     if (lane == 0) {
       // ============================ TMA producer (both CTAs) ============================
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair;; t += npairs) {
+      for (int t = t_begin; t < t_end; t += t_step) {
         int e, mt, nt;
-        if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+        if (!decode_tile_ord<Tr::kgroup>(t, s_prefix, n_local, MT, NT, nfast, e, mt, nt)) break;
         const int m0 = mt * TC2_M + (int)crank * TC_BM;   // this CTA's A rows
         const int n0 = nt * BN + (int)crank * BNH;        // this CTA's B columns
         const int base = p.ct.base[e];
         const int nk = Tr::kgroup ? (p.kept[e] + TC_BK - 1) / TC_BK : p.K / TC_BK;
+        if (p.pf_kb > 0 && t_step > 1) {
+          // Warm L2 with the NEXT wave's B tile: only the pair that will be its first user
+          // (m-tile 0) prefetches, so the other pairs of that wave hit L2 (one DRAM read).
+          int e2, mt2, nt2;
+          if (decode_tile_ord<Tr::kgroup>(t + t_step, s_prefix, n_local, MT, NT, nfast, e2, mt2,
+                                          nt2) && mt2 == 0) {
+            const int n2 = nt2 * BN + (int)crank * BNH;
+            const int nk2 = Tr::kgroup ? (p.kept[e2] + TC_BK - 1) / TC_BK : p.K / TC_BK;
+            const int npf = nk2 < p.pf_kb ? nk2 : p.pf_kb;
+            for (int kb = 0; kb < npf; ++kb) {
+              if (Tr::b_mn) {
+                const int krow = Tr::kgroup ? p.ct.base[e2] + kb * TC_BK : e2 * p.K + kb * TC_BK;
+                for (int j = 0; j < BNH / 64; ++j) tma_prefetch_2d(&tmB, n2 + j * 64, krow);
+              } else {
+                tma_prefetch_2d(&tmB, kb * TC_BK, e2 * p.N + n2);
+              }
+            }
+          }
+        }
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           // the bias warps observe every use of every stage (in lockstep with empty[s], so
@@ -202,9 +237,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = pair;; t += npairs, ++it) {
+      for (int t = t_begin; t < t_end; t += t_step, ++it) {
         int e, mt, nt;
-        if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+        if (!decode_tile_ord<Tr::kgroup>(t, s_prefix, n_local, MT, NT, nfast, e, mt, nt)) break;
         const int acc = it & 1;
         const int nk = Tr::kgroup ? (p.kept[e] + TC_BK - 1) / TC_BK : p.K / TC_BK;
         mbar_wait_cluster(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
@@ -245,9 +280,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const int bj = cb >> 3, bc = cb & 7;
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair;; t += npairs) {
+      for (int t = t_begin; t < t_end; t += t_step) {
         int e, mt, nt;
-        if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+        if (!decode_tile_ord<Tr::kgroup>(t, s_prefix, n_local, MT, NT, nfast, e, mt, nt)) break;
         const int nk = (p.kept[e] + TC_BK - 1) / TC_BK;
         float a8[8];
 #pragma unroll
@@ -296,9 +331,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int row_in_tile = (int)crank * TC_BM + q * 32 + lane;
     const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty_bar[0]), 0);
     int it = 0;
-    for (int t = pair;; t += npairs, ++it) {
+    for (int t = t_begin; t < t_end; t += t_step, ++it) {
       int e, mt, nt;
-      if (!decode_tile<Tr::kgroup>(t, s_prefix, n_local, MT, NT, e, mt, nt)) break;
+      if (!decode_tile_ord<Tr::kgroup>(t, s_prefix, n_local, MT, NT, nfast, e, mt, nt)) break;
       const int acc = it & 1;
       const int m0 = mt * TC2_M, n0 = nt * BN;
       const int row = m0 + row_in_tile;

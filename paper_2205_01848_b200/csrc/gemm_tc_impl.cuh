@@ -27,6 +27,9 @@ struct TcParams {
                                 // of dA, [sum_e ceil(kept_e/256) * 8][N] fp32 (db1 partials)
   uint32_t* mask;               // FWD1 writes / DGRAD_A reads: bit j of word [row][c] = (H > 0)
                                 // for column 32c + j (relu' mask, 16x fewer bytes than H)
+  int pf_kb;                    // 2-CTA: k-blocks of the next wave's B tile to prefetch to L2
+  int sched;                    // 2-CTA tile schedule: 0 round-robin (m fastest),
+                                // 1 contiguous chunk per CTA pair (n fastest), 2 chunk (m fastest)
   CapTable ct;                  // base rows of each local expert region
 };
 
@@ -38,6 +41,46 @@ struct KindTraits {
 };
 
 // Decode a linear tile index into (expert, m0, n0).
+// total number of tiles (M-grouped: prefix of m-tiles x NT; K-grouped: n_local x MT x NT)
+template <bool KG>
+__device__ __forceinline__ int total_tiles(const int32_t* s_prefix, int n_local, int MT, int NT) {
+  return KG ? n_local * MT * NT : s_prefix[n_local] * NT;
+}
+
+// Like decode_tile, with the order inside an expert selectable: nfast = n-tile fastest (the
+// A m-tile is reused by consecutive tiles of one CTA pair) or m-tile fastest.
+template <bool KG>
+__device__ __forceinline__ bool decode_tile_ord(int t, const int32_t* s_prefix, int n_local,
+                                                int MT, int NT, bool nfast, int& e, int& mt,
+                                                int& nt) {
+  int r, mte;
+  if (KG) {
+    const int per = MT * NT;
+    e = t / per;
+    if (e >= n_local) return false;
+    r = t - e * per;
+    mte = MT;
+  } else {
+    if (t >= s_prefix[n_local] * NT) return false;
+    int lo = 0, hi = n_local - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (s_prefix[mid] * NT <= t) lo = mid; else hi = mid - 1;
+    }
+    e = lo;
+    r = t - s_prefix[e] * NT;
+    mte = s_prefix[e + 1] - s_prefix[e];
+  }
+  if (nfast) {
+    mt = r / NT;
+    nt = r - mt * NT;
+  } else {
+    nt = r / mte;
+    mt = r - nt * mte;
+  }
+  return true;
+}
+
 template <bool KG>
 __device__ __forceinline__ bool decode_tile(int t, const int32_t* s_prefix, int n_local, int MT,
                                             int NT, int& e, int& mt, int& nt) {
