@@ -38,8 +38,7 @@ struct GateFwdParams {
 
 struct GateDxParams {
   int T, n_pad, k, d;
-  const int32_t* idx;
-  const int32_t* slot_of;
+  const int32_t* grow;    // [T x k] dX row of each (token, r) pair or -1 (from combine_bwd)
   const __nv_bfloat16* dxbuf;  // [rows x d]
   __nv_bfloat16* dx;           // [T x d]
   int accumulate;
@@ -393,62 +392,86 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
     }
     __syncwarp();
   } else if (warp >= 4) {
-    // Epilogue: warp (q, half) owns token rows 32q..32q+31 (its TMEM lanes) x HC columns.
-    // The gathered dX rows and the dx output go through a per-warp shared-memory staging
-    // buffer so every global access is a coalesced 16-byte-per-lane row segment
-    // (a thread-per-row access pattern would touch 32 rows per instruction).
+    // Epilogue, software-pipelined over this CTA's tiles.  Warp (q, half) owns token rows
+    // 32q..32q+31 (its TMEM lanes) x HC columns.  The dX rows gathered for the NEXT tile are
+    // fetched with cp.async into a second shared-memory staging buffer while the current
+    // tile is combined, and dx leaves through the staging buffer with coalesced stores, so a
+    // tile costs about one memory round trip instead of three dependent ones.
     const int q = warp & 3, half = (warp - 4) >> 2;
     constexpr int HC = BN / 2;    // columns per warp
     constexpr int RB = HC * 2;    // bytes of one row segment
     constexpr int RS = RB + 16;   // padded staging stride (conflict-free 16-B row reads)
     constexpr int LPR = RB / 16;  // lanes per row segment
     constexpr int RPI = 32 / LPR; // rows per cooperative instruction
-    uint8_t* stg = smem + STAGES * STAGE_BYTES + 256 + (warp - 4) * 32 * RS;
+    constexpr int KS = 2;         // rows per token staged asynchronously (k > 2: direct loads)
+    uint8_t* stg_w = smem + STAGES * STAGE_BYTES + 256 + (warp - 4) * (2 * KS * 32 * RS);
     const int sub = lane / LPR, seg = lane % LPR;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
-      const int acc = it & 1;
+    const int kk = p.k;
+    auto stg = [&](int par, int r) { return stg_w + (par * KS + r) * 32 * RS; };
+    auto load_rows = [&](int tile, int* rows) {
+      const int t = (tile % MT) * TC_BM + q * 32 + lane;
+#pragma unroll
+      for (int r = 0; r < MOE_MAX_K; ++r)
+        rows[r] = (tile < total && t < p.T && r < kk) ? p.grow[(size_t)t * kk + r] : -1;
+    };
+    auto issue_gather = [&](int tile, int par, const int* rows) {
+      if (tile < total) {
+        const int col_base = (tile / MT) * BN + half * HC;
+#pragma unroll
+        for (int r = 0; r < KS; ++r) {
+          if (r >= kk) break;
+#pragma unroll
+          for (int i = 0; i < 32; i += RPI) {
+            const int rowid = __shfl_sync(0xffffffffu, rows[r], i + sub);
+            if (rowid >= 0)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                               smem_u32(stg(par, r) + (i + sub) * RS + seg * 16)),
+                           "l"(p.dxbuf + (size_t)rowid * p.d + col_base + seg * 8)
+                           : "memory");
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int rows_cur[MOE_MAX_K], rows_nxt[MOE_MAX_K];
+    int tile = blockIdx.x;
+    load_rows(tile, rows_cur);
+    issue_gather(tile, 0, rows_cur);
+    for (int it = 0; tile < total; tile += gridDim.x, ++it) {
+      const int acc = it & 1, par = it & 1;
       const int mt = tile % MT, nt = tile / MT;
       const int t0w = mt * TC_BM + q * 32;
       const int t = t0w + lane;
       const bool valid = t < p.T;
-      int rows[MOE_MAX_K];
-      int nr = 0;
-      if (valid) {
-        for (int r = 0; r < p.k; ++r) {
-          const int sl = p.slot_of[(size_t)t * p.k + r];
-          if (sl >= 0) rows[nr++] = p.ct.base[p.idx[(size_t)t * p.k + r]] + sl;
-        }
-      }
-      const int maxnr = __reduce_max_sync(0xffffffffu, nr);
       const int col_base = nt * BN + half * HC;
+      load_rows(tile + gridDim.x, rows_nxt);
+      issue_gather(tile + gridDim.x, par ^ 1, rows_nxt);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's gather landed
+      __syncwarp();
       float v[HC];
 #pragma unroll
       for (int i = 0; i < HC; ++i) v[i] = 0.f;
-      for (int r = 0; r < maxnr; ++r) {  // expert path first, r order (as the SIMT form)
-        int rr = -1;
 #pragma unroll
-        for (int q2 = 0; q2 < MOE_MAX_K; ++q2)
-          if (q2 == r && q2 < nr) rr = rows[q2];
-#pragma unroll
-        for (int i = 0; i < 32; i += RPI) {
-          const int rowid = __shfl_sync(0xffffffffu, rr, i + sub);
-          if (rowid >= 0) {
-            const uint4 val = ld_nc_v4(p.dxbuf + (size_t)rowid * p.d + col_base + seg * 8);
-            *reinterpret_cast<uint4*>(stg + (i + sub) * RS + seg * 16) = val;
-          }
-        }
-        __syncwarp();
-        if (rr >= 0) {
+      for (int r = 0; r < MOE_MAX_K; ++r) {  // expert path first, r order (as the SIMT form)
+        if (r >= kk) break;
+        if (rows_cur[r] < 0) continue;
+        if (r < KS) {
 #pragma unroll
           for (int c = 0; c < HC / 8; ++c) {
             float xv[8];
-            unpack(*reinterpret_cast<const uint4*>(stg + lane * RS + c * 16), xv, __nv_bfloat16());
+            unpack(*reinterpret_cast<const uint4*>(stg(par, r) + lane * RS + c * 16), xv, __nv_bfloat16());
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[8 * c + j] += xv[j];
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < HC / 8; ++c) {
+            float xv[8];
+            unpack(ld_nc_v4(p.dxbuf + (size_t)rows_cur[r] * p.d + col_base + 8 * c), xv, __nv_bfloat16());
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[8 * c + j] += xv[j];
           }
         }
-        __syncwarp();
       }
       mbar_wait(&b.tfull[acc], (it >> 1) & 1);
       tc_fence_after();
@@ -472,19 +495,23 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
           for (int j = 0; j < 8; ++j) v[8 * c + j] += o[j];
         }
       }
+      __syncwarp();  // every lane finished reading stg(par, 0) before it is reused for dx
 #pragma unroll
       for (int c = 0; c < HC / 8; ++c)
-        *reinterpret_cast<uint4*>(stg + lane * RS + c * 16) = pack(v + 8 * c, __nv_bfloat16());
+        *reinterpret_cast<uint4*>(stg(par, 0) + lane * RS + c * 16) = pack(v + 8 * c, __nv_bfloat16());
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < 32; i += RPI) {
         const int tok = t0w + i + sub;
         if (tok < p.T)
           st_v4(p.dx + (size_t)tok * p.d + col_base + seg * 8,
-                *reinterpret_cast<const uint4*>(stg + (i + sub) * RS + seg * 16));
+                *reinterpret_cast<const uint4*>(stg(par, 0) + (i + sub) * RS + seg * 16));
       }
       __syncwarp();
+#pragma unroll
+      for (int r = 0; r < MOE_MAX_K; ++r) rows_cur[r] = rows_nxt[r];
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   teardown(tmem_base, 2 * BN, warp);
 }
@@ -694,7 +721,7 @@ cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb
       !map2d(&mw, wg, d, n, 64, 64))
     return cudaErrorInvalidValue;
   GateDxParams p{};
-  p.T = T; p.n_pad = n_pad; p.k = k; p.d = d; p.idx = b.idx; p.slot_of = b.slot_of;
+  p.T = T; p.n_pad = n_pad; p.k = k; p.d = d; p.grow = b.grow;
   p.dxbuf = (const __nv_bfloat16*)dxbuf; p.dx = (__nv_bfloat16*)dx; p.accumulate = accumulate;
   p.ct = ct;
   const int bn = d % 128 == 0 ? 128 : 64;
@@ -704,12 +731,12 @@ cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb
 #define GX(BN, ST)                                                                       \
   {                                                                                      \
     auto kf = gate_dx_tc_kernel<BN, ST>;                                                 \
-    size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 8 * 32 * (BN + 16);                  \
+    size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 8 * 2 * 2 * 32 * (BN + 16);          \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \
     kf<<<grid, GX_THREADS, sm, s>>>(mhi, mlo, mw, p);                                     \
   }
-  if (bn == 128) GX(128, 4) else GX(64, 6)
+  if (bn == 128) GX(128, 2) else GX(64, 4)
 #undef GX
   return cudaGetLastError();
 }

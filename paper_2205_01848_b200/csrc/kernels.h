@@ -31,6 +31,7 @@ struct RouteBufs {
   const void* dspec;      // [T*k x d_out] gradient w.r.t. the spec rows (backward input)
   const float* dw_ext;    // [T x k] extra gradient w.r.t. the gate weights (backward input)
   const float* bal_g;     // [n] balance-term coefficients lambda*n*T_i/T_g (backward)
+  int32_t* grow;          // [T x k] token-side dO/dX row of each pair or -1 (combine_bwd)
 };
 
 // dtype: 0 = fp32, 1 = bf16 for every templated launcher below.

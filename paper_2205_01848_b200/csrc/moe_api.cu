@@ -23,7 +23,7 @@ using namespace moe;
 
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
-      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, ep_all, sendbuf, oret, dwg32, total;
+      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, grow, ep_all, sendbuf, oret, dwg32, total;
 };
 
 struct moe_ctx {
@@ -122,6 +122,7 @@ void compute_layout(moe_ctx* h) {
   // db1 partials: sum_e ceil(kept_e/256) <= rows/256 + n_local tiles x 8 rows x f
   // balance term: partial column sums [ceil(T/64) x n], gsum [n], g [n], aux [1]
   L.bal = take(((T + 63) / 64 + 3) * n * 4 + 256);
+  L.grow = take(T * k * 4);
   L.bpart = take(h->dtype == MOE_BF16 ? ((size_t)h->rows / 256 + h->n_local) * 8 * h->f * 4 : 0);
   const bool ep = h->use_ep;
   L.ep_all = take(ep ? (size_t)h->R * n * 4 : 0);
@@ -153,6 +154,7 @@ void bind_buffers(moe_ctx* h) {
   r.flags = meta + 781;
   r.ticket = (uint32_t*)(meta + 782);
   r.token_of_slot = (int32_t*)(b + L.token_of_slot);
+  r.grow = (int32_t*)(b + L.grow);
 }
 
 void relayout(moe_ctx* h) {

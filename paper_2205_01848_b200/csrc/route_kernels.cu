@@ -549,7 +549,8 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
     const float* __restrict__ logits, CapTable ct, int Tn, int k, int n, int dout, int renorm,
     T* __restrict__ dobuf, float* __restrict__ dw, float* __restrict__ dl,
     __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad, const T* __restrict__ dspec,
-    const float* __restrict__ dw_ext, const float* __restrict__ bal_g) {
+    const float* __restrict__ dw_ext, const float* __restrict__ bal_g,
+    int32_t* __restrict__ grow) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
@@ -631,7 +632,10 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   }
 #pragma unroll
   for (int r = 0; r < KM; ++r)
-    if (r < k && lane == r) dw[(size_t)t * k + r] = dwr[r];
+    if (r < k && lane == r) {
+      dw[(size_t)t * k + r] = dwr[r];
+      if (grow) grow[(size_t)t * k + r] = rows[r];  // the gate-dx kernel's gather table
+    }
   float m = -INFINITY, sp = 0.f, cb = 0.f;
   if (need_p) {
 #pragma unroll
@@ -705,7 +709,7 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
                                                    b.slot_of, b.logits, ct, T_, k, n, d_out,   \
                                                    renorm, (T*)dobuf, b.dw, b.dl,              \
                                                    (__nv_bfloat16*)dlb, maxT, n_pad,           \
-                                                   (const T*)b.dspec, b.dw_ext, b.bal_g)
+                                                   (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow)
   const int km = k == 1 ? 1 : (k == 2 ? 2 : 8);
   if (vpl <= 2) { if (km == 1) CB(2, 1); else if (km == 2) CB(2, 2); else CB(2, 8); }
   else if (vpl <= 4) { if (km == 1) CB(4, 1); else if (km == 2) CB(4, 2); else CB(4, 8); }
