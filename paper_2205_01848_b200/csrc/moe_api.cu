@@ -360,7 +360,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   KL(h, T > 0, "route_hist", sd, launch_route_hist(rb.idx, T, k, n, rb.tile_hist, sd));
   KL(h, 1, "route_scan", sd, launch_route_scan(rb.tile_hist, ntiles, n, h->ct, rb, sd));
   if (!h->use_ep) {
-    KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->cts, rb, X, sd));
+    KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->cts, rb, X, rb.kept, sd));
   } else {
     // C1 + the single host sync of EP v1: all-gather the per-rank pre-drop counts, then every
     // rank derives the same global slot offsets, kept counts and message sizes (reading 12).
@@ -382,11 +382,12 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     CUDA_TRY(h, cudaMemcpyAsync(rb.drops, &drops, 8, cudaMemcpyHostToDevice, sd));
     void* sendbuf = ws + h->L.sendbuf;
     KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, (int64_t)h->rank * T,
-                                                 h->cts, rb, sendbuf, sd));
+                                                 h->cts, rb, sendbuf, nullptr, sd));
     st = ep_to_experts(h->ep, P, sendbuf, X, h->ct, d, (int)h->s, sd, &err);   // C2
     if (st != MOE_OK) return fail(h, st, err);
+    // pad rows of the received regions (single GPU: fused into the dispatch kernel)
+    KL(h, 1, "zero_pad", sd, launch_zero_pad(dt, X, d, rb.kept, h->n_local, h->ct, sd));
   }
-  KL(h, 1, "zero_pad", sd, launch_zero_pad(dt, X, d, rb.kept, h->n_local, h->ct, sd));
   // expert FFN: H = relu(X W1^T + b1); O = H W2^T + b2 over kept_e rows per local expert
   const int nl = h->n_local;
   const char* w1 = (const char*)a->w1 + (size_t)h->e_lo * f * d * h->s;
@@ -492,15 +493,16 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                  ? (const float*)(ws + h->L.bal) + (size_t)((h->maxT + 63) / 64) * n + n
                  : nullptr;
   KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O_tok, rb, T, k, n, dout, h->renorm, h->cts,
-                                                     dO_tok, dlb, h->maxT, h->n_pad, s0));
+                                                     dO_tok, dlb, h->maxT, h->n_pad,
+                                                     h->use_ep ? nullptr : rb.kept, s0));
   rb.dspec = nullptr;
   rb.dw_ext = nullptr;
   rb.bal_g = nullptr;
   if (h->use_ep) {  // C4: dO rows to the expert owners
     moe_status_t st = ep_to_experts(h->ep, h->plan, dO_tok, dO, h->ct, dout, (int)h->s, s0, &err);
     if (st != MOE_OK) return fail(h, st, err);
+    KL(h, 1, "zero_pad", s0, launch_zero_pad(dt, dO, dout, kept_local, nl, h->ct, s0));
   }
-  KL(h, 1, "zero_pad", s0, launch_zero_pad(dt, dO, dout, kept_local, nl, h->ct, s0));
   const char* w1 = (const char*)fa.w1 + (size_t)h->e_lo * f * d * h->s;
   const char* w2 = (const char*)fa.w2 + (size_t)h->e_lo * dout * f * h->s;
   char* dw1 = a->dw1 ? (char*)a->dw1 + (size_t)h->e_lo * f * d * h->s : nullptr;

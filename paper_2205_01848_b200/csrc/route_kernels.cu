@@ -236,20 +236,36 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // one warp: parallel loads, warp scan for the GEMM m-tile prefix
+    const int lane = threadIdx.x;
     long long dr = 0;
-    int pre = 0;
-    for (int q = 0; q < n; ++q) {
-      int c = *((volatile int32_t*)counts + q);
-      int kq = min(c, ct.cap[q]);
-      kept[q] = kq;
-      dr += (long long)(c - kq);
-      mtile_prefix[q] = pre;
-      pre += (kq + 127) / 128;
+    int carry = 0;
+    for (int q0 = 0; q0 < n; q0 += 32) {
+      const int q = q0 + lane;
+      int kq = 0;
+      if (q < n) {
+        const int c = *((volatile int32_t*)counts + q);
+        kq = min(c, ct.cap[q]);
+        kept[q] = kq;
+        dr += (long long)(c - kq);
+      }
+      const int v = (kq + 127) / 128;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (q < n) mtile_prefix[q] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    mtile_prefix[n] = pre;
-    *drops = dr;
-    *ticket = 0u;  // self-reset for the next launch
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dr += __shfl_xor_sync(0xffffffffu, dr, o);
+    if (lane == 0) {
+      mtile_prefix[n] = carry;
+      *drops = dr;
+      *ticket = 0u;  // self-reset for the next launch
+    }
   }
 }
 
@@ -267,12 +283,35 @@ cudaError_t launch_route_scan(const int32_t* hist, int ntiles, int n, const CapT
 // copies its tokens' rows x[t] -> X_buf[base_e + slot] with 16-byte vectors (row read once,
 // written once per kept pair).
 // =====================================================================================
+// Zero rows [kept_e, min(roundup(kept_e, PAD), region end)) of expert regions e = first,
+// first + stride, ... with all threads of the calling block (the token-contraction GEMMs read
+// whole 64-row K-blocks).  Fused into the dispatch / combine-backward kernels on one GPU.
+template <typename T>
+__device__ __forceinline__ void zero_pads_block(T* __restrict__ buf, int cols,
+                                                const int32_t* __restrict__ kept,
+                                                const CapTable& ct, int n, int first,
+                                                int stride) {
+  constexpr int VE = Vec<T>::N;
+  const int nvec = cols / VE;
+  for (int e = first; e < n; e += stride) {
+    const int kp = kept[e];
+    const int r0 = ct.base[e] + kp;
+    const int r1 = min(ct.base[e] + ((kp + MOE_PAD_ROWS - 1) / MOE_PAD_ROWS) * MOE_PAD_ROWS,
+                       ct.base[e + 1]);
+    const size_t total = (size_t)max(r1 - r0, 0) * nvec;
+    for (size_t i = threadIdx.x; i < total; i += blockDim.x)
+      st_v4(buf + (size_t)r0 * cols + i * VE, make_uint4(0, 0, 0, 0));
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) dispatch_kernel(
     const int32_t* __restrict__ idx, const T* __restrict__ x, int Tn, int k, int n, int d,
     long long token_base, CapTable ct, const int32_t* __restrict__ tile_off,
-    int32_t* __restrict__ slot_of, int32_t* __restrict__ token_of_slot, T* __restrict__ xbuf) {
+    int32_t* __restrict__ slot_of, int32_t* __restrict__ token_of_slot, T* __restrict__ xbuf,
+    const int32_t* __restrict__ pad_kept) {
   __shared__ uint32_t masks[MOE_MAX_E][MOE_ROUTE_TILE / 32];
+  if (pad_kept) zero_pads_block(xbuf, d, pad_kept, ct, n, blockIdx.x, gridDim.x);
   __shared__ int32_t srow[MOE_ROUTE_TILE * MOE_MAX_K];  // destination row or -1
   const int tile = blockIdx.x;
   const int t0 = tile * MOE_ROUTE_TILE;
@@ -342,17 +381,17 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
 
 cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T, int k,
                             int n, int d, int64_t token_base, const CapTable& ct,
-                            RouteBufs b, void* xbuf, cudaStream_t s) {
+                            RouteBufs b, void* xbuf, const int32_t* pad_kept, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   int ntiles = (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE;
   if (dtype == 1)
     dispatch_kernel<__nv_bfloat16><<<ntiles, 256, 0, s>>>(
         idx, (const __nv_bfloat16*)x, T, k, n, d, token_base, ct, b.tile_off, b.slot_of,
-        b.token_of_slot, (__nv_bfloat16*)xbuf);
+        b.token_of_slot, (__nv_bfloat16*)xbuf, pad_kept);
   else
     dispatch_kernel<float><<<ntiles, 256, 0, s>>>(idx, (const float*)x, T, k, n, d,
                                                   token_base, ct, b.tile_off, b.slot_of,
-                                                  b.token_of_slot, (float*)xbuf);
+                                                  b.token_of_slot, (float*)xbuf, pad_kept);
   return cudaGetLastError();
 }
 
@@ -550,7 +589,8 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
     T* __restrict__ dobuf, float* __restrict__ dw, float* __restrict__ dl,
     __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad, const T* __restrict__ dspec,
     const float* __restrict__ dw_ext, const float* __restrict__ bal_g,
-    int32_t* __restrict__ grow) {
+    int32_t* __restrict__ grow, const int32_t* __restrict__ pad_kept) {
+  if (pad_kept) zero_pads_block(dobuf, dout, pad_kept, ct, n, blockIdx.x, gridDim.x);
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
@@ -701,7 +741,8 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
 template <typename T>
 static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, int T_, int k,
                                  int n, int d_out, int renorm, const CapTable& ct, void* dobuf,
-                                 void* dlb, int maxT, int n_pad, cudaStream_t s) {
+                                 void* dlb, int maxT, int n_pad, const int32_t* pad_kept,
+                                 cudaStream_t s) {
   dim3 grid((T_ + 7) / 8);
   const int vpl = (d_out / Vec<T>::N + 31) / 32;  // > 8: the kernel loops over 4 KB blocks
 #define CB(V, K)                                                                               \
@@ -709,7 +750,7 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
                                                    b.slot_of, b.logits, ct, T_, k, n, d_out,   \
                                                    renorm, (T*)dobuf, b.dw, b.dl,              \
                                                    (__nv_bfloat16*)dlb, maxT, n_pad,           \
-                                                   (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow)
+                                                   (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow, pad_kept)
   const int km = k == 1 ? 1 : (k == 2 ? 2 : 8);
   if (vpl <= 2) { if (km == 1) CB(2, 1); else if (km == 2) CB(2, 2); else CB(2, 8); }
   else if (vpl <= 4) { if (km == 1) CB(4, 1); else if (km == 2) CB(4, 2); else CB(4, 8); }
@@ -721,12 +762,13 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
 cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, RouteBufs b,
                                int T, int k, int n, int d_out, int renorm,
                                const CapTable& ct, void* dobuf, void* dlb, int maxT, int n_pad,
-                               cudaStream_t s) {
+                               const int32_t* pad_kept, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   if (dtype == 1)
     return combine_bwd_t<__nv_bfloat16>(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf, dlb,
-                                        maxT, n_pad, s);
-  return combine_bwd_t<float>(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf, dlb, maxT, n_pad, s);
+                                        maxT, n_pad, pad_kept, s);
+  return combine_bwd_t<float>(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf, dlb, maxT, n_pad,
+                              pad_kept, s);
 }
 
 // =====================================================================================
