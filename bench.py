@@ -42,7 +42,10 @@ def parse():
     ap.add_argument("--graph", action="store_true",
                     help="also time the step replayed from a CUDA graph (reported as graph_*)")
     ap.add_argument("--ep", action="store_true",
-                    help="force the expert-parallel (NCCL) path at N=1 (loopback)")
+                    help="force the expert-parallel path at N=1 (loopback)")
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="expert-parallel exchange: peer = device-initiated through peer "
+                         "memory over NVLink (N1, default); nccl = grouped send/recv")
     return ap.parse_args()
 
 
@@ -160,8 +163,9 @@ def run_ours(args):
     n, k, d, f, do = cfg.n_experts, cfg.top_k, cfg.d_model, cfg.d_ff, cfg.d_out
     s = 2 if cfg.dtype == "bf16" else 4
     use_ep = ws > 1 or args.ep
+    peer = use_ep and args.transport == "peer"
     comm = 0
-    if use_ep:
+    if use_ep and not peer:
         import torch.distributed as tdist
         if not tdist.is_initialized():  # --ep at N = 1: a 1-rank NCCL group (loopback)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -177,7 +181,14 @@ def run_ours(args):
         g["x"] = make_layer(n, d, 64, do, T, cfg.dtype, "uniform", device=dev, seed_offset=rank)["x"]
     dy = make_dy(T, do, cfg.dtype, device=dev, seed_offset=rank)
     layer = MoELayer(n, k, d, f, do, T, cfg.dtype, cfg.renormalize, world_size=ws if use_ep else 1,
-                     rank=rank if use_ep else 0, nccl_comm=comm, device=dev)
+                     rank=rank if use_ep else 0, nccl_comm=comm, device=dev,
+                     transport="peer" if peer else "nccl")
+    if peer:  # open every rank's peer window (CUDA IPC handles over the process group)
+        if ws > 1:
+            from paper_2205_01848_b200.dist import peer_connect
+            peer_connect(layer)
+        else:
+            layer.peer_attach([layer.peer_window()])
     layer.set_capacity_factors([alpha] * n, T * (ws if use_ep else 1))
     tdt = layer.tdtype
     grads = dict(dx=torch.empty(T, d, dtype=tdt, device=dev),
@@ -251,7 +262,7 @@ def run_ours(args):
     value = T * ws * args.steps / (ms / 1e3)
 
     graph_ms = None
-    if args.graph and not use_ep:   # EP has a host sync per forward: not capturable
+    if args.graph and not (use_ep and not peer):  # NCCL EP syncs the host per forward
         from paper_2205_01848_b200 import GraphedStep
         gs = GraphedStep(layer, g["x"], g, dy, grads, y=y)
         for _ in range(3):
@@ -377,7 +388,8 @@ def run_ours(args):
                                    + (", cached assignments" if args.cached else ""),
                        "tokens_per_gpu": T, "n_experts": n, "top_k": k, "d_model": d, "d_ff": f,
                        "capacity_factor": alpha, "renormalize": cfg.renormalize,
-                       "parallelism": (f"ep{ws} (experts sharded, tokens data-parallel, NCCL)"
+                       "parallelism": (f"ep{ws} (experts sharded, tokens data-parallel, "
+                                       + ("peer memory, device-initiated)" if peer else "NCCL)")
                                        if use_ep else "1 GPU"),
                        "l2": "inputs > L2 (x 134 MB + weights 1 GB), no flush",
                        "kept_assignments": A, "drops": stats["drops"],

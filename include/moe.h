@@ -89,7 +89,18 @@ typedef struct {
                            Expert parameter / gradient tensors keep the full [n, ...] shape;
                            only the local experts' slices are read and written. */
   void*   stream;       /* cudaStream_t all work is ordered on (NULL = legacy default) */
+  int32_t transport;    /* moe_transport_t of the expert-parallel exchanges (R > 1 or loopback):
+                           MOE_TRANSPORT_NCCL: nccl_comm required (above).
+                           MOE_TRANSPORT_PEER: device-initiated exchange through peer memory
+                           (see "Peer-memory expert parallelism" below);
+                           nccl_comm unused (may be NULL), world_size 1..8 */
+  int32_t reserved0;    /* must be 0 */
+  int64_t window_rows;  /* MOE_TRANSPORT_PEER: rows of each peer-visible expert buffer (bounds
+                           sum_local roundup(C_e, 128) for every later moe_set_capacities);
+                           0 = the bound for Eq. 4 at alpha = 8 (the policy's maximum) */
 } moe_config_t;
+
+typedef enum { MOE_TRANSPORT_NCCL = 0, MOE_TRANSPORT_PEER = 1 } moe_transport_t;
 
 /* Create / destroy a layer handle.  moe_init validates cfg (MOE_ERR_CONFIG) and sets the
    capacities to Eq. 4 with alpha = 1 over T_g = max_tokens * world_size. */
@@ -265,6 +276,30 @@ MOE_API moe_status_t moe_ep_plan(int32_t R, int32_t rank, int32_t n, const int32
    all-reduce semantics.  Every rank must issue the same sequence of layer calls. */
 MOE_API moe_status_t moe_vcomm_create(int32_t R, void** comm_out);
 MOE_API moe_status_t moe_vcomm_destroy(void* comm);
+
+/* ----------------------------------------------------------------------------------- *
+ * Peer-memory expert parallelism (the exchange of S8(e) without the host).
+ * With cfg.transport = MOE_TRANSPORT_PEER, moe_init allocates (cudaMalloc, library-owned)
+ * this rank's peer window: the X / O / dO / dX rows and token_of_slot of its local experts,
+ * a count table, fp32 reduction slots and exchange flags.  Before the first forward every
+ * rank attaches the windows of all R ranks (same config and window_rows on every rank):
+ *   - in one process (R ranks as threads / streams, e.g. on one GPU): moe_peer_window on
+ *     each handle, then moe_peer_attach(h, windows[R]) with windows[rank] = its own;
+ *   - across processes (one per GPU): moe_peer_export gives a 64-byte CUDA IPC handle; the
+ *     caller all-gathers them (any host channel) and calls moe_peer_import(h, handles[R]),
+ *     which opens the peers' windows (peer access over NVLink is enabled lazily).
+ * The forward / backward then never synchronise the host: dispatch stores token rows into
+ * the owners' X buffers, combine reads O rows from them, the combine backward stores dO rows
+ * into them and the gate-input gradient reads dX rows from them; the counts, dW_g and the
+ * balance sums are exchanged through the windows; one-block barrier kernels order producer
+ * and consumer kernels across ranks.  Every rank must call moe_forward / moe_backward the
+ * same number of times (the barrier epochs advance in lockstep).  Routing, outputs and
+ * gradients equal the NCCL path and the single-GPU path on the concatenated batch
+ * (reading 12); dW_g is summed in rank order (identical on every rank). */
+MOE_API moe_status_t moe_peer_window(moe_handle_t h, void** window, size_t* bytes);
+MOE_API moe_status_t moe_peer_export(moe_handle_t h, void* ipc_handle /* host, 64 bytes */);
+MOE_API moe_status_t moe_peer_attach(moe_handle_t h, void* const* windows /* host [R] */);
+MOE_API moe_status_t moe_peer_import(moe_handle_t h, const void* handles /* host [R][64] */);
 
 /* Number of kernels the library launched since the handle was created (for bench
    accounting of "our kernels in the timed region"). */

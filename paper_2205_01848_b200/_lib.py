@@ -24,7 +24,11 @@ class MoEConfig(C.Structure):
     _fields_ = [("n_experts", C.c_int32), ("top_k", C.c_int32), ("d_model", C.c_int32),
                 ("d_ff", C.c_int32), ("d_out", C.c_int32), ("max_tokens", C.c_int32),
                 ("dtype", C.c_int32), ("renormalize", C.c_int32), ("world_size", C.c_int32),
-                ("rank", C.c_int32), ("nccl_comm", C.c_void_p), ("stream", C.c_void_p)]
+                ("rank", C.c_int32), ("nccl_comm", C.c_void_p), ("stream", C.c_void_p),
+                ("transport", C.c_int32), ("reserved0", C.c_int32), ("window_rows", C.c_int64)]
+
+
+TRANSPORTS = {"nccl": 0, "peer": 1}
 
 
 class FwdArgs(C.Structure):
@@ -106,6 +110,10 @@ EXPORTS = {
     "moe_policy_update": ([C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                            C.POINTER(C.c_int32)], C.c_int),
     "moe_policy_destroy": ([C.c_void_p], C.c_int),
+    "moe_peer_window": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)], C.c_int),
+    "moe_peer_export": ([C.c_void_p, C.c_void_p], C.c_int),
+    "moe_peer_attach": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+    "moe_peer_import": ([C.c_void_p, C.c_void_p], C.c_int),
 }
 
 _lib = None

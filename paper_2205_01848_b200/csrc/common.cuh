@@ -23,6 +23,34 @@ struct CapTable {
   int32_t pre[MOE_MAX_E];       // token side: global slot of this rank's first pair of e
 };
 
+// Peer-memory expert parallelism: per-owner base pointers of one expert
+// buffer, valid in this process (NVLink peer mappings, or the same GPU for virtual ranks).
+// nl == 0: single buffer (no peers); otherwise expert e lives on rank e / nl.
+#define MOE_MAX_R 8
+struct PeerBufs {
+  char* p[MOE_MAX_R];
+  int nl;
+};
+
+// Row `row` (in its owner's region numbering) of expert e's buffer with `cols` columns.
+// (owner selected with constant indices: a dynamically indexed kernel-parameter array would
+// be copied to local memory)
+template <typename T>
+__device__ __forceinline__ T* peer_row(T* local, const PeerBufs& pb, int e, size_t row,
+                                       int cols) {
+  T* b = local;
+  if (pb.nl) {
+    const int o = e / pb.nl;
+#pragma unroll
+    for (int j = 0; j < MOE_MAX_R; ++j)
+      if (o == j) b = reinterpret_cast<T*>(pb.p[j]);
+  }
+  return b + row * (size_t)cols;
+}
+
+// gather-table encoding of a peer row: owner in the top 5 bits (rows < 2^26)
+#define MOE_GROW_SHIFT 26
+
 template <typename T> struct Vec;  // 16-byte vector of T
 template <> struct Vec<float> { static constexpr int N = 4; };
 template <> struct Vec<__nv_bfloat16> { static constexpr int N = 8; };

@@ -43,7 +43,22 @@ struct GateDxParams {
   __nv_bfloat16* dx;           // [T x d]
   int accumulate;
   CapTable ct;
+  PeerBufs pdx;                // peer EP (N1): dX rows read from the owners; grow encodes owner
 };
+
+// dX row of a gather-table entry (peer EP: owner in the top bits, see MOE_GROW_SHIFT)
+template <bool PEER>
+__device__ __forceinline__ const __nv_bfloat16* gdx_row(const GateDxParams& p, int g) {
+  if (PEER) {
+    const int o = g >> MOE_GROW_SHIFT;
+    const __nv_bfloat16* b = p.dxbuf;
+#pragma unroll
+    for (int j = 0; j < MOE_MAX_R; ++j)  // constant indices (no local copy of the table)
+      if (o == j) b = reinterpret_cast<const __nv_bfloat16*>(p.pdx.p[j]);
+    return b + (size_t)(g & ((1 << MOE_GROW_SHIFT) - 1)) * p.d;
+  }
+  return p.dxbuf + (size_t)g * p.d;
+}
 
 struct GateDwParams {
   int T, n, d, chunk, splits;
@@ -320,7 +335,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 // ======================================================================================
 constexpr int GX_THREADS = 384;  // 4 control warps + 8 epilogue warps (gather-heavy epilogue)
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool PEER>
 __global__ void __launch_bounds__(GX_THREADS, 1)
     gate_dx_tc_kernel(const __grid_constant__ CUtensorMap tmHi,
                       const __grid_constant__ CUtensorMap tmLo,
@@ -426,7 +441,7 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
             if (rowid >= 0)
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                                smem_u32(stg(par, r) + (i + sub) * RS + seg * 16)),
-                           "l"(p.dxbuf + (size_t)rowid * p.d + col_base + seg * 8)
+                           "l"(gdx_row<PEER>(p, rowid) + col_base + seg * 8)
                            : "memory");
           }
         }
@@ -467,7 +482,7 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
 #pragma unroll
           for (int c = 0; c < HC / 8; ++c) {
             float xv[8];
-            unpack(ld_nc_v4(p.dxbuf + (size_t)rows_cur[r] * p.d + col_base + 8 * c), xv, __nv_bfloat16());
+            unpack(ld_nc_v4(gdx_row<PEER>(p, rows_cur[r]) + col_base + 8 * c), xv, __nv_bfloat16());
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[8 * c + j] += xv[j];
           }
@@ -711,7 +726,8 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
 
 cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb, int maxT,
                               int n_pad, RouteBufs b, int T, int k, int n, int d,
-                              const CapTable& ct, void* dx, int accumulate, cudaStream_t s) {
+                              const CapTable& ct, void* dx, int accumulate, cudaStream_t s,
+                              const PeerBufs& pdx) {
   if (T == 0) return cudaSuccess;
   if (!enc_init()) return cudaErrorNotSupported;
   CUtensorMap mhi, mlo, mw;
@@ -724,13 +740,14 @@ cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb
   p.T = T; p.n_pad = n_pad; p.k = k; p.d = d; p.grow = b.grow;
   p.dxbuf = (const __nv_bfloat16*)dxbuf; p.dx = (__nv_bfloat16*)dx; p.accumulate = accumulate;
   p.ct = ct;
+  p.pdx = pdx;
   const int bn = d % 128 == 0 ? 128 : 64;
   const int total = ((T + 127) / 128) * (d / bn);
   const int grid = total < g_sms ? total : g_sms;
   (void)n;
 #define GX(BN, ST)                                                                       \
   {                                                                                      \
-    auto kf = gate_dx_tc_kernel<BN, ST>;                                                 \
+    auto kf = pdx.nl ? gate_dx_tc_kernel<BN, ST, true> : gate_dx_tc_kernel<BN, ST, false>; \
     size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 8 * 2 * 2 * 32 * (BN + 16);          \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \

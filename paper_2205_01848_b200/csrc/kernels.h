@@ -44,18 +44,22 @@ cudaError_t launch_route_scan(const int32_t* hist, int ntiles, int n, const CapT
                               RouteBufs b, cudaStream_t s);
 cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T, int k,
                             int n, int d, int64_t token_base, const CapTable& ct,
-                            RouteBufs b, void* xbuf, const int32_t* pad_kept, cudaStream_t s);
+                            RouteBufs b, void* xbuf, const int32_t* pad_kept, cudaStream_t s,
+                            int pad_e0 = 0, const PeerBufs& px = PeerBufs{},
+                            const PeerBufs& ptos = PeerBufs{}, const int32_t* pre_dev = nullptr);
 cudaError_t launch_zero_pad(int dtype, void* buf, int cols, const int32_t* kept, int n,
                             const CapTable& ct, cudaStream_t s);
 cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, int k,
-                               int d_out, const CapTable& ct, void* y, cudaStream_t s);
+                               int d_out, const CapTable& ct, void* y, cudaStream_t s,
+                               const PeerBufs& po = PeerBufs{});
 cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, RouteBufs b,
                                int T, int k, int n, int d_out, int renorm,
                                const CapTable& ct, void* dobuf, void* dlb, int maxT, int n_pad,
-                               const int32_t* pad_kept, cudaStream_t s);
+                               const int32_t* pad_kept, cudaStream_t s, int pad_e0 = 0,
+                               const PeerBufs& po = PeerBufs{}, const PeerBufs& pdo = PeerBufs{});
 cudaError_t launch_gate_dx(int dtype, const void* wg, const void* dxbuf, RouteBufs b, int T,
                            int k, int n, int d, const CapTable& ct, void* dx, int accumulate,
-                           cudaStream_t s);
+                           cudaStream_t s, const PeerBufs& pdx = PeerBufs{});
 // f32_out != null: write the fp32 sum there instead (EP: all-reduced before rounding)
 cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int n, int d,
                            float* partial, int splits, void* dwg, int accumulate,

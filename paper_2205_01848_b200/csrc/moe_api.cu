@@ -17,13 +17,15 @@
 #include "gate_tc.h"
 #include "prof.h"
 #include "ep.h"
+#include "peer.h"
 #include <map>
 
 using namespace moe;
 
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
-      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, grow, ep_all, sendbuf, oret, dwg32, total;
+      xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, grow, ep_all, sendbuf, oret, dwg32,
+      pre_dev, total;
 };
 
 struct moe_ctx {
@@ -66,6 +68,12 @@ struct moe_ctx {
   int use_ep = 0;             // expert-parallel path (nccl_comm given; R may be 1 = loopback)
   EpState* ep = nullptr;
   EpPlan plan;
+  // peer-memory transport (N1)
+  int use_peer = 0, peer_attached = 0;
+  PeerLayout PL{};
+  char* pwin = nullptr;              // own window (cudaMalloc)
+  PeerBufs wins{};                   // all ranks' windows in this process
+  bool opened[MOE_MAX_R] = {};       // windows opened from IPC handles (closed at destroy)
   std::string err;
 };
 
@@ -109,12 +117,14 @@ void compute_layout(moe_ctx* h) {
   L.tile_hist = take(ntiles * n * 4);
   L.tile_off = take(ntiles * n * 4);
   L.meta = take(4096);
-  L.token_of_slot = take(std::max<size_t>((size_t)h->rows, T * k) * 4);
-  L.xbuf = take((size_t)h->rows * h->d * h->s);
+  // peer transport: X/O/dO/dX and token_of_slot live in the peer window instead
+  const size_t prow = h->use_peer ? 0 : (size_t)h->rows;
+  L.token_of_slot = take(h->use_peer ? 0 : std::max<size_t>((size_t)h->rows, T * k) * 4);
+  L.xbuf = take(prow * h->d * h->s);
   L.hbuf = take((size_t)h->rows * h->f * h->s);
-  L.obuf = take((size_t)h->rows * h->dout * h->s);
-  L.dobuf = take((size_t)h->rows * h->dout * h->s);
-  L.dxbuf = take((size_t)h->rows * h->d * h->s);
+  L.obuf = take(prow * h->dout * h->s);
+  L.dobuf = take(prow * h->dout * h->s);
+  L.dxbuf = take(prow * h->d * h->s);
   const size_t splits = std::max(gate_dw_splits(h->maxT, h->d), gate_dw_tc_splits(h->maxT, h->n, h->d));
   L.partial = take(splits * n * h->d * 4 + 4096);
   L.dlb = take(h->dtype == MOE_BF16 ? 2 * T * (size_t)h->n_pad * 2 : 0);
@@ -124,7 +134,8 @@ void compute_layout(moe_ctx* h) {
   L.bal = take(((T + 63) / 64 + 3) * n * 4 + 256);
   L.grow = take(T * k * 4);
   L.bpart = take(h->dtype == MOE_BF16 ? ((size_t)h->rows / 256 + h->n_local) * 8 * h->f * 4 : 0);
-  const bool ep = h->use_ep;
+  const bool ep = h->use_ep && !h->use_peer;  // NCCL transport buffers
+  L.pre_dev = take(n * 4);
   L.ep_all = take(ep ? (size_t)h->R * n * 4 : 0);
   L.sendbuf = take(ep ? T * k * (size_t)std::max(h->d, h->dout) * h->s : 0);
   L.oret = take(ep ? T * k * (size_t)h->dout * h->s : 0);
@@ -153,7 +164,7 @@ void bind_buffers(moe_ctx* h) {
   r.hit_count = meta + 780;
   r.flags = meta + 781;
   r.ticket = (uint32_t*)(meta + 782);
-  r.token_of_slot = (int32_t*)(b + L.token_of_slot);
+  r.token_of_slot = h->use_peer ? (int32_t*)(h->pwin + h->PL.tos) : (int32_t*)(b + L.token_of_slot);
   r.grow = (int32_t*)(b + L.grow);
 }
 
@@ -172,7 +183,41 @@ void relayout(moe_ctx* h) {
   h->rows = base;
   h->cts = h->ct;  // single GPU: token side indexes the same regions, pre = 0
   for (int e = 0; e < MOE_MAX_E; ++e) h->cts.pre[e] = 0;
+  if (h->use_peer) {  // token side: every global expert's region base inside its owner's window
+    for (int o = 0; o < h->R; ++o) {
+      int64_t b = 0;
+      for (int j = 0; j < h->n_local; ++j) {
+        const int e = o * h->n_local + j;
+        h->cts.base[e] = (int32_t)b;
+        b += ((int64_t)h->cap[e] + MOE_ROW_ALIGN - 1) / MOE_ROW_ALIGN * MOE_ROW_ALIGN;
+      }
+    }
+  }
   compute_layout(h);
+}
+
+// The expert-major buffers: in the peer window (N1) or in the workspace.
+void* buf_x(moe_ctx* h) { return h->use_peer ? (void*)(h->pwin + h->PL.x) : (void*)(h->ws + h->L.xbuf); }
+void* buf_o(moe_ctx* h) { return h->use_peer ? (void*)(h->pwin + h->PL.o) : (void*)(h->ws + h->L.obuf); }
+void* buf_do(moe_ctx* h) { return h->use_peer ? (void*)(h->pwin + h->PL.dob) : (void*)(h->ws + h->L.dobuf); }
+void* buf_dx(moe_ctx* h) { return h->use_peer ? (void*)(h->pwin + h->PL.dxb) : (void*)(h->ws + h->L.dxbuf); }
+// per-owner pointers of one window buffer
+PeerBufs peer_bufs(const moe_ctx* h, size_t off) {
+  PeerBufs p{};
+  for (int j = 0; j < h->R; ++j) p.p[j] = h->wins.p[j] + off;
+  p.nl = h->n_local;
+  return p;
+}
+// Sum over the local experts of roundup(C_e, 128) for every owner (the rows a window needs).
+int64_t max_owner_rows(const moe_ctx* h, const std::vector<int32_t>& cap) {
+  int64_t m = 0;
+  for (int o = 0; o < h->R; ++o) {
+    int64_t b = 0;
+    for (int j = 0; j < h->n_local; ++j)
+      b += ((int64_t)cap[o * h->n_local + j] + MOE_ROW_ALIGN - 1) / MOE_ROW_ALIGN * MOE_ROW_ALIGN;
+    m = std::max(m, b);
+  }
+  return m;
 }
 
 int64_t tokens_global(const moe_ctx* h) { return (int64_t)h->maxT * h->R; }
@@ -210,7 +255,10 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
   if (c.max_tokens < 0) return MOE_ERR_INVALID_ARG;
   if (c.world_size < 1 || c.rank < 0 || c.rank >= c.world_size) return MOE_ERR_INVALID_ARG;
   if (c.n_experts % c.world_size) return MOE_ERR_CONFIG;
-  if (c.world_size > 1 && !c.nccl_comm) return MOE_ERR_INVALID_ARG;
+  if (c.transport != MOE_TRANSPORT_NCCL && c.transport != MOE_TRANSPORT_PEER) return MOE_ERR_CONFIG;
+  if (c.reserved0 != 0 || c.window_rows < 0) return MOE_ERR_INVALID_ARG;
+  if (c.transport == MOE_TRANSPORT_NCCL && c.world_size > 1 && !c.nccl_comm) return MOE_ERR_INVALID_ARG;
+  if (c.transport == MOE_TRANSPORT_PEER && c.world_size > MOE_MAX_R) return MOE_ERR_CONFIG;
   if (c.n_experts / c.world_size > MOE_MAX_E) return MOE_ERR_CONFIG;
   moe_ctx* h = new moe_ctx();
   h->cfg = c;
@@ -229,14 +277,41 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
     delete h;
     return MOE_ERR_CUDA;
   }
-  h->use_ep = c.nccl_comm ? 1 : 0;
+  h->use_peer = c.transport == MOE_TRANSPORT_PEER ? 1 : 0;
+  h->use_ep = (c.nccl_comm || h->use_peer) ? 1 : 0;
+  if (h->use_peer) {  // the peer window, sized for the largest capacities allowed later
+    int64_t wrows = c.window_rows;
+    if (wrows == 0) {
+      std::vector<int32_t> c8(h->n);
+      std::vector<double> a8(h->n, 8.0);
+      moe_capacity_from_factors(h->n, tokens_global(h), h->k, a8.data(), c8.data());
+      for (auto& v : c8) v = (int32_t)std::min<int64_t>(v, std::max<int64_t>(1, tokens_global(h)));
+      wrows = max_owner_rows(h, c8);
+    }
+    wrows = (wrows + MOE_ROW_ALIGN - 1) / MOE_ROW_ALIGN * MOE_ROW_ALIGN;
+    peer_layout(h->PL, wrows, h->n, h->d, h->dout, h->s);
+    if (cudaMalloc((void**)&h->pwin, h->PL.total) != cudaSuccess ||
+        cudaMemset(h->pwin, 0, h->PL.total) != cudaSuccess) {
+      if (h->pwin) cudaFree(h->pwin);
+      cudaEventDestroy(h->ev_fork);
+      cudaEventDestroy(h->ev_join);
+      cudaStreamDestroy(h->side);
+      delete h;
+      return MOE_ERR_CUDA;
+    }
+  }
   // default capacities: Eq. 4 with alpha = 1 over the global token count
   h->cap.assign(h->n, 1);
   std::vector<double> a(h->n, 1.0);
   moe_capacity_from_factors(h->n, tokens_global(h), h->k, a.data(), h->cap.data());
   for (auto& v : h->cap) v = (int32_t)std::min<int64_t>(v, std::max<int64_t>(1, tokens_global(h)));
+  if (h->use_peer && max_owner_rows(h, h->cap) > h->PL.rows) {
+    cudaFree(h->pwin);
+    delete h;
+    return MOE_ERR_CONFIG;
+  }
   relayout(h);
-  if (c.nccl_comm) {
+  if (c.nccl_comm && !h->use_peer) {
     h->use_ep = 1;
     moe_status_t st = ep_create(&h->ep, c.nccl_comm, h->R, h->rank, &h->err);
     if (st != MOE_OK) {
@@ -252,6 +327,12 @@ moe_status_t moe_destroy(moe_handle_t h) {
   if (!h) return MOE_ERR_INVALID_ARG;
   if (h->side) cudaStreamSynchronize(h->side);
   if (h->ep) ep_destroy(h->ep);
+  for (int j = 0; j < MOE_MAX_R; ++j)
+    if (h->opened[j]) cudaIpcCloseMemHandle(h->wins.p[j]);
+  if (h->pwin) {
+    cudaDeviceSynchronize();
+    cudaFree(h->pwin);
+  }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->side) cudaStreamDestroy(h->side);
@@ -276,7 +357,12 @@ moe_status_t moe_set_capacities(moe_handle_t h, const int32_t* cap) {
   for (int e = 0; e < h->n; ++e)
     if (cap[e] < 1) return fail(h, MOE_ERR_INVALID_ARG, "capacity < 1");
   const int64_t tg = std::max<int64_t>(1, tokens_global(h));
-  for (int e = 0; e < h->n; ++e) h->cap[e] = (int32_t)std::min<int64_t>(cap[e], tg);
+  std::vector<int32_t> nc(h->n);
+  for (int e = 0; e < h->n; ++e) nc[e] = (int32_t)std::min<int64_t>(cap[e], tg);
+  if (h->use_peer && max_owner_rows(h, nc) > h->PL.rows)
+    return fail(h, MOE_ERR_WORKSPACE_TOO_SMALL, "peer window too small for these capacities "
+                                                "(raise cfg.window_rows)");
+  h->cap = nc;
   relayout(h);
   h->have_fwd = 0;  // saved activations no longer match the layout
   if (h->ws && h->ws_bytes < h->L.total) {
@@ -328,13 +414,15 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     return fail(h, MOE_ERR_INVALID_ARG, "null tensor");
   if (!h->mq.empty() && h->mq_count == (int)h->mq.size())
     return fail(h, MOE_ERR_STATE, "metrics queue full: pop before launching more iterations");
+  if (h->use_peer && !h->peer_attached)
+    return fail(h, MOE_ERR_STATE, "peer transport: call moe_peer_attach / moe_peer_import first");
   const int T = a->T, n = h->n, k = h->k, d = h->d, f = h->f, dout = h->dout, dt = h->dtype;
   cudaStream_t s0 = h->stream;
   RouteBufs& rb = h->rb;
   uint8_t* ws = h->ws;
-  void* X = ws + h->L.xbuf;
+  void* X = buf_x(h);
   void* H = ws + h->L.hbuf;
-  void* O = ws + h->L.obuf;
+  void* O = buf_o(h);
   const int ntiles = (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE;
   const bool cached = h->cached != nullptr;
   CUDA_TRY(h, cudaMemsetAsync(rb.hit_count, 0, 4, s0));
@@ -361,6 +449,17 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   KL(h, 1, "route_scan", sd, launch_route_scan(rb.tile_hist, ntiles, n, h->ct, rb, sd));
   if (!h->use_ep) {
     KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->cts, rb, X, rb.kept, sd));
+  } else if (h->use_peer) {
+    // N1: counts exchange + global plan on the device, then the dispatch stores every kept
+    // row straight into its owner's X buffer; the barrier publishes "X rows landed".
+    int32_t* pre_dev = (int32_t*)(ws + h->L.pre_dev);
+    KL(h, 1, "peer_plan", sd, launch_peer_plan(h->wins, h->R, h->rank, n, h->n_local, rb.counts,
+                                               h->ct, rb, pre_dev, sd));
+    KL(h, 1, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, (int64_t)h->rank * T,
+                                             h->cts, rb, X, rb.kept, sd, h->e_lo,
+                                             peer_bufs(h, h->PL.x), peer_bufs(h, h->PL.tos),
+                                             pre_dev));
+    KL(h, 1, "peer_barrier", sd, launch_peer_barrier(h->wins, h->R, h->rank, PH_X, sd));
   } else {
     // C1 + the single host sync of EP v1: all-gather the per-rank pre-drop counts, then every
     // rank derives the same global slot offsets, kept counts and message sizes (reading 12).
@@ -409,7 +508,11 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
                                      kept_local, nl, h->ct, h->max_cap_local, EPI_BIAS, sd));
   }
   void* O_tok = O;  // expert outputs as the token side indexes them
-  if (h->use_ep) {
+  PeerBufs po{};    // peer EP: combine reads O rows from the owners
+  if (h->use_peer) {
+    KL(h, 1, "peer_barrier", sd, launch_peer_barrier(h->wins, h->R, h->rank, PH_O, sd));
+    po = peer_bufs(h, h->PL.o);
+  } else if (h->use_ep) {
     std::string err;
     O_tok = ws + h->L.oret;
     moe_status_t st = ep_from_experts(h->ep, h->plan, O, O_tok, h->ct, dout, (int)h->s, sd, &err);  // C3
@@ -426,8 +529,15 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   if (h->balance_lambda != 0.f) {  // Eq. 3 balance term (N3)
     float* bal = (float*)(ws + h->L.bal);
     float* gsum = bal + (size_t)((h->maxT + 63) / 64) * n;
-    KL(h, T > 0 ? 2 : 1, "balance", s0, launch_balance_partial(rb.logits, T, n, bal, gsum, s0));
-    if (h->use_ep) {
+    if (h->use_peer) {  // column sums through the windows, summed in rank order
+      KL(h, T > 0 ? 2 : 1, "balance", s0, launch_balance_partial(rb.logits, T, n, bal,
+                                                                 (float*)(h->pwin + h->PL.bal), s0));
+      KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_BAL, s0));
+      KL(h, 1, "peer_sum", s0, launch_peer_sum(h->wins, h->PL.bal, h->R, (size_t)n, 2, gsum, 0, s0));
+    } else {
+      KL(h, T > 0 ? 2 : 1, "balance", s0, launch_balance_partial(rb.logits, T, n, bal, gsum, s0));
+    }
+    if (h->use_ep && !h->use_peer) {
       std::string err;
       moe_status_t st = ep_allreduce_f32(h->ep, gsum, (size_t)n, s0, &err);
       if (st != MOE_OK) return fail(h, st, err);
@@ -437,7 +547,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   }
   rb.spec = h->spec;
   rb.spec_valid = h->spec_valid;
-  KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O_tok, rb, T, k, dout, h->cts, a->y, s0));
+  KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O_tok, rb, T, k, dout, h->cts, a->y, s0, po));
   rb.spec = nullptr;
   rb.spec_valid = nullptr;
   if (!h->mq.empty()) {  // push this iteration's metric futures (App. B)
@@ -472,11 +582,13 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   cudaStream_t s0 = h->stream;
   RouteBufs& rb = h->rb;
   uint8_t* ws = h->ws;
-  void* X = ws + h->L.xbuf;
+  void* X = buf_x(h);
   void* H = ws + h->L.hbuf;   // holds H; overwritten by dA below
-  void* O = ws + h->L.obuf;
-  void* dO = ws + h->L.dobuf;
-  void* dXb = ws + h->L.dxbuf;
+  void* O = buf_o(h);
+  void* dO = buf_do(h);
+  void* dXb = buf_dx(h);
+  const bool peer = h->use_peer != 0;
+  const bool nccl_ep = h->use_ep && !peer;
   const moe_fwd_args_t& fa = h->fa;
   const int nl = h->n_local;
   const int acc = a->accumulate ? 1 : 0;
@@ -484,8 +596,8 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
 
   // K6 combine backward -> dO rows (local or, in EP, returned to the expert owners), dw, dl
   void* dlb = h->use_tc ? (void*)(ws + h->L.dlb) : nullptr;
-  void* O_tok = h->use_ep ? (void*)(ws + h->L.oret) : O;
-  void* dO_tok = h->use_ep ? (void*)(ws + h->L.sendbuf) : dO;
+  void* O_tok = nccl_ep ? (void*)(ws + h->L.oret) : O;
+  void* dO_tok = nccl_ep ? (void*)(ws + h->L.sendbuf) : dO;
   std::string err;
   rb.dspec = h->dspec;
   rb.dw_ext = h->dw_ext;
@@ -494,11 +606,16 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                  : nullptr;
   KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O_tok, rb, T, k, n, dout, h->renorm, h->cts,
                                                      dO_tok, dlb, h->maxT, h->n_pad,
-                                                     h->use_ep ? nullptr : rb.kept, s0));
+                                                     nccl_ep ? nullptr : rb.kept, s0,
+                                                     peer ? h->e_lo : 0,
+                                                     peer ? peer_bufs(h, h->PL.o) : PeerBufs{},
+                                                     peer ? peer_bufs(h, h->PL.dob) : PeerBufs{}));
   rb.dspec = nullptr;
   rb.dw_ext = nullptr;
   rb.bal_g = nullptr;
-  if (h->use_ep) {  // C4: dO rows to the expert owners
+  if (peer) {  // N1: dO rows were stored into the owners by the combine backward
+    KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DO, s0));
+  } else if (h->use_ep) {  // C4: dO rows to the expert owners
     moe_status_t st = ep_to_experts(h->ep, h->plan, dO_tok, dO, h->ct, dout, (int)h->s, s0, &err);
     if (st != MOE_OK) return fail(h, st, err);
     KL(h, 1, "zero_pad", s0, launch_zero_pad(dt, dO, dout, kept_local, nl, h->ct, s0));
@@ -533,7 +650,11 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   }
   // B4: dx = gather(dX) + dl W_g ;  B5: dW_g = dl^T x
   void* dX_tok = dXb;
-  if (h->use_ep) {  // C5: dX rows back to the token owners (send layout, reuses the send buffer)
+  PeerBufs pdx{};
+  if (peer) {  // N1: the gate-input gradient reads dX rows from the owners
+    KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DX, s0));
+    pdx = peer_bufs(h, h->PL.dxb);
+  } else if (h->use_ep) {  // C5: dX rows back to the token owners (send layout, reuses the send buffer)
     dX_tok = ws + h->L.sendbuf;
     moe_status_t st = ep_from_experts(h->ep, h->plan, dXb, dX_tok, h->ct, d, (int)h->s, s0, &err);
     if (st != MOE_OK) return fail(h, st, err);
@@ -541,12 +662,14 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   if (a->dx) {
     if (h->use_tc)
       KL(h, T > 0, "gate_dx", s0, launch_gate_dx_tc(fa.w_gate, dX_tok, dlb, h->maxT, h->n_pad, rb, T, k, n, d,
-                                                    h->cts, a->dx, acc, s0));
+                                                    h->cts, a->dx, acc, s0, pdx));
     else
-      KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dX_tok, rb, T, k, n, d, h->cts, a->dx, acc, s0));
+      KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dX_tok, rb, T, k, n, d, h->cts, a->dx, acc, s0,
+                                                 pdx));
   }
   if (a->dw_gate) {
-    float* f32 = h->use_ep ? (float*)(ws + h->L.dwg32) : nullptr;  // EP: all-reduce in fp32
+    float* f32 = peer ? (float*)(h->pwin + h->PL.dwg)          // N1: pulled by every rank
+                 : nccl_ep ? (float*)(ws + h->L.dwg32) : nullptr;  // EP: all-reduce in fp32
     if (h->use_tc) {
       KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw_tc(dlb, h->maxT, h->n_pad, fa.x, T, n, d,
                                                             (float*)(ws + h->L.partial), a->dw_gate, acc, s0, f32));
@@ -555,7 +678,12 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
       KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw(dt, rb.dl, fa.x, T, n, d, (float*)(ws + h->L.partial),
                                           splits, a->dw_gate, acc, s0, f32));
     }
-    if (h->use_ep) {  // C6
+    if (T == 0 && f32) CUDA_TRY(h, cudaMemsetAsync(f32, 0, (size_t)n * d * 4, s0));  // no tokens
+    if (peer) {  // N1: sum of every rank's fp32 partial in rank order
+      KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DW, s0));
+      KL(h, 1, "gate_dw", s0, launch_peer_sum(h->wins, h->PL.dwg, h->R, (size_t)n * d, dt,
+                                              a->dw_gate, acc, s0));
+    } else if (h->use_ep) {  // C6
       moe_status_t st = ep_allreduce_f32(h->ep, f32, (size_t)n * d, s0, &err);
       if (st != MOE_OK) return fail(h, st, err);
       KL(h, 1, "gate_dw", s0, launch_f32_to(dt, f32, (size_t)n * d, a->dw_gate, acc, s0));
@@ -563,6 +691,59 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   }
   h->have_fwd = 0;  // H has been consumed
   return MOE_OK;
+}
+
+moe_status_t moe_peer_window(moe_handle_t h, void** window, size_t* bytes) {
+  if (!h || !window) return MOE_ERR_INVALID_ARG;
+  if (!h->use_peer) return fail(h, MOE_ERR_STATE, "not a peer-transport handle");
+  *window = h->pwin;
+  if (bytes) *bytes = h->PL.total;
+  return MOE_OK;
+}
+
+moe_status_t moe_peer_export(moe_handle_t h, void* ipc_handle) {
+  if (!h || !ipc_handle) return MOE_ERR_INVALID_ARG;
+  if (!h->use_peer) return fail(h, MOE_ERR_STATE, "not a peer-transport handle");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t hd;
+  CUDA_TRY(h, cudaIpcGetMemHandle(&hd, h->pwin));
+  std::memcpy(ipc_handle, &hd, 64);
+  return MOE_OK;
+}
+
+moe_status_t moe_peer_attach(moe_handle_t h, void* const* windows) {
+  if (!h || !windows) return MOE_ERR_INVALID_ARG;
+  if (!h->use_peer) return fail(h, MOE_ERR_STATE, "not a peer-transport handle");
+  if (windows[h->rank] != h->pwin)
+    return fail(h, MOE_ERR_INVALID_ARG, "windows[rank] must be this handle's own window");
+  for (int j = 0; j < h->R; ++j)
+    if (!windows[j]) return fail(h, MOE_ERR_INVALID_ARG, "null peer window");
+  for (int j = 0; j < MOE_MAX_R; ++j) h->wins.p[j] = j < h->R ? (char*)windows[j] : nullptr;
+  h->wins.nl = h->n_local;
+  h->peer_attached = 1;
+  return MOE_OK;
+}
+
+moe_status_t moe_peer_import(moe_handle_t h, const void* handles) {
+  if (!h || !handles) return MOE_ERR_INVALID_ARG;
+  if (!h->use_peer) return fail(h, MOE_ERR_STATE, "not a peer-transport handle");
+  void* w[MOE_MAX_R] = {};
+  for (int j = 0; j < h->R; ++j) {
+    if (j == h->rank) {
+      w[j] = h->pwin;
+      continue;
+    }
+    if (h->opened[j]) {
+      w[j] = h->wins.p[j];
+      continue;
+    }
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, (const char*)handles + 64 * j, 64);
+    CUDA_TRY(h, cudaIpcOpenMemHandle(&w[j], hd, cudaIpcMemLazyEnablePeerAccess));
+    h->opened[j] = true;
+    h->wins.p[j] = (char*)w[j];
+  }
+  return moe_peer_attach(h, w);
 }
 
 moe_status_t moe_get_routing(moe_handle_t h, moe_routing_t* out) {
@@ -580,9 +761,9 @@ moe_status_t moe_get_routing(moe_handle_t h, moe_routing_t* out) {
   out->kept = r.kept;
   out->dl = r.dl;
   out->dw = r.dw;
-  out->x_buf = h->ws + h->L.xbuf;
+  out->x_buf = buf_x(h);
   out->h_buf = h->ws + h->L.hbuf;
-  out->o_buf = h->ws + h->L.obuf;
+  out->o_buf = buf_o(h);
   out->rows = h->rows;
   for (int j = 0; j <= h->n_local; ++j) out->base_host[j] = h->ct.base[j];
   return MOE_OK;

@@ -7,6 +7,8 @@
 // Readings: top-k on fp32 logits, IEEE '>', ties -> lower expert
 // index; token-major global drop order; relu'(0) = 0; fp32 accumulators everywhere; no
 // floating-point atomics (bitwise run-to-run determinism).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -286,18 +288,19 @@ cudaError_t launch_route_scan(const int32_t* hist, int ntiles, int n, const CapT
 // Zero rows [kept_e, min(roundup(kept_e, PAD), region end)) of expert regions e = first,
 // first + stride, ... with all threads of the calling block (the token-contraction GEMMs read
 // whole 64-row K-blocks).  Fused into the dispatch / combine-backward kernels on one GPU.
+// Local region j starts at row ct.base[e0 + j]; regions are 128-row aligned and kept <= cap,
+// so roundup(kept, 64) never leaves the region.
 template <typename T>
 __device__ __forceinline__ void zero_pads_block(T* __restrict__ buf, int cols,
                                                 const int32_t* __restrict__ kept,
-                                                const CapTable& ct, int n, int first,
+                                                const CapTable& ct, int nreg, int e0, int first,
                                                 int stride) {
   constexpr int VE = Vec<T>::N;
   const int nvec = cols / VE;
-  for (int e = first; e < n; e += stride) {
-    const int kp = kept[e];
-    const int r0 = ct.base[e] + kp;
-    const int r1 = min(ct.base[e] + ((kp + MOE_PAD_ROWS - 1) / MOE_PAD_ROWS) * MOE_PAD_ROWS,
-                       ct.base[e + 1]);
+  for (int j = first; j < nreg; j += stride) {
+    const int kp = kept[j];
+    const int r0 = ct.base[e0 + j] + kp;
+    const int r1 = ct.base[e0 + j] + ((kp + MOE_PAD_ROWS - 1) / MOE_PAD_ROWS) * MOE_PAD_ROWS;
     const size_t total = (size_t)max(r1 - r0, 0) * nvec;
     for (size_t i = threadIdx.x; i < total; i += blockDim.x)
       st_v4(buf + (size_t)r0 * cols + i * VE, make_uint4(0, 0, 0, 0));
@@ -309,10 +312,15 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
     const int32_t* __restrict__ idx, const T* __restrict__ x, int Tn, int k, int n, int d,
     long long token_base, CapTable ct, const int32_t* __restrict__ tile_off,
     int32_t* __restrict__ slot_of, int32_t* __restrict__ token_of_slot, T* __restrict__ xbuf,
-    const int32_t* __restrict__ pad_kept) {
+    const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs px, PeerBufs ptos,
+    const int32_t* __restrict__ pre_dev) {
+  // px.nl != 0 (peer EP, N1): rows go straight into the owners' X buffers over NVLink, the
+  // global slot offsets come from the device plan (pre_dev), token_of_slot is the owner's.
   __shared__ uint32_t masks[MOE_MAX_E][MOE_ROUTE_TILE / 32];
-  if (pad_kept) zero_pads_block(xbuf, d, pad_kept, ct, n, blockIdx.x, gridDim.x);
+  if (pad_kept)
+    zero_pads_block(xbuf, d, pad_kept, ct, px.nl ? px.nl : n, pad_e0, blockIdx.x, gridDim.x);
   __shared__ int32_t srow[MOE_ROUTE_TILE * MOE_MAX_K];  // destination row or -1
+  __shared__ int32_t sexp[MOE_ROUTE_TILE * MOE_MAX_K];  // its expert
   const int tile = blockIdx.x;
   const int t0 = tile * MOE_ROUTE_TILE;
   for (int i = threadIdx.x; i < n * (MOE_ROUTE_TILE / 32); i += blockDim.x)
@@ -322,26 +330,32 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
   const int t = t0 + lt;
   int ev[MOE_MAX_K];
   if (lt < MOE_ROUTE_TILE && t < Tn) {
-    for (int r = 0; r < k; ++r) {
+#pragma unroll
+    for (int r = 0; r < MOE_MAX_K; ++r) {
+      if (r >= k) break;
       ev[r] = idx[(size_t)t * k + r];
       atomicOr(&masks[ev[r]][lt >> 5], 1u << (lt & 31));
     }
   }
   __syncthreads();
   if (lt < MOE_ROUTE_TILE) {
-    for (int r = 0; r < k; ++r) {
+#pragma unroll
+    for (int r = 0; r < MOE_MAX_K; ++r) {
+      if (r >= k) break;
       int row = -1;
       if (t < Tn) {
         const int e = ev[r];
         int rank = __popc(masks[e][lt >> 5] & ((1u << (lt & 31)) - 1u));
         for (int q = 0; q < (lt >> 5); ++q) rank += __popc(masks[e][q]);
-        const int slot = ct.pre[e] + tile_off[(size_t)tile * n + e] + rank;
+        const int pre = pre_dev ? pre_dev[e] : ct.pre[e];
+        const int slot = pre + tile_off[(size_t)tile * n + e] + rank;
         const bool keep = slot < ct.cap[e];
         slot_of[(size_t)t * k + r] = keep ? slot : -1;
         if (keep) {
           row = ct.base[e] + slot;
-          token_of_slot[row] = (int32_t)((token_base + t) * k + r);
+          *peer_row(token_of_slot, ptos, e, (size_t)row, 1) = (int32_t)((token_base + t) * k + r);
         }
+        sexp[lt * k + r] = e;
       }
       srow[lt * k + r] = row;
     }
@@ -354,13 +368,18 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
   for (int lt2 = wid; lt2 < MOE_ROUTE_TILE; lt2 += 8) {
     const int tt = t0 + lt2;
     if (tt >= Tn) break;
-    int rows[MOE_MAX_K];
-    int nk = 0;
-    for (int r = 0; r < k; ++r) {
-      int rw = srow[lt2 * k + r];
-      if (rw >= 0) rows[nk++] = rw;
+    T* dsts[MOE_MAX_K];  // fully unrolled (registers, no local-memory array)
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < MOE_MAX_K; ++r) {
+      dsts[r] = nullptr;
+      if (r < k) {
+        const int rw = srow[lt2 * k + r];
+        if (rw >= 0) dsts[r] = peer_row(xbuf, px, sexp[lt2 * k + r], (size_t)rw, d);
+      }
+      any |= dsts[r] != nullptr;
     }
-    if (nk == 0) continue;
+    if (!any) continue;
     const T* src = x + (size_t)tt * d;
     for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
       uint4 buf[4];
@@ -373,25 +392,32 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
       for (int u = 0; u < 4; ++u) {
         int v = v0 + u * 32 + lane;
         if (v < nvec)
-          for (int q = 0; q < nk; ++q) st_v4(xbuf + (size_t)rows[q] * d + (size_t)v * VE, buf[u]);
+#pragma unroll
+          for (int q = 0; q < MOE_MAX_K; ++q)
+            if (dsts[q]) st_v4(dsts[q] + (size_t)v * VE, buf[u]);
       }
     }
   }
+  // (no fence here: the exchange barrier kernel that follows on this stream releases, at
+  // system scope, everything this kernel wrote -- see peer.h)
 }
 
 cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T, int k,
                             int n, int d, int64_t token_base, const CapTable& ct,
-                            RouteBufs b, void* xbuf, const int32_t* pad_kept, cudaStream_t s) {
-  if (T == 0) return cudaSuccess;
-  int ntiles = (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE;
+                            RouteBufs b, void* xbuf, const int32_t* pad_kept, cudaStream_t s,
+                            int pad_e0, const PeerBufs& px, const PeerBufs& ptos,
+                            const int32_t* pre_dev) {
+  if (T == 0 && !(pad_kept && px.nl)) return cudaSuccess;  // peer EP: own pads still zeroed
+  int ntiles = std::max(1, (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE);
   if (dtype == 1)
     dispatch_kernel<__nv_bfloat16><<<ntiles, 256, 0, s>>>(
         idx, (const __nv_bfloat16*)x, T, k, n, d, token_base, ct, b.tile_off, b.slot_of,
-        b.token_of_slot, (__nv_bfloat16*)xbuf, pad_kept);
+        b.token_of_slot, (__nv_bfloat16*)xbuf, pad_kept, pad_e0, px, ptos, pre_dev);
   else
     dispatch_kernel<float><<<ntiles, 256, 0, s>>>(idx, (const float*)x, T, k, n, d,
                                                   token_base, ct, b.tile_off, b.slot_of,
-                                                  b.token_of_slot, (float*)xbuf, pad_kept);
+                                                  b.token_of_slot, (float*)xbuf, pad_kept,
+                                                  pad_e0, px, ptos, pre_dev);
   return cudaGetLastError();
 }
 
@@ -431,22 +457,23 @@ template <typename T, int VPL, int KM>
 __global__ void __launch_bounds__(256) combine_fwd_kernel(
     const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
-    T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid) {
+    T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid, PeerBufs po) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
   constexpr int VE = Vec<T>::N;
   const int nvec = dout / VE;
-  int rows[KM];
+  const T* src[KM];  // O row of each kept pair (peer EP: read from the owner over NVLink)
   float wr[KM];
 #pragma unroll
   for (int r = 0; r < KM; ++r) {
-    rows[r] = -1;
+    src[r] = nullptr;
     wr[r] = 0.f;
     if (r < k) {
       const int sl = slot_of[(size_t)t * k + r];
       if (sl >= 0) {
-        rows[r] = ct.base[idx[(size_t)t * k + r]] + sl;
+        const int e = idx[(size_t)t * k + r];
+        src[r] = peer_row(obuf, po, e, (size_t)(ct.base[e] + sl), dout);
         wr[r] = w[(size_t)t * k + r];
       }
     }
@@ -459,7 +486,7 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int v = vb + j * 32 + lane;
-      if (rows[r] >= 0 && v < nvec) u[r][j] = ld_nc_v4(obuf + (size_t)rows[r] * dout + (size_t)v * VE);
+      if (src[r] && v < nvec) u[r][j] = ld_nc_v4(src[r] + (size_t)v * VE);
     }
   if (spec) {  // AggregateSpec (App. A): the chosen experts' rows, zeros if dropped
 #pragma unroll
@@ -470,7 +497,7 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
         const int v = vb + j * 32 + lane;
         if (v < nvec)
           st_v4(spec + ((size_t)t * k + r) * dout + (size_t)v * VE,
-                rows[r] >= 0 ? u[r][j] : make_uint4(0, 0, 0, 0));
+                src[r] ? u[r][j] : make_uint4(0, 0, 0, 0));
       }
     }
   }
@@ -483,7 +510,7 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
     for (int i = 0; i < VE; ++i) acc[i] = 0.f;
 #pragma unroll
     for (int r = 0; r < KM; ++r) {
-      if (rows[r] < 0) continue;
+      if (!src[r]) continue;
       float o[VE];
       unpack(u[r][j], o, T());
 #pragma unroll
@@ -495,7 +522,7 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
   if (valid && lane < k) {
 #pragma unroll
     for (int r = 0; r < KM; ++r)
-      if (r == lane) valid[(size_t)t * k + r] = rows[r] >= 0 ? 1 : 0;
+      if (r == lane) valid[(size_t)t * k + r] = src[r] ? 1 : 0;
   }
 }
 
@@ -504,19 +531,20 @@ template <typename T>
 __global__ void __launch_bounds__(256) combine_fwd_generic_kernel(
     const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
-    T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid) {
+    T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid, PeerBufs po) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
-  int rows[MOE_MAX_K];
+  const T* rows[MOE_MAX_K];
   float wr[MOE_MAX_K];
   int nk = 0;
-  int rsel[MOE_MAX_K];
+  const T* rsel[MOE_MAX_K];
   for (int r = 0; r < k; ++r) {
     int sl = slot_of[(size_t)t * k + r];
-    rsel[r] = -1;
+    rsel[r] = nullptr;
     if (sl >= 0) {
-      rows[nk] = ct.base[idx[(size_t)t * k + r]] + sl;
+      const int e = idx[(size_t)t * k + r];
+      rows[nk] = peer_row(obuf, po, e, (size_t)(ct.base[e] + sl), dout);
       rsel[r] = rows[nk];
       wr[nk] = w[(size_t)t * k + r];
       ++nk;
@@ -530,7 +558,7 @@ __global__ void __launch_bounds__(256) combine_fwd_generic_kernel(
 #pragma unroll
     for (int i = 0; i < VE; ++i) acc[i] = 0.f;
     for (int q = 0; q < nk; ++q) {
-      uint4 u = ld_nc_v4(obuf + (size_t)rows[q] * dout + (size_t)v * VE);
+      uint4 u = ld_nc_v4(rows[q] + (size_t)v * VE);
       float o[VE];
       unpack(u, o, T());
 #pragma unroll
@@ -540,39 +568,39 @@ __global__ void __launch_bounds__(256) combine_fwd_generic_kernel(
     if (spec)
       for (int r = 0; r < k; ++r)
         st_v4(spec + ((size_t)t * k + r) * dout + (size_t)v * VE,
-              rsel[r] >= 0 ? ld_nc_v4(obuf + (size_t)rsel[r] * dout + (size_t)v * VE)
-                           : make_uint4(0, 0, 0, 0));
+              rsel[r] ? ld_nc_v4(rsel[r] + (size_t)v * VE) : make_uint4(0, 0, 0, 0));
   }
   if (valid && lane < k) valid[(size_t)t * k + lane] = slot_of[(size_t)t * k + lane] >= 0 ? 1 : 0;
 }
 
 template <typename T>
 static cudaError_t combine_fwd_t(const void* obuf, RouteBufs b, int T_, int k, int d_out,
-                                 const CapTable& ct, void* y, cudaStream_t s) {
+                                 const CapTable& ct, void* y, cudaStream_t s, const PeerBufs& po) {
   T* spec = (T*)b.spec;
   uint8_t* valid = b.spec_valid;
   dim3 grid((T_ + 7) / 8);
   const int vpl = (d_out / Vec<T>::N + 31) / 32;
 #define CF(V, K)                                                                            \
   combine_fwd_kernel<T, V, K><<<grid, 256, 0, s>>>((const T*)obuf, b.w, b.idx, b.slot_of, ct, \
-                                                   T_, k, d_out, (T*)y, spec, valid)
+                                                   T_, k, d_out, (T*)y, spec, valid, po)
   if (k <= 2) {
     if (vpl <= 2) { if (k == 1) CF(2, 1); else CF(2, 2); }
     else if (vpl <= 4) { if (k == 1) CF(4, 1); else CF(4, 2); }
     else { if (k == 1) CF(8, 1); else CF(8, 2); }
   } else {
     combine_fwd_generic_kernel<T><<<grid, 256, 0, s>>>((const T*)obuf, b.w, b.idx, b.slot_of, ct,
-                                                       T_, k, d_out, (T*)y, spec, valid);
+                                                       T_, k, d_out, (T*)y, spec, valid, po);
   }
 #undef CF
   return cudaGetLastError();
 }
 
 cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, int k,
-                               int d_out, const CapTable& ct, void* y, cudaStream_t s) {
+                               int d_out, const CapTable& ct, void* y, cudaStream_t s,
+                               const PeerBufs& po) {
   if (T == 0) return cudaSuccess;
-  if (dtype == 1) return combine_fwd_t<__nv_bfloat16>(obuf, b, T, k, d_out, ct, y, s);
-  return combine_fwd_t<float>(obuf, b, T, k, d_out, ct, y, s);
+  if (dtype == 1) return combine_fwd_t<__nv_bfloat16>(obuf, b, T, k, d_out, ct, y, s, po);
+  return combine_fwd_t<float>(obuf, b, T, k, d_out, ct, y, s, po);
 }
 
 // =====================================================================================
@@ -589,8 +617,11 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
     T* __restrict__ dobuf, float* __restrict__ dw, float* __restrict__ dl,
     __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad, const T* __restrict__ dspec,
     const float* __restrict__ dw_ext, const float* __restrict__ bal_g,
-    int32_t* __restrict__ grow, const int32_t* __restrict__ pad_kept) {
-  if (pad_kept) zero_pads_block(dobuf, dout, pad_kept, ct, n, blockIdx.x, gridDim.x);
+    int32_t* __restrict__ grow, const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs po,
+    PeerBufs pdo) {
+  // peer EP (N1): O rows are read from, and dO rows written to, the experts' owners
+  if (pad_kept)
+    zero_pads_block(dobuf, dout, pad_kept, ct, pdo.nl ? pdo.nl : n, pad_e0, blockIdx.x, gridDim.x);
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
@@ -600,14 +631,21 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   const int nvec = dout / VE;
   int rows[KM], er[KM];
   float wr[KM], part[KM];
+  const T* osrc[KM];
+  T* odst[KM];
 #pragma unroll
   for (int r = 0; r < KM; ++r) {
     rows[r] = -1; er[r] = -1; wr[r] = 0.f; part[r] = 0.f;
+    osrc[r] = nullptr; odst[r] = nullptr;
     if (r < k) {
       const int sl = slot_of[(size_t)t * k + r];
       er[r] = idx[(size_t)t * k + r];
       rows[r] = sl >= 0 ? ct.base[er[r]] + sl : -1;
       wr[r] = w[(size_t)t * k + r];
+      if (rows[r] >= 0) {
+        osrc[r] = peer_row(obuf, po, er[r], (size_t)rows[r], dout);
+        odst[r] = peer_row(dobuf, pdo, er[r], (size_t)rows[r], dout);
+      }
     }
   }
   // this lane's experts: pairs e = 2*lane + 64*j (+1)
@@ -633,7 +671,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
 #pragma unroll
     for (int jv = 0; jv < VPL; ++jv) {
       const int v = vb + jv * 32 + lane;
-      if (rows[r] >= 0 && v < nvec) u[r][jv] = ld_nc_v4(obuf + (size_t)rows[r] * dout + (size_t)v * VE);
+      if (rows[r] >= 0 && v < nvec) u[r][jv] = ld_nc_v4(osrc[r] + (size_t)v * VE);
     }
 #pragma unroll
   for (int jv = 0; jv < VPL; ++jv) {
@@ -657,7 +695,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
         part[r] = fmaf(gv[i], o[i], part[r]);
         dov[i] = fmaf(wr[r], gv[i], ds[i]);
       }
-      st_v4(dobuf + (size_t)rows[r] * dout + (size_t)v * VE, pack(dov, T()));
+      st_v4(odst[r] + (size_t)v * VE, pack(dov, T()));
     }
   }
   }
@@ -674,7 +712,10 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   for (int r = 0; r < KM; ++r)
     if (r < k && lane == r) {
       dw[(size_t)t * k + r] = dwr[r];
-      if (grow) grow[(size_t)t * k + r] = rows[r];  // the gate-dx kernel's gather table
+      if (grow)  // the gate-dx kernel's gather table (peer EP: owner in the top bits)
+        grow[(size_t)t * k + r] = (pdo.nl && rows[r] >= 0)
+                                      ? rows[r] | ((er[r] / pdo.nl) << MOE_GROW_SHIFT)
+                                      : rows[r];
     }
   float m = -INFINITY, sp = 0.f, cb = 0.f;
   if (need_p) {
@@ -742,15 +783,17 @@ template <typename T>
 static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, int T_, int k,
                                  int n, int d_out, int renorm, const CapTable& ct, void* dobuf,
                                  void* dlb, int maxT, int n_pad, const int32_t* pad_kept,
-                                 cudaStream_t s) {
-  dim3 grid((T_ + 7) / 8);
+                                 cudaStream_t s, int pad_e0, const PeerBufs& po,
+                                 const PeerBufs& pdo) {
+  dim3 grid(std::max(1, (T_ + 7) / 8));
   const int vpl = (d_out / Vec<T>::N + 31) / 32;  // > 8: the kernel loops over 4 KB blocks
 #define CB(V, K)                                                                               \
   combine_bwd_kernel<T, V, K><<<grid, 256, 0, s>>>((const T*)dy, (const T*)obuf, b.w, b.idx,   \
                                                    b.slot_of, b.logits, ct, T_, k, n, d_out,   \
                                                    renorm, (T*)dobuf, b.dw, b.dl,              \
                                                    (__nv_bfloat16*)dlb, maxT, n_pad,           \
-                                                   (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow, pad_kept)
+                                                   (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow, pad_kept, \
+                                                   pad_e0, po, pdo)
   const int km = k == 1 ? 1 : (k == 2 ? 2 : 8);
   if (vpl <= 2) { if (km == 1) CB(2, 1); else if (km == 2) CB(2, 2); else CB(2, 8); }
   else if (vpl <= 4) { if (km == 1) CB(4, 1); else if (km == 2) CB(4, 2); else CB(4, 8); }
@@ -762,13 +805,14 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
 cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, RouteBufs b,
                                int T, int k, int n, int d_out, int renorm,
                                const CapTable& ct, void* dobuf, void* dlb, int maxT, int n_pad,
-                               const int32_t* pad_kept, cudaStream_t s) {
-  if (T == 0) return cudaSuccess;
+                               const int32_t* pad_kept, cudaStream_t s, int pad_e0,
+                               const PeerBufs& po, const PeerBufs& pdo) {
+  if (T == 0 && !(pad_kept && pdo.nl)) return cudaSuccess;  // peer EP: own pads still zeroed
   if (dtype == 1)
     return combine_bwd_t<__nv_bfloat16>(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf, dlb,
-                                        maxT, n_pad, pad_kept, s);
+                                        maxT, n_pad, pad_kept, s, pad_e0, po, pdo);
   return combine_bwd_t<float>(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf, dlb, maxT, n_pad,
-                              pad_kept, s);
+                              pad_kept, s, pad_e0, po, pdo);
 }
 
 // =====================================================================================
@@ -780,7 +824,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) gate_dx_kernel(
     const float* __restrict__ dl, const T* __restrict__ wg, const T* __restrict__ dxbuf,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of, CapTable ct, int Tn,
-    int k, int n, int d, T* __restrict__ dx, int accumulate) {
+    int k, int n, int d, T* __restrict__ dx, int accumulate, PeerBufs pdx) {
   __shared__ float dls[32][33];
   __shared__ float wgs[32][128];
   const int tid = threadIdx.x;
@@ -828,7 +872,8 @@ __global__ void __launch_bounds__(256) gate_dx_kernel(
     for (int r = 0; r < k; ++r) {
       int sl = slot_of[(size_t)t * k + r];
       if (sl < 0) continue;
-      const T* src = dxbuf + (size_t)(ct.base[idx[(size_t)t * k + r]] + sl) * d;
+      const int e = idx[(size_t)t * k + r];
+      const T* src = peer_row(dxbuf, pdx, e, (size_t)(ct.base[e] + sl), d);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         int col = c0 + c + 32 * j;
@@ -848,17 +893,17 @@ __global__ void __launch_bounds__(256) gate_dx_kernel(
 
 cudaError_t launch_gate_dx(int dtype, const void* wg, const void* dxbuf, RouteBufs b, int T,
                            int k, int n, int d, const CapTable& ct, void* dx, int accumulate,
-                           cudaStream_t s) {
+                           cudaStream_t s, const PeerBufs& pdx) {
   if (T == 0) return cudaSuccess;
   dim3 grid((d + 127) / 128, (T + 31) / 32);
   if (dtype == 1)
     gate_dx_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
         b.dl, (const __nv_bfloat16*)wg, (const __nv_bfloat16*)dxbuf, b.idx, b.slot_of, ct, T, k,
-        n, d, (__nv_bfloat16*)dx, accumulate);
+        n, d, (__nv_bfloat16*)dx, accumulate, pdx);
   else
     gate_dx_kernel<float><<<grid, 256, 0, s>>>(b.dl, (const float*)wg, (const float*)dxbuf,
                                                b.idx, b.slot_of, ct, T, k, n, d, (float*)dx,
-                                               accumulate);
+                                               accumulate, pdx);
   return cudaGetLastError();
 }
 

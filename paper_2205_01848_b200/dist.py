@@ -21,3 +21,20 @@ def nccl_comm_ptr(group=None, device=None) -> int:
     if not ptr:
         raise RuntimeError("ProcessGroupNCCL returned a null communicator")
     return int(ptr)
+
+
+def peer_connect(layer, group=None):
+    """Peer-memory transport across processes (one per GPU): all-gather the layers' 64-byte
+    CUDA IPC window handles over the process group and open the peers' windows (N1)."""
+    group = group or dist.group.WORLD
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, layer.peer_export(), group=group)
+    layer.peer_import(handles)
+    dist.barrier(group=group)
+
+
+def peer_connect_local(layers):
+    """Peer-memory transport for R ranks in ONE process (threads / streams, e.g. one GPU)."""
+    wins = [L.peer_window() for L in layers]
+    for L in layers:
+        L.peer_attach(wins)

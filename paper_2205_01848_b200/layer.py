@@ -34,7 +34,8 @@ class MoELayer:
 
     def __init__(self, n_experts: int, top_k: int, d_model: int, d_ff: int, d_out: int = 0,
                  max_tokens: int = 4096, dtype: str = "bf16", renormalize: int = 1,
-                 world_size: int = 1, rank: int = 0, nccl_comm: int = 0, device=None):
+                 world_size: int = 1, rank: int = 0, nccl_comm: int = 0, device=None,
+                 transport: str = "nccl", window_rows: int = 0):
         self.lib = L.load()
         dev = torch.device(device if device is not None else "cuda")
         if dev.type != "cuda":
@@ -53,7 +54,9 @@ class MoELayer:
         self.uses_tcgen05 = dtype == "bf16" and os.environ.get("MOE_FORCE_SIMT", "0") != "1"
         cfg = L.MoEConfig(n_experts, top_k, d_model, d_ff, d_out, max_tokens, L.DTYPES[dtype],
                           int(renormalize), world_size, rank, C.c_void_p(nccl_comm),
-                          C.c_void_p(self._stream()))
+                          C.c_void_p(self._stream()), L.TRANSPORTS[transport], 0,
+                          int(window_rows))
+        self.transport = transport
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             L.check(self.lib.moe_init(C.byref(cfg), C.byref(h)), None, "moe_init")
@@ -90,6 +93,29 @@ class MoELayer:
             self.close()
         except Exception:
             pass
+
+    # -- peer-memory expert parallelism (N1) -------------------------------------------
+    def peer_window(self) -> int:
+        """Device address of this rank's library-owned peer window."""
+        w = C.c_void_p()
+        L.check(self.lib.moe_peer_window(self.h, C.byref(w), None), self.h)
+        return w.value
+
+    def peer_export(self) -> bytes:
+        """64-byte CUDA IPC handle of the peer window (for other processes)."""
+        buf = C.create_string_buffer(64)
+        L.check(self.lib.moe_peer_export(self.h, buf), self.h)
+        return buf.raw
+
+    def peer_attach(self, windows):
+        """In-process ranks: every rank's window address (own one at index rank)."""
+        arr = (C.c_void_p * len(windows))(*windows)
+        L.check(self.lib.moe_peer_attach(self.h, arr), self.h, "moe_peer_attach")
+
+    def peer_import(self, handles):
+        """Cross-process ranks: all ranks' IPC handles (list of 64-byte strings)."""
+        buf = C.create_string_buffer(b"".join(handles), 64 * len(handles))
+        L.check(self.lib.moe_peer_import(self.h, buf), self.h, "moe_peer_import")
 
     # -- recompile-enabled optimisations ----------------------------------------------
     @property
@@ -203,10 +229,23 @@ class MoELayer:
         L.check(self.lib.moe_get_routing(self.h, C.byref(r)), self.h)
         base = self.ws.data_ptr()
 
+        ws_end = base + self.ws.numel()
+
         def view(ptr, count, dt):
-            off = ptr - base
             nbytes = count * torch.tensor([], dtype=dt).element_size()
-            return self.ws[off:off + nbytes].view(dt).clone()
+            if base <= ptr < ws_end:
+                off = ptr - base
+                return self.ws[off:off + nbytes].view(dt).clone()
+            # peer transport: the expert-major buffers live in the library's peer window
+            out = torch.empty(count, dtype=dt, device=self.device)
+            torch.cuda.synchronize(self.device)
+            if nbytes:
+                rt = C.CDLL("libcudart.so.12")
+                rc = rt.cudaMemcpy(C.c_void_p(out.data_ptr()), C.c_void_p(ptr),
+                                   C.c_size_t(nbytes), 4)  # cudaMemcpyDefault
+                if rc != 0:
+                    raise RuntimeError(f"cudaMemcpy failed ({rc})")
+            return out
 
         n, k = self.n, self.k
         out = dict(

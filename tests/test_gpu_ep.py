@@ -60,43 +60,57 @@ def test_ep_loopback_cached(comm):
     assert_values(gpu, st, gr, ol, "bf16")
 
 
-def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0):
-    """R expert-parallel ranks as threads on one GPU over the library's virtual communicator,
-    against the single-GPU layer on the concatenated batch."""
+def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0, transport="nccl",
+                 iters=1, caps_seq=None):
+    """R expert-parallel ranks as threads on one GPU -- over the library's virtual NCCL-style
+    communicator, or through the peer-memory transport (N1) with in-process windows -- against
+    the single-GPU layer on the concatenated batch.  iters > 1 repeats forward+backward
+    (caps_seq[i] = capacities of iteration i), returning the last iteration."""
     import ctypes as C
     import threading
     from paper_2205_01848_b200 import MoELayer, _lib
+    from paper_2205_01848_b200.dist import peer_connect_local
     from synth import make_dy, make_layer
     lib = _lib.load()
     comm = C.c_void_p()
-    assert lib.moe_vcomm_create(R, C.byref(comm)) == 0
+    if transport == "nccl":
+        assert lib.moe_vcomm_create(R, C.byref(comm)) == 0
     Tg = R * T
     cpu = make_layer(n, d, f, d, Tg, dtype)
     g = {kk: v.cuda() for kk, v in cpu.items()}
     dy = make_dy(Tg, d, dtype).cuda()
     caps = O.capacities_from_factors([1.0] * n, Tg, k)
+    if caps_seq is None:
+        caps_seq = [caps] * iters
+    caps = caps_seq[-1]
     cached = None
     if cached_frac is not None:
         from synth import perturb_cached
         fresh = O.topk_sorted(O.gate_logits(to_np(cpu["x"]), to_np(cpu["w_gate"])), k)
         cached = torch.from_numpy(perturb_cached(fresh, n, cached_frac)).cuda()
     layers = [MoELayer(n, k, d, f, 0, T, dtype, renorm, world_size=R, rank=r,
-                       nccl_comm=comm.value, device="cuda") for r in range(R)]
+                       nccl_comm=comm.value or 0, device="cuda", transport=transport)
+              for r in range(R)]
+    if transport == "peer":
+        peer_connect_local(layers)
     out = [None] * R
     errs = []
 
     def work(r):
         try:
             L = layers[r]
-            L.set_capacities(caps)
             L.set_balance_loss(lam)
             if cached is not None:
                 L.set_cached_assignment(cached[r * T:(r + 1) * T].contiguous())
             s = torch.cuda.Stream()
+            for it in range(iters):
+                L.set_capacities(caps_seq[it])
+                with torch.cuda.stream(s):
+                    xs = g["x"][r * T:(r + 1) * T]
+                    y = L.forward(xs, g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+                    gr = L.backward(dy[r * T:(r + 1) * T].contiguous())
             with torch.cuda.stream(s):
-                xs = g["x"][r * T:(r + 1) * T]
-                y = L.forward(xs, g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
-                gr = L.backward(dy[r * T:(r + 1) * T].contiguous())
+                s.synchronize()
                 rt = L.routing(T)
                 s.synchronize()
             out[r] = (y, gr, rt, L.stats())
@@ -119,7 +133,10 @@ def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0):
     gr_ref = ref.backward(dy)
     rt_ref = ref.routing(Tg)
     torch.cuda.synchronize()
-    lib.moe_vcomm_destroy(comm)
+    if transport == "nccl":
+        lib.moe_vcomm_destroy(comm)
+    for L in layers:
+        L.close()
     return out, (y_ref, gr_ref, rt_ref, st_ref)
 
 
@@ -160,3 +177,92 @@ def test_ep_virtual_ranks_cached_and_balance():
     assert sum(o[3]["hit_count"] for o in out) == st_ref["hit_count"]
     assert np.allclose(np.concatenate([o[2]["dl"].cpu().numpy() for o in out]),
                        rt_ref["dl"].cpu().numpy(), rtol=1e-5, atol=1e-7)
+
+
+# --------------------------------------------------------------------------------------
+# Peer-memory transport: device-initiated exchange, no host sync
+# --------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n,k,renorm", [(8, 2, 1), (16, 1, 0)])
+def test_peer_loopback_parity(dtype, n, k, renorm):
+    """R = 1 through the peer path (plan kernel, window buffers, barriers, rank-order sums)."""
+    from paper_2205_01848_b200 import MoELayer
+    T, d, f = 1000, 64, 128
+    caps = O.capacities_from_factors([1.0] * n, T, k)
+    pl = MoELayer(n, k, d, f, 0, T, dtype, renorm, world_size=1, rank=0, device="cuda",
+                  transport="peer")
+    pl.peer_attach([pl.peer_window()])
+    layer, gpu, st, gr, ol = run_pair(n, k, d, f, T, dtype, caps, renorm, layer=pl)
+    assert st.routing.drops > 0
+    assert_routing_exact(gpu, st, k, check_token_of_slot=True)
+    assert_values(gpu, st, gr, ol, dtype)
+    _, ref, _, _, _ = run_pair(n, k, d, f, T, dtype, caps, renorm)
+    for key in ("y", "dx", "dw1", "db1", "dw2", "db2", "dw_gate"):
+        assert np.array_equal(gpu[key], ref[key]), key
+
+
+def _check_virtual(out, ref, R, n, dtype):
+    y_ref, gr_ref, rt_ref, st_ref = ref
+    nl = n // R
+    assert np.array_equal(np.concatenate([o[2]["slot_of"].cpu().numpy() for o in out]),
+                          rt_ref["slot_of"].cpu().numpy())
+    for o in out:
+        assert o[3]["counts"] == st_ref["counts"] and o[3]["drops"] == st_ref["drops"]
+    assert torch.equal(torch.cat([o[0] for o in out]), y_ref)
+    assert torch.equal(torch.cat([o[1]["dx"] for o in out]), gr_ref["dx"])
+    for r, o in enumerate(out):
+        sl = slice(r * nl, (r + 1) * nl)
+        for key in ("dw1", "db1", "dw2", "db2"):
+            assert torch.equal(o[1][key][sl], gr_ref[key][sl]), (r, key)
+        a, b = to_np(o[1]["dw_gate"]), to_np(gr_ref["dw_gate"])
+        assert np.abs(a - b).max() <= (1e-5 if dtype == "f32" else 1e-2) * np.abs(b).max()
+
+
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("R", [2, 4])
+@pytest.mark.parametrize("dtype,k,renorm", [("bf16", 2, 1), ("bf16", 1, 0), ("f32", 2, 0)])
+def test_peer_virtual_ranks_match_single_gpu(R, dtype, k, renorm):
+    n, T, d, f = 16, 512, 64, 128
+    out, ref = _run_virtual(R, n, k, T, d, f, dtype, renorm, transport="peer")
+    _check_virtual(out, ref, R, n, dtype)
+    # dW_g is summed in rank order from the windows: identical on every rank
+    for o in out[1:]:
+        assert torch.equal(o[1]["dw_gate"], out[0][1]["dw_gate"])
+    # each owner's token_of_slot holds the global token ids of its experts' kept rows,
+    # exactly the single-GPU table (reading 12)
+    rt_ref = ref[2]
+    nl = n // R
+    kept = [min(c, cap) for c, cap in zip(ref[3]["counts"],
+                                          O.capacities_from_factors([1.0] * n, R * T, k))]
+    for r, o in enumerate(out):
+        rt = o[2]
+        for j in range(nl):
+            e = r * nl + j
+            a = rt["token_of_slot"][rt["base"][j]: rt["base"][j] + kept[e]].cpu().numpy()
+            b0 = rt_ref["base"][e]
+            b = rt_ref["token_of_slot"][b0: b0 + kept[e]].cpu().numpy()
+            assert np.array_equal(a, b), (r, e)
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_peer_virtual_ranks_cached_and_balance():
+    n, T, d, f, R = 16, 512, 64, 128, 2
+    out, (y_ref, gr_ref, rt_ref, st_ref) = _run_virtual(R, n, 2, T, d, f, "bf16", 1,
+                                                        cached_frac=0.03, lam=0.2,
+                                                        transport="peer")
+    assert torch.equal(torch.cat([o[0] for o in out]), y_ref)
+    assert sum(o[3]["hit_count"] for o in out) == st_ref["hit_count"]
+    assert np.allclose(np.concatenate([o[2]["dl"].cpu().numpy() for o in out]),
+                       rt_ref["dl"].cpu().numpy(), rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_peer_virtual_ranks_many_iterations_with_recompiles():
+    """Barrier epochs advance in lockstep over iterations; capacity changes (recompiles)
+    between iterations re-lay out every owner's regions."""
+    n, T, d, f, R, k = 16, 384, 64, 128, 4, 2
+    Tg = R * T
+    seq = [O.capacities_from_factors([a] * n, Tg, k) for a in (1.0, 0.5, 2.0, 1.25, 0.75)]
+    out, ref = _run_virtual(R, n, k, T, d, f, "bf16", 1, transport="peer", iters=len(seq),
+                            caps_seq=seq)
+    _check_virtual(out, ref, R, n, "bf16")

@@ -67,10 +67,17 @@ def test_config_validation_before_cuda(lib):
         _lib.MoEConfig(300, 1, 64, 64, 0, 16, 0, 1, 1, 0, None, None),   # n > 256
         _lib.MoEConfig(4, 1, 96, 64, 0, 16, 1, 1, 1, 0, None, None),     # bf16 d % 64
         _lib.MoEConfig(4, 1, 64, 64, 0, 16, 7, 1, 1, 0, None, None),     # bad dtype
+        _lib.MoEConfig(4, 1, 64, 64, 0, 16, 0, 1, 1, 0, None, None, 5),  # unknown transport
+        _lib.MoEConfig(18, 1, 64, 64, 0, 16, 0, 1, 9, 0, None, None, 1), # peer: R > 8
     ]
     for cfg in bad:
         assert lib.moe_init(C.byref(cfg), C.byref(h)) == 2
     assert lib.moe_init(None, C.byref(h)) == 1
+    # NCCL transport needs a communicator at R > 1; peer transport does not (checked later)
+    assert lib.moe_init(C.byref(_lib.MoEConfig(4, 1, 64, 64, 0, 16, 0, 1, 2, 0, None, None)),
+                        C.byref(h)) == 1
+    assert lib.moe_init(C.byref(_lib.MoEConfig(4, 1, 64, 64, 0, 16, 0, 1, 1, 0, None, None, 1, 3)),
+                        C.byref(h)) == 1      # reserved field must be 0
 
 
 def test_caching_trigger_matches_oracle_and_spec(lib):
