@@ -1,0 +1,27 @@
+"""Peer-memory transport across PROCESSES (N1): two ranks as two processes, windows opened
+from CUDA IPC handles (moe_peer_export / moe_peer_import) all-gathered over a gloo group.
+On the one-GPU test box both processes share cuda:0 (the kernels time-slice, so this checks
+the IPC plumbing and the cross-process flag protocol, not speed)."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_peer_transport_two_processes_ipc():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tests", "workers", "peer_ipc_worker.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0, out[-3000:]
+    assert out.count(": OK") == 2, out[-3000:]
