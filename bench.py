@@ -59,14 +59,42 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region: NVML polled every 2 ms
+    from a host thread (the timed region can be only tens of ms), nvidia-smi as a fallback."""
 
-    def __init__(self, index):
+    REASONS = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4),
+               ("hw_power_brake_slowdown", 0x80)]
+
+    def __init__(self, index, device=None):
         self.index = index
         self.rows = []
         self.proc = None
+        self.nvml = None
+        self.stop_flag = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            if device is not None:
+                try:
+                    import torch
+                    pr = torch.cuda.get_device_properties(device)
+                    bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                    h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+                except Exception:
+                    h = None
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nvml = (pynvml, h)
+        except Exception:
+            self.nvml = None
 
     def start(self):
+        if self.nvml is not None:
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -79,12 +107,38 @@ class ClockSampler:
             return
         self.t = threading.Thread(target=self._read, daemon=True)
         self.t.start()
+        time.sleep(0.3)  # nvidia-smi start-up
+
+    def _poll(self):
+        nv, h = self.nvml
+        while not self.stop_flag:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
 
     def stop(self):
+        if self.nvml is not None:
+            self.stop_flag = True
+            self.t.join(timeout=2)
+            nv, h = self.nvml
+            if not self.rows:
+                return None
+            sm = sorted(r[0] for r in self.rows)
+            try:
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            except Exception:
+                mx = None
+            reasons = sorted({nm for _, rs in self.rows for nm, bit in self.REASONS if rs & bit})
+            return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": reasons,
+                    "samples": len(sm), "source": "nvml, 2 ms"}
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -241,10 +295,9 @@ def run_ours(args):
     layer.profile(True)
     layer.profile_read(reset=True)
     l0 = layer.launch_count()
-    clk = ClockSampler(local)
+    clk = ClockSampler(local, dev)
     barrier()
     clk.start()
-    time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):

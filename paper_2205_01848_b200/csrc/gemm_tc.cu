@@ -354,15 +354,20 @@ static bool ensure_encode() {
 
 // 2-D bf16 tensor map over a row-major [outer x inner] matrix, 128-byte swizzle.
 static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
-                     uint32_t box_inner, uint32_t box_outer) {
+                     uint32_t box_inner, uint32_t box_outer,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {inner * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
-                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+// epilogue store map of the 2-CTA kernel: 32 x 32 boxes, 64-byte swizzle
+static bool make_store_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer) {
+  return make_map(m, ptr, inner, outer, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 template <int KIND, int BN>
@@ -394,12 +399,21 @@ static cudaError_t launch_tc_bn(int N, const CUtensorMap& a, const CUtensorMap& 
 static int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64); }
 
 cudaError_t launch_tc2_kind(int kind, int BN, const CUtensorMap& a, const CUtensorMap& b,
-                            const TcParams& p, int grid, cudaStream_t s);
+                            const CUtensorMap& c, const TcParams& p, int grid, cudaStream_t s);
 
 static int tc_pf() {  // MOE_TC_PF: k-blocks of B prefetched to L2 for the next wave
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("MOE_TC_PF");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+static int tc_dbg() {  // MOE_TC_DBG: timing experiments only (1: skip epilogue stores)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_TC_DBG");
     v = e ? atoi(e) : 0;
   }
   return v;
@@ -488,10 +502,14 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   p.bias_part = two ? bias_part : nullptr;
   p.sched = tc_sched();
   p.pf_kb = tc_pf();
-  if (two)
-    TC_CUDA(launch_tc2_kind(KIND, bn, ma, mb, p, g_num_sms & ~1, s));
-  else
+  p.dbg = tc_dbg();
+  if (two) {
+    CUtensorMap mc;
+    TC_TRY(make_store_map(&mc, C, ldc, rows));
+    TC_CUDA(launch_tc2_kind(KIND, bn, ma, mb, mc, p, g_num_sms & ~1, s));
+  } else {
     TC_CUDA(launch_tc_bn<KIND>(N, ma, mb, p, s));
+  }
   return MOE_OK;
 }
 
@@ -508,10 +526,14 @@ static moe_status_t wgrad(const void* Abuf, int M, const void* Bbuf, int N, int6
   p.ct = ct;
   p.sched = tc_sched();
   p.pf_kb = tc_pf();
-  if (use_2cta(N, TC_WGRAD))
-    TC_CUDA(launch_tc2_kind(TC_WGRAD, pick_bn(N), ma, mb, p, g_num_sms & ~1, s));
-  else
+  p.dbg = tc_dbg();
+  if (use_2cta(N, TC_WGRAD)) {
+    CUtensorMap mc;
+    TC_TRY(make_store_map(&mc, Out, N, (uint64_t)n_local * M));
+    TC_CUDA(launch_tc2_kind(TC_WGRAD, pick_bn(N), ma, mb, mc, p, g_num_sms & ~1, s));
+  } else {
     TC_CUDA(launch_tc_bn<TC_WGRAD>(N, ma, mb, p, s));
+  }
   return MOE_OK;
 }
 

@@ -56,6 +56,21 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
       : "memory");
 }
+// TMA store of one staged 32 x 32 bf16 box (64-byte swizzle) into C at (col c0, row c1).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -89,10 +104,15 @@ __host__ __device__ constexpr uint32_t make_idesc2(int n, int a_mn, int b_mn) {
 
 constexpr int TC2_M = 256;
 
+// Epilogue staging: one 32 x 32 bf16 box (2 KB, 64-byte swizzle) per epilogue warp, written
+// to C by TMA (cp.async.bulk.tensor store): whole 64-byte row segments instead of one 16-byte
+// piece per lane and row, and asynchronous, so the warp moves on to its next TMEM chunk.
+constexpr int TC2_STG_BYTES = 32 * 32 * 2;
+
 template <int KIND, int BN, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    TcParams p) {
+                    const __grid_constant__ CUtensorMap tmC, TcParams p) {
   using Tr = KindTraits<KIND>;
   constexpr int BNH = BN / 2;                    // B columns held by each CTA
   constexpr int A_BYTES = TC_BM * TC_BK * 2;     // 16 KB: this CTA's 128 rows
@@ -111,6 +131,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bias_bar + STAGES);
   int32_t* s_prefix = reinterpret_cast<int32_t*>(s_tmem + 4);        // [n_local + 1]
   float* s_bias = reinterpret_cast<float*>(s_prefix + MOE_MAX_E + 4);  // [4][128]
+  uint8_t* s_stg = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(s_bias + 4 * 128) + 1023) & ~uintptr_t(1023));  // [8][2 KB]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank();
@@ -137,6 +159,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    prefetch_tmap(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);   // multicast MMA commit
@@ -330,6 +353,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int half = (warp - 4) >> 2;
     const int row_in_tile = (int)crank * TC_BM + q * 32 + lane;
     const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty_bar[0]), 0);
+    uint8_t* stg = s_stg + (warp - 4) * TC2_STG_BYTES;
+    const int blk_in_tile = (int)crank * TC_BM + q * 32;  // this warp's first row in the tile
     int it = 0;
     for (int t = t_begin; t < t_end; t += t_step, ++it) {
       int e, mt, nt;
@@ -337,6 +362,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const int acc = it & 1;
       const int m0 = mt * TC2_M, n0 = nt * BN;
       const int row = m0 + row_in_tile;
+      const int blk_row = m0 + blk_in_tile;  // warp-uniform
       const bool zero_acc = Tr::kgroup && p.kept[e] == 0;
       const int Me = Tr::kgroup ? p.M : p.kept[e];
       const bool row_ok = row < Me;
@@ -456,13 +482,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             }
           }
         }
-        if (store) {
+        (void)store;
+        // One 32-row box per warp (warp-uniform decision).  Boxes start 32-aligned inside a
+        // 128-aligned region, so a box lies entirely below roundup(M_e, 64) or entirely above
+        // it: padded kinds (FWD1, DGRAD_A) store boxes below roundup(M_e, 64) (rows >= M_e are
+        // zeros), the others boxes below roundup(M_e, 32) (rows >= M_e: zeros, never read).
+        bool box;
+        if (Tr::kgroup) box = blk_row < p.M;
+        else if (KIND == TC_FWD1 || KIND == TC_DGRAD_A) box = blk_row < ((Me + 63) & ~63);
+        else box = blk_row < Me;
+        if (!Tr::kgroup && !row_ok) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        if (p.dbg & 1) box = false;
+        if (box) {
           uint4 pk[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            pk[i] = pack(v + 8 * i, __nv_bfloat16());
-            st_v4(crow + col0 + 8 * i, pk[i]);
-          }
+          for (int i = 0; i < 4; ++i) pk[i] = pack(v + 8 * i, __nv_bfloat16());
+          if (lane == 0) tma_store_wait_read();  // the previous box has left the buffer
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i)  // 64-byte swizzle: chunk i of row r at i ^ ((r >> 1) & 3)
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4)) = pk[i];
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            tma_store_2d(&tmC, stg, col0,
+                         Tr::kgroup ? e * p.M + blk_row : p.ct.base[e] + blk_row);
           if (KIND == TC_FWD1) {  // bit j: the stored bf16 H is > 0 (relu output >= 0)
             uint32_t bits = 0;
 #pragma unroll
@@ -491,6 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
     }
   }
+  if (warp >= 4 && lane == 0) tma_store_wait_all();
   tc_fence_before();
   cluster_sync_all();
   if (warp == 2) {
@@ -502,11 +550,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 
 // ------------------------------------------------------------------------------ host side
 template <int KIND, int BN>
-static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p,
-                           int grid, cudaStream_t s) {
+static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                           const TcParams& p, int grid, cudaStream_t s) {
   constexpr int STAGES = (BN == 256) ? 6 : 8;
   constexpr int STAGE_BYTES = (TC_BM + BN / 2) * TC_BK * 2;
-  const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 512 + 4 * (MOE_MAX_E + 8) + 2048;
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 512 + 4 * (MOE_MAX_E + 8) + 2048 +
+                      1024 + 8 * TC2_STG_BYTES;
   auto kf = tc_gemm2_kernel<KIND, BN, STAGES>;
   static bool attr = false;
   if (!attr) {
@@ -514,15 +563,16 @@ static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const TcP
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kf<<<grid, TC_THREADS, smem, s>>>(a, b, p);
+  kf<<<grid, TC_THREADS, smem, s>>>(a, b, c, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tc2_kind(int kind, int BN, const CUtensorMap& a, const CUtensorMap& b,
-                            const TcParams& p, int grid, cudaStream_t s) {
-#define K2(KD)                                                               \
-  case KD:                                                                   \
-    return BN == 256 ? launch2<KD, 256>(a, b, p, grid, s) : launch2<KD, 128>(a, b, p, grid, s);
+                            const CUtensorMap& c, const TcParams& p, int grid, cudaStream_t s) {
+#define K2(KD)                                                                         \
+  case KD:                                                                             \
+    return BN == 256 ? launch2<KD, 256>(a, b, c, p, grid, s)                           \
+                     : launch2<KD, 128>(a, b, c, p, grid, s);
   switch (kind) {
     K2(TC_FWD1) K2(TC_FWD2) K2(TC_DGRAD_A) K2(TC_DGRAD_X) K2(TC_WGRAD)
     default: return cudaErrorInvalidValue;

@@ -30,6 +30,7 @@ struct TcParams {
   int pf_kb;                    // 2-CTA: k-blocks of the next wave's B tile to prefetch to L2
   int sched;                    // 2-CTA tile schedule: 0 round-robin (m fastest),
                                 // 1 contiguous chunk per CTA pair (n fastest), 2 chunk (m fastest)
+  int dbg;                      // timing experiments (MOE_TC_DBG), 0 in production
   CapTable ct;                  // base rows of each local expert region
 };
 
