@@ -65,8 +65,9 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void tma_store_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+template <int N>
+__device__ __forceinline__ void tma_store_wait_read() {  // at most N groups still reading smem
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void tma_store_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -108,6 +109,10 @@ constexpr int TC2_M = 256;
 // to C by TMA (cp.async.bulk.tensor store): whole 64-byte row segments instead of one 16-byte
 // piece per lane and row, and asynchronous, so the warp moves on to its next TMEM chunk.
 constexpr int TC2_STG_BYTES = 32 * 32 * 2;
+#ifndef MOE_TC2_NBUF
+#define MOE_TC2_NBUF 1
+#endif
+constexpr int TC2_NBUF = MOE_TC2_NBUF;  // staging buffers per epilogue warp
 
 template <int KIND, int BN, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
@@ -353,7 +358,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int half = (warp - 4) >> 2;
     const int row_in_tile = (int)crank * TC_BM + q * 32 + lane;
     const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty_bar[0]), 0);
-    uint8_t* stg = s_stg + (warp - 4) * TC2_STG_BYTES;
+    uint8_t* stg0 = s_stg + (warp - 4) * TC2_NBUF * TC2_STG_BYTES;
+    int nbox = 0;
     const int blk_in_tile = (int)crank * TC_BM + q * 32;  // this warp's first row in the tile
     int it = 0;
     for (int t = t_begin; t < t_end; t += t_step, ++it) {
@@ -500,7 +506,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           uint4 pk[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) pk[i] = pack(v + 8 * i, __nv_bfloat16());
-          if (lane == 0) tma_store_wait_read();  // the previous box has left the buffer
+          uint8_t* stg = stg0 + (nbox++ % TC2_NBUF) * TC2_STG_BYTES;
+          if (lane == 0) tma_store_wait_read<TC2_NBUF - 1>();  // this buffer's last box left
           __syncwarp();
 #pragma unroll
           for (int i = 0; i < 4; ++i)  // 64-byte swizzle: chunk i of row r at i ^ ((r >> 1) & 3)
@@ -552,10 +559,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 template <int KIND, int BN>
 static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                            const TcParams& p, int grid, cudaStream_t s) {
-  constexpr int STAGES = (BN == 256) ? 6 : 8;
+  constexpr int STAGES = (BN == 256) ? (TC2_NBUF > 1 ? 5 : 6) : 8;
   constexpr int STAGE_BYTES = (TC_BM + BN / 2) * TC_BK * 2;
   const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 512 + 4 * (MOE_MAX_E + 8) + 2048 +
-                      1024 + 8 * TC2_STG_BYTES;
+                      1024 + 8 * TC2_NBUF * TC2_STG_BYTES;
   auto kf = tc_gemm2_kernel<KIND, BN, STAGES>;
   static bool attr = false;
   if (!attr) {
