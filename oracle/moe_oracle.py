@@ -259,9 +259,52 @@ def aggregate_spec(O, idx, slot_of):
     return out, valid
 
 
+class AssignmentCache:
+    """Per-sample assignment cache (SPEC cache_step S:252-257 and cached_route
+    S:259-267; reading 11): row s = the expert indices sample s was routed to the last time
+    the gate saw it, -1 = unknown (never seen).
+
+    lookup(): cached_route's dispatch indices for a batch: the remembered row of a known
+    sample; for an unknown sample the fallback of S:263 ("falls back to gate-derived routing
+    for that sample, counted as a miss"), i.e. the gate's fresh top-k.
+    update(): cache_step's post-condition: after the gate's forward the remembered
+    rows of the batch's samples are overwritten with the current (fresh) decision."""
+
+    def __init__(self, num_samples: int, k: int):
+        self.table = np.full((num_samples, k), -1, np.int32)
+
+    def known(self, sample_ids):
+        return np.array([bool((self.table[s] >= 0).all()) for s in sample_ids])
+
+    def lookup(self, sample_ids, fresh):
+        fresh = np.asarray(fresh, np.int32)
+        idx = np.empty_like(fresh)
+        for t, sid in enumerate(sample_ids):
+            row = self.table[sid]
+            idx[t] = row if (row >= 0).all() else fresh[t]
+        return idx
+
+    def hit_fraction(self, sample_ids, fresh):
+        """fraction of the batch whose remembered row equals (as a set) the fresh
+        decision; unknown samples are misses (first epoch -> 0.0)."""
+        fresh = np.asarray(fresh)
+        hits = 0
+        for t, sid in enumerate(sample_ids):
+            row = self.table[sid]
+            if (row >= 0).all() and set(row.tolist()) == set(fresh[t].tolist()):
+                hits += 1
+        return hits / max(1, len(sample_ids))
+
+    def update(self, sample_ids, fresh):
+        fresh = np.asarray(fresh, np.int32)
+        for t, sid in enumerate(sample_ids):
+            self.table[sid] = fresh[t]
+
+
 def moe_forward(x, params, k: int, capacities, renormalize: int = 1, cached_idx=None,
                 logits=None, emulate_bf16: bool = False, token_offset: int = 0,
-                prior_counts=None, balance_lambda: float = 0.0) -> FwdState:
+                prior_counts=None, balance_lambda: float = 0.0,
+                cache_fallback: bool = False) -> FwdState:
     """One MoE layer forward.
 
     params: w_gate [n,d], w1 [n,f,d], b1 [n,f], w2 [n,d_out,f], b2 [n,d_out] (fp64 arrays).
@@ -269,7 +312,9 @@ def moe_forward(x, params, k: int, capacities, renormalize: int = 1, cached_idx=
     fp64 gate logits for top-k, weights and backward; else l = x W_g^T.
     cached_idx: sample-assignment caching (reading 11): the cached [T,k] indices
     drive dispatch; weights are normalize(p[t, cached]) from the fresh gate; the fresh top-k
-    is still computed and hit_count = #{t : set(fresh_t) == set(cached_t)}."""
+    is still computed and hit_count = #{t : set(fresh_t) == set(cached_t)}.
+    cache_fallback: cached rows containing -1 are unknown samples: they are routed by the
+    fresh top-k and counted as misses (AssignmentCache.lookup)."""
     x = np.asarray(x, np.float64)
     T = x.shape[0]
     wg = np.asarray(params["w_gate"], np.float64)
@@ -278,12 +323,18 @@ def moe_forward(x, params, k: int, capacities, renormalize: int = 1, cached_idx=
     p = softmax(l)
     fresh = topk_sorted(l, k)
     if cached_idx is not None:
-        idx = np.asarray(cached_idx, np.int32)
+        idx = np.array(cached_idx, np.int32)
+        known = np.ones(T, bool)
         for t in range(T):
             row = idx[t]
+            if cache_fallback and (row < 0).any():
+                idx[t] = fresh[t]          # unknown sample: gate-derived routing, a miss
+                known[t] = False
+                continue
             if len(set(row.tolist())) != k or row.min() < 0 or row.max() >= n:
                 raise ValueError(f"invalid cached row {t}: {row}")
-        hit = int(sum(set(fresh[t].tolist()) == set(idx[t].tolist()) for t in range(T)))
+        hit = int(sum(known[t] and set(fresh[t].tolist()) == set(idx[t].tolist())
+                      for t in range(T)))
     else:
         idx = fresh
         hit = 0

@@ -358,6 +358,45 @@ def test_cached_equals_uncached_when_hit():
         O.moe_forward(x, p, k, caps, 1, cached_idx=bad)
 
 
+def test_assignment_cache_spec_examples():
+    """SPEC cache_step / cached_route examples."""
+    rng = np.random.default_rng(9)
+    n, k, T, d, f, N = 6, 2, 30, 5, 7, 50
+    x = rng.standard_normal((T, d))
+    p = _params(rng, n, d, f, d)
+    caps = [T] * n
+    ids = rng.permutation(N)[:T]
+    cache = O.AssignmentCache(N, k)
+    a = O.moe_forward(x, p, k, caps, 1)
+    # first epoch: empty cache -> hit fraction 0.0 by convention, every sample falls back
+    assert cache.hit_fraction(ids, a.fresh_idx) == 0.0
+    assert not cache.known(ids).any()
+    idx = cache.lookup(ids, a.fresh_idx)
+    assert np.array_equal(idx, a.fresh_idx)
+    b = O.moe_forward(x, p, k, caps, 1, cached_idx=np.full((T, k), -1), cache_fallback=True)
+    assert b.hit_count == 0 and np.array_equal(b.y, a.y)     # fallback = uncached routing
+    cache.update(ids, a.fresh_idx)
+    # identical assignments across epochs -> hit fraction 1.0, bit-identical outputs
+    assert cache.hit_fraction(ids, a.fresh_idx) == 1.0
+    c = O.moe_forward(x, p, k, caps, 1, cached_idx=cache.lookup(ids, a.fresh_idx))
+    assert c.hit_count == T and np.array_equal(c.y, a.y)
+    # all samples reassigned -> 0.0
+    other = np.array([[e for e in range(n) if e not in row][:k] for row in a.fresh_idx], np.int32)
+    cache.update(ids, other)
+    assert cache.hit_fraction(ids, a.fresh_idx) == 0.0
+    # one unknown sample among known ones: it is routed by its fresh top-k and is a miss;
+    # the others use the remembered rows
+    cache.update(ids, a.fresh_idx)
+    cache.table[ids[3]] = -1
+    rows = cache.table[ids].copy()
+    e_ = O.moe_forward(x, p, k, caps, 1, cached_idx=rows, cache_fallback=True)
+    assert e_.hit_count == T - 1
+    assert np.array_equal(e_.idx, a.fresh_idx) and np.array_equal(e_.y, a.y)
+    # without the fallback an unknown row is an error (v1 contract)
+    with pytest.raises(ValueError):
+        O.moe_forward(x, p, k, caps, 1, cached_idx=rows)
+
+
 def test_capacity_change_without_drops_is_identity():
     # S:158 plan equivalence
     rng = np.random.default_rng(7)
