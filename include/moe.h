@@ -138,6 +138,27 @@ MOE_API moe_status_t moe_set_workspace(moe_handle_t h, void* dptr, size_t bytes)
    forward has been consumed by the stream.  Invalid rows raise the device flag. */
 MOE_API moe_status_t moe_set_cached_assignment(moe_handle_t h, const int32_t* d_idx);
 
+/* Per-sample assignment cache (S4.2 P:245-256; SPEC cache_step S:252-257,
+   cached_route S:259-267).  d_table: caller-owned device int32 [num_samples x k], row s =
+   the experts sample s was last routed to, -1 = unknown (the caller fills it with -1).
+   d_sample_ids: device int64 [T], the sample id of each token of the NEXT forwards (the
+   caller rewrites it per batch; ids must be distinct within a batch).  mode:
+     0  off (the default);
+     1  every sample of the batch is known: idx = table[ids] drives dispatch on the side
+        stream concurrently with the gate, exactly as moe_set_cached_assignment (a row with
+        -1 raises device flag 2 and its pairs are dropped);
+     2  fallback: a sample whose row holds -1 is routed by its fresh top-k (counted as a
+        miss); known samples use their rows; routing waits for the gate;
+     3  observe: routing by the fresh top-k (caching off); hit_count is still measured
+        against the remembered rows (the metric that switches caching on).
+   Every forward then overwrites table[ids[t]] with the fresh top-k after the gate
+   (cache_step).  hit_count (stats, metrics) = known samples whose row equals the
+   fresh top-k as a set.  An id outside [0, num_samples) raises device flag 4 (row treated as
+   unknown).  Not combinable with moe_set_cached_assignment (MOE_ERR_STATE). */
+MOE_API moe_status_t moe_set_assignment_cache(moe_handle_t h, int32_t* d_table,
+                                              int64_t num_samples, const int64_t* d_sample_ids,
+                                              int32_t mode);
+
 /* Forward.  T <= max_tokens (T may be 0).  All pointers device; y is written
    (y[t] = 0 for a token whose every pair was dropped). */
 typedef struct {

@@ -5,9 +5,9 @@ This package is the thin Python binding (argument marshalling, workspace allocat
 """
 from ._lib import MoEError, load  # noqa: F401
 from .layer import CapacityPolicy, DynaMoE, MoEFunction, MoELayer, capacity_from_factors  # noqa: F401
-from .runtime import (GraphedStep, MetricQueue, RecompileRuntime, caching_trigger,  # noqa: F401
-                      capacity_trigger)
+from .runtime import (AssignmentCache, GraphedStep, MetricQueue, RecompileRuntime,  # noqa: F401
+                      caching_trigger, capacity_trigger)
 
 __all__ = ["MoELayer", "MoEFunction", "DynaMoE", "CapacityPolicy", "capacity_from_factors",
-           "MoEError", "load", "GraphedStep", "MetricQueue", "RecompileRuntime", "caching_trigger",
+           "MoEError", "load", "AssignmentCache", "GraphedStep", "MetricQueue", "RecompileRuntime", "caching_trigger",
            "capacity_trigger"]

@@ -81,6 +81,8 @@ EXPORTS = {
     "moe_workspace_size": ([C.c_void_p, C.POINTER(C.c_size_t)], C.c_int),
     "moe_set_workspace": ([C.c_void_p, C.c_void_p, C.c_size_t], C.c_int),
     "moe_set_cached_assignment": ([C.c_void_p, C.c_void_p], C.c_int),
+    "moe_set_assignment_cache": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32],
+                                 C.c_int),
     "moe_forward": ([C.c_void_p, C.POINTER(FwdArgs)], C.c_int),
     "moe_backward": ([C.c_void_p, C.POINTER(BwdArgs)], C.c_int),
     "moe_get_routing": ([C.c_void_p, C.POINTER(Routing)], C.c_int),

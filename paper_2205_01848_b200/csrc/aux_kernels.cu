@@ -96,4 +96,76 @@ cudaError_t launch_balance_final(const float* gsum, const int32_t* counts, int n
   return cudaGetLastError();
 }
 
+// --------------------------------------------------------------------------------------
+// Per-sample assignment cache (S4.2 P:245-256; SPEC cache_step S:252-257, cached_route
+// S:259-267): a caller-owned table [num_samples x k] int32, -1 = unknown.
+// --------------------------------------------------------------------------------------
+__global__ void cache_gather_kernel(const int32_t* __restrict__ table, long long num, int k,
+                                    const int64_t* __restrict__ ids, int Tn,
+                                    int32_t* __restrict__ idx, int32_t* __restrict__ flags) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Tn) return;
+  const long long sid = ids[t];
+  const bool ok = sid >= 0 && sid < num;
+  if (!ok) atomicOr(flags, 4);  // sample id out of range
+  for (int r = 0; r < k; ++r) idx[(size_t)t * k + r] = ok ? table[sid * k + r] : -1;
+}
+
+__global__ void cache_update_kernel(int32_t* __restrict__ table, long long num, int k,
+                                    const int64_t* __restrict__ ids, int Tn,
+                                    const int32_t* __restrict__ fresh) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Tn) return;
+  const long long sid = ids[t];
+  if (sid < 0 || sid >= num) return;
+  for (int r = 0; r < k; ++r) table[sid * k + r] = fresh[(size_t)t * k + r];
+}
+
+// observe mode: hit = the remembered row equals the fresh top-k as a set (unknown: a miss),
+// then remember the fresh row (the metric of P:353 while caching is off)
+__global__ void cache_observe_kernel(int32_t* __restrict__ table, long long num, int k,
+                                     const int64_t* __restrict__ ids, int Tn,
+                                     const int32_t* __restrict__ fresh, int32_t* __restrict__ hit,
+                                     int32_t* __restrict__ flags) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Tn) return;
+  const long long sid = ids[t];
+  if (sid < 0 || sid >= num) {
+    atomicOr(flags, 4);
+    return;
+  }
+  int32_t* row = table + sid * k;
+  const int32_t* fr = fresh + (size_t)t * k;
+  bool same = true;
+  for (int r = 0; r < k; ++r) {
+    bool found = false;
+    for (int q = 0; q < k; ++q) found |= row[r] == fr[q];
+    same &= found && row[r] >= 0;
+  }
+  if (same) atomicAdd(hit, 1);
+  for (int r = 0; r < k; ++r) row[r] = fr[r];
+}
+
+cudaError_t launch_cache_observe(int32_t* table, int64_t num, int k, const int64_t* ids, int T,
+                                 const int32_t* fresh, int32_t* hit, int32_t* flags,
+                                 cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  cache_observe_kernel<<<(T + 255) / 256, 256, 0, s>>>(table, num, k, ids, T, fresh, hit, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cache_gather(const int32_t* table, int64_t num, int k, const int64_t* ids,
+                                int T, int32_t* idx, int32_t* flags, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  cache_gather_kernel<<<(T + 255) / 256, 256, 0, s>>>(table, num, k, ids, T, idx, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cache_update(int32_t* table, int64_t num, int k, const int64_t* ids, int T,
+                                const int32_t* fresh, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  cache_update_kernel<<<(T + 255) / 256, 256, 0, s>>>(table, num, k, ids, T, fresh);
+  return cudaGetLastError();
+}
+
 }  // namespace moe

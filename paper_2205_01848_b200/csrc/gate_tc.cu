@@ -34,6 +34,7 @@ struct GateFwdParams {
   float* w_out;           // [T x k]
   int32_t* hit;
   int32_t* flags;
+  int32_t* idx_fix;       // fallback mode: rows of unknown samples (-1) get the fresh top-k
 };
 
 struct GateDxParams {
@@ -270,15 +271,22 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         float lv[KM];
         int use[KM];
         if (p.cached) {
-          bool ok = true;
+          bool ok = true, unknown = false;
 #pragma unroll
           for (int r = 0; r < KM; ++r) {
             if (r >= k) break;
             ok &= (cidx[r] >= 0 && cidx[r] < n);
+            unknown |= cidx[r] == -1;
 #pragma unroll
             for (int q2 = 0; q2 < r; ++q2) ok &= (cidx[q2] != cidx[r]);
           }
-          if (!ok) atomicOr(p.flags, 2);
+          // an unknown sample (fallback mode) is routed by its fresh top-k, a miss
+          if (!ok && !(unknown && p.idx_fix)) atomicOr(p.flags, 2);
+          if (!ok && p.idx_fix) {
+#pragma unroll
+            for (int r = 0; r < KM; ++r)
+              if (r < k) p.idx_fix[(size_t)t * k + r] = sel_e[r];
+          }
           bool same = true;
 #pragma unroll
           for (int r = 0; r < KM; ++r) {
@@ -705,7 +713,7 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
   const int bn = n <= 64 ? 64 : (n <= 128 ? 128 : 256);
   if (!map2d(&mx, x, d, T, 64, 128) || !map2d(&mw, wg, d, n, 64, bn)) return cudaErrorInvalidValue;
   GateFwdParams p{T, n, k, renorm, cached, b.logits, cached ? b.fresh_idx : b.idx, b.w,
-                  b.hit_count, b.flags};
+                  b.hit_count, b.flags, cached ? b.idx_fix : nullptr};
   const int MT = (T + 127) / 128;
   const int grid = MT < g_sms ? MT : g_sms;
 #define GF(BN, ST)                                                                       \

@@ -32,7 +32,19 @@ struct RouteBufs {
   const float* dw_ext;    // [T x k] extra gradient w.r.t. the gate weights (backward input)
   const float* bal_g;     // [n] balance-term coefficients lambda*n*T_i/T_g (backward)
   int32_t* grow;          // [T x k] token-side dO/dX row of each pair or -1 (combine_bwd)
+  int32_t* idx_fix;       // cache fallback mode: the gate writes the fresh top-k of unknown
+                          // samples (cached row with -1) into these dispatch-index rows
 };
+
+// Per-sample assignment cache (N4; SPEC cache_step / cached_route): idx[t] = table[ids[t]]
+// (flag 4 and a -1 row for an out-of-range id) / table[ids[t]] = fresh[t].
+cudaError_t launch_cache_gather(const int32_t* table, int64_t num, int k, const int64_t* ids,
+                                int T, int32_t* idx, int32_t* flags, cudaStream_t s);
+cudaError_t launch_cache_observe(int32_t* table, int64_t num, int k, const int64_t* ids, int T,
+                                 const int32_t* fresh, int32_t* hit, int32_t* flags,
+                                 cudaStream_t s);
+cudaError_t launch_cache_update(int32_t* table, int64_t num, int k, const int64_t* ids, int T,
+                                const int32_t* fresh, cudaStream_t s);
 
 // dtype: 0 = fp32, 1 = bf16 for every templated launcher below.
 cudaError_t launch_gate_topk(int dtype, const void* x, const void* wg, int T, int n, int d,

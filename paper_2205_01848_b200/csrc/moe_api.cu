@@ -45,6 +45,12 @@ struct moe_ctx {
   size_t ws_bytes = 0;
   RouteBufs rb{};
   const int32_t* cached = nullptr;
+  // per-sample assignment cache (N4): caller-owned table [ctab_num x k], sample ids [T]
+  int32_t* ctab = nullptr;
+  int64_t ctab_num = 0;
+  const int64_t* cids = nullptr;
+  int ctab_mode = 0;
+  int last_cached = 0;        // the last forward dispatched from cached indices
   // saved forward state for backward
   int have_fwd = 0, T_last = 0;
   moe_fwd_args_t fa{};
@@ -402,7 +408,24 @@ moe_status_t moe_set_workspace(moe_handle_t h, void* dptr, size_t bytes) {
 
 moe_status_t moe_set_cached_assignment(moe_handle_t h, const int32_t* d_idx) {
   if (!h) return MOE_ERR_INVALID_ARG;
+  if (d_idx && h->ctab_mode)
+    return fail(h, MOE_ERR_STATE, "an assignment cache table is active (mode != 0)");
   h->cached = d_idx;
+  return MOE_OK;
+}
+
+moe_status_t moe_set_assignment_cache(moe_handle_t h, int32_t* d_table, int64_t num_samples,
+                                      const int64_t* d_sample_ids, int32_t mode) {
+  if (!h) return MOE_ERR_INVALID_ARG;
+  if (mode < 0 || mode > 3) return fail(h, MOE_ERR_INVALID_ARG, "mode must be 0..3");
+  if (mode && (!d_table || num_samples <= 0 || !d_sample_ids))
+    return fail(h, MOE_ERR_INVALID_ARG, "null table / sample ids");
+  if (mode && h->cached)
+    return fail(h, MOE_ERR_STATE, "raw cached indices are set (moe_set_cached_assignment)");
+  h->ctab = mode ? d_table : nullptr;
+  h->ctab_num = mode ? num_samples : 0;
+  h->cids = mode ? d_sample_ids : nullptr;
+  h->ctab_mode = mode;
   return MOE_OK;
 }
 
@@ -424,8 +447,19 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   void* H = ws + h->L.hbuf;
   void* O = buf_o(h);
   const int ntiles = (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE;
-  const bool cached = h->cached != nullptr;
+  // dispatch-index sources: raw cached indices, or the per-sample table (mode 1: every
+  // sample known -> the same side-stream overlap; mode 2: unknown samples fall back to the
+  // gate, so routing waits for it), else the gate's top-k
+  const bool observe = h->ctab_mode == 3;   // metric + remember only, fresh routing
+  const bool tab = h->ctab_mode != 0 && !observe;
+  const bool fallback = h->ctab_mode == 2;
+  const bool cached = h->cached != nullptr || (tab && !fallback);
+  const int32_t* cidx = tab ? rb.idx : h->cached;   // what the gate compares/weights against
+  h->last_cached = cached || fallback;
   CUDA_TRY(h, cudaMemsetAsync(rb.hit_count, 0, 4, s0));
+  if (tab)  // idx[t] = table[sample_ids[t]] (before the fork: the side stream reads it)
+    KL(h, T > 0, "cache_gather", s0, launch_cache_gather(h->ctab, h->ctab_num, k, h->cids, T,
+                                                         rb.idx, rb.flags, s0));
 
   // Everything from the routing tables up to the expert outputs depends only on the
   // dispatch indices.  Uncached: they are the gate's top-k, so it all follows the gate on
@@ -437,13 +471,23 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, s0));
     CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
     sd = h->side;
-    if (T > 0)
+    if (T > 0 && !tab)
       CUDA_TRY(h, cudaMemcpyAsync(rb.idx, h->cached, (size_t)T * k * 4, cudaMemcpyDeviceToDevice, sd));
   } else {
+    // fallback mode: the gate rewrites the rows of unknown samples with their fresh top-k
+    rb.idx_fix = fallback ? rb.idx : nullptr;
+    const int32_t* gc = fallback ? rb.idx : nullptr;
     if (h->use_tc)
-      KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, nullptr, rb, s0));
+      KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, gc, rb, s0));
     else
-      KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, nullptr, rb, s0));
+      KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, gc, rb, s0));
+    rb.idx_fix = nullptr;
+    if (tab)  // cache_step: remember this batch's fresh decisions
+      KL(h, T > 0, "cache_update", s0, launch_cache_update(h->ctab, h->ctab_num, k, h->cids, T,
+                                                           fallback ? rb.fresh_idx : rb.idx, s0));
+    if (observe)  // hit metric against the remembered rows, then remember
+      KL(h, T > 0, "cache_update", s0, launch_cache_observe(h->ctab, h->ctab_num, k, h->cids, T,
+                                                            rb.idx, rb.hit_count, rb.flags, s0));
   }
   KL(h, T > 0, "route_hist", sd, launch_route_hist(rb.idx, T, k, n, rb.tile_hist, sd));
   KL(h, 1, "route_scan", sd, launch_route_scan(rb.tile_hist, ntiles, n, h->ct, rb, sd));
@@ -520,9 +564,12 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   }
   if (cached) {
     if (h->use_tc)
-      KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, h->cached, rb, s0));
+      KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, cidx, rb, s0));
     else
-      KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, h->cached, rb, s0));
+      KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, cidx, rb, s0));
+    if (tab)  // cache_step; the side stream only reads idx, never the table
+      KL(h, T > 0, "cache_update", s0, launch_cache_update(h->ctab, h->ctab_num, k, h->cids, T,
+                                                           rb.fresh_idx, s0));
     CUDA_TRY(h, cudaEventRecord(h->ev_join, sd));
     CUDA_TRY(h, cudaStreamWaitEvent(s0, h->ev_join, 0));
   }
@@ -754,7 +801,7 @@ moe_status_t moe_get_routing(moe_handle_t h, moe_routing_t* out) {
   out->logits = r.logits;
   out->weights = r.w;
   out->idx = r.idx;
-  out->fresh_idx = h->cached ? r.fresh_idx : r.idx;
+  out->fresh_idx = h->last_cached ? r.fresh_idx : r.idx;
   out->slot_of = r.slot_of;
   out->token_of_slot = r.token_of_slot;
   out->counts = r.counts;
@@ -792,7 +839,8 @@ moe_status_t moe_check_device_flags(moe_handle_t h, int32_t* flags_out) {
     CUDA_TRY(h, cudaMemsetAsync(h->rb.flags, 0, 4, h->stream));
     return fail(h, MOE_ERR_DEVICE_FLAG,
                 std::string("device flags: ") + ((fl & 1) ? "NaN logit " : "") +
-                    ((fl & 2) ? "invalid cached index" : ""));
+                    ((fl & 2) ? "invalid cached index " : "") +
+                    ((fl & 4) ? "sample id out of range" : ""));
   }
   return MOE_OK;
 }

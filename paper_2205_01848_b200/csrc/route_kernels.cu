@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(
     const T* __restrict__ x, const T* __restrict__ wg, int Tn, int n, int d, int k,
     int renorm, const int32_t* __restrict__ cached, float* __restrict__ logits,
     int32_t* __restrict__ idx_out, float* __restrict__ w_out, int32_t* __restrict__ hit,
-    int32_t* __restrict__ flags) {
+    int32_t* __restrict__ flags, int32_t* __restrict__ idx_fix) {
   extern __shared__ float smem[];
   float* xs = smem;                              // [GATE_TOK][GATE_DK+1]
   float* ws = xs + GATE_TOK * (GATE_DK + 1);     // [n][GATE_DK+1]
@@ -101,15 +101,18 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(
       int use[MOE_MAX_K];
       if (cached) {
         const int32_t* crow = cached + (size_t)t * k;
-        bool ok = true;
+        bool ok = true, unknown = false;
         for (int r = 0; r < k; ++r) {
           use[r] = crow[r];
           ok &= (use[r] >= 0 && use[r] < n);
+          unknown |= use[r] == -1;
           for (int q = 0; q < r; ++q) ok &= (use[q] != use[r]);
         }
-        if (!ok) {
-          atomicOr(flags, 2);
+        if (!ok) {  // unknown sample in fallback mode: fresh top-k, a miss
+          if (!(unknown && idx_fix)) atomicOr(flags, 2);
           for (int r = 0; r < k; ++r) use[r] = sel[r];
+          if (idx_fix)
+            for (int r = 0; r < k; ++r) idx_fix[(size_t)t * k + r] = sel[r];
         }
         bool same = true;  // set equality of fresh and cached rows
         for (int r = 0; r < k; ++r) {
@@ -155,12 +158,13 @@ cudaError_t launch_gate_topk(int dtype, const void* x, const void* wg, int T, in
       cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
       kf<<<grid, 256, smem, s>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)wg, T, n,  \
                                  d, k, renorm, cached, b.logits, idx_out, b.w,             \
-                                 b.hit_count, b.flags);                                    \
+                                 b.hit_count, b.flags, cached ? b.idx_fix : nullptr);      \
     } else {                                                                               \
       auto kf = gate_topk_kernel<float, NJ>;                                               \
       cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
       kf<<<grid, 256, smem, s>>>((const float*)x, (const float*)wg, T, n, d, k, renorm,    \
-                                 cached, b.logits, idx_out, b.w, b.hit_count, b.flags);    \
+                                 cached, b.logits, idx_out, b.w, b.hit_count, b.flags,     \
+                                 cached ? b.idx_fix : nullptr);                            \
     }                                                                                      \
     return cudaGetLastError();                                                             \
   }
@@ -179,7 +183,10 @@ __global__ void route_hist_kernel(const int32_t* __restrict__ idx, int Tn, int k
   __syncthreads();
   int t = blockIdx.x * MOE_ROUTE_TILE + threadIdx.x;
   if (t < Tn)
-    for (int r = 0; r < k; ++r) atomicAdd(&h[idx[(size_t)t * k + r]], 1);
+    for (int r = 0; r < k; ++r) {
+      const int e = idx[(size_t)t * k + r];
+      if ((unsigned)e < (unsigned)n) atomicAdd(&h[e], 1);  // invalid cached index: flagged
+    }
   __syncthreads();
   for (int e = threadIdx.x; e < n; e += blockDim.x) hist[(size_t)blockIdx.x * n + e] = h[e];
 }
@@ -334,7 +341,8 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
     for (int r = 0; r < MOE_MAX_K; ++r) {
       if (r >= k) break;
       ev[r] = idx[(size_t)t * k + r];
-      atomicOr(&masks[ev[r]][lt >> 5], 1u << (lt & 31));
+      if ((unsigned)ev[r] < (unsigned)n) atomicOr(&masks[ev[r]][lt >> 5], 1u << (lt & 31));
+      else ev[r] = -1;  // invalid cached index (device flag raised by the gate): dropped
     }
   }
   __syncthreads();
@@ -343,7 +351,9 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
     for (int r = 0; r < MOE_MAX_K; ++r) {
       if (r >= k) break;
       int row = -1;
-      if (t < Tn) {
+      if (t < Tn && ev[r] < 0) {
+        slot_of[(size_t)t * k + r] = -1;
+      } else if (t < Tn) {
         const int e = ev[r];
         int rank = __popc(masks[e][lt >> 5] & ((1u << (lt & 31)) - 1u));
         for (int q = 0; q < (lt >> 5); ++q) rank += __popc(masks[e][q]);

@@ -147,6 +147,22 @@ class MoELayer:
         self._cached_ref = idx
         L.check(self.lib.moe_set_cached_assignment(self.h, _ptr(idx)), self.h)
 
+    def set_assignment_cache(self, table, sample_ids, mode: int):
+        """Per-sample assignment cache (N4): table int32 [num_samples, k] (device, -1 =
+        unknown), sample_ids int64 [T] (device) of the next forwards; mode 0 off, 1 all
+        samples known (overlap with the gate), 2 unknown samples fall back to the gate."""
+        if mode:
+            if table.dtype != torch.int32 or not table.is_cuda or not table.is_contiguous():
+                raise ValueError("table must be a contiguous int32 CUDA tensor")
+            if sample_ids.dtype != torch.int64 or not sample_ids.is_cuda:
+                raise ValueError("sample_ids must be an int64 CUDA tensor")
+            self._ctab_ref = (table, sample_ids)
+            L.check(self.lib.moe_set_assignment_cache(self.h, _ptr(table), table.shape[0],
+                                                      _ptr(sample_ids), int(mode)), self.h)
+        else:
+            self._ctab_ref = None
+            L.check(self.lib.moe_set_assignment_cache(self.h, None, 0, None, 0), self.h)
+
     # -- loss variants (N3) -----------------------------------------------------------
     def set_balance_loss(self, lam: float):
         """Eq. 3 balance term weight (0 = off); the backward then includes dB/dl."""

@@ -30,6 +30,47 @@ def caching_trigger(hit_fraction, epoch, enabled, enable_at=0.96, disable_below=
     return bool(out.value)
 
 
+class AssignmentCache:
+    """Per-sample assignment cache of one layer (N4; S4.2 P:245-256).
+
+    The table lives on the device (int32 [num_samples, k], -1 = unknown) and is read and
+    updated by the library's kernels; the host only tracks WHICH ids have been seen, so it
+    can pick the library mode for a batch without a device sync:
+      caching off  -> mode 3 (observe: fresh routing, hit metric, remember);
+      caching on, every id seen -> mode 1 (cached routing overlaps the gate);
+      caching on, some id unseen -> mode 2 (unknown samples fall back to the gate).
+    `enabled` is switched by the caching trigger from the per-iteration hit metric."""
+
+    def __init__(self, layer, num_samples: int):
+        import numpy as np
+        self.layer = layer
+        self.table = torch.full((num_samples, layer.k), -1, dtype=torch.int32, device=layer.device)
+        self.seen = np.zeros(num_samples, dtype=bool)
+        self.ids = torch.empty(max(1, layer.max_tokens), dtype=torch.int64, device=layer.device)
+        self.enabled = False
+        self.last_mode = 0
+
+    def bind(self, sample_ids):
+        """Set the sample ids (host sequence / CPU tensor, distinct) of the next forward."""
+        import numpy as np
+        ids = np.asarray(sample_ids, dtype=np.int64)
+        T = ids.shape[0]
+        self.ids[:T].copy_(torch.from_numpy(ids))   # pageable source: host-synchronous copy
+        if not self.enabled:
+            mode = 3
+        elif self.seen[ids].all():
+            mode = 1
+        else:
+            mode = 2
+        self.layer.set_assignment_cache(self.table, self.ids, mode)
+        self.seen[ids] = True
+        self.last_mode = mode
+        return mode
+
+    def unbind(self):
+        self.layer.set_assignment_cache(None, None, 0)
+
+
 class MetricQueue:
     """Python view of the library's per-iteration metric queue of one layer."""
 
