@@ -35,7 +35,13 @@ struct GateFwdParams {
   int32_t* hit;
   int32_t* flags;
   int32_t* idx_fix;       // fallback mode: rows of unknown samples (-1) get the fresh top-k
+  int dbg;                 // timing experiments (MOE_GATE_DBG), 0 in production
+  int tma_logits;          // logits written by TMA from a staged 32 x 16 box (n % 16 == 0)
 };
+
+// logits staging of the gate epilogue: one 32-row x 16-column fp32 box (2 KB, 64-byte
+// swizzle) per epilogue warp
+constexpr int GF_STG_BYTES = 32 * 16 * 4;
 
 struct GateDxParams {
   int T, n_pad, k, d;
@@ -126,9 +132,10 @@ __device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
 // K1: gate forward + fused softmax / top-k / normalize epilogue
 // ======================================================================================
 template <int BN, int STAGES, int KM>
-__global__ void __launch_bounds__(G_THREADS, 1)
+__global__ void __launch_bounds__(G_THREADS, 2)
     gate_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmX,
-                       const __grid_constant__ CUtensorMap tmW, GateFwdParams p, int K) {
+                       const __grid_constant__ CUtensorMap tmW,
+                       const __grid_constant__ CUtensorMap tmL, GateFwdParams p, int K) {
   constexpr int A_BYTES = TC_BM * TC_BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + BN * TC_BK * 2;
   constexpr uint32_t IDESC = make_idesc(BN, 0, 0);
@@ -140,12 +147,14 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     prefetch_tmap(&tmW);
   }
   Bars b = setup_bars<STAGES>(smem + STAGES * STAGE_BYTES, 2 * BN, warp, lane);
+  uint8_t* s_stg = smem + STAGES * STAGE_BYTES + 1024;  // [4 warps][2 KB], 1 KB aligned
   const uint32_t tmem_base = *b.tmem;
   const int MT = (p.T + TC_BM - 1) / TC_BM;
   const int nk = K / TC_BK;
 
   if (warp == 0) {
     if (lane == 0) {
+      if (p.tma_logits) prefetch_tmap(&tmL);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < MT; t += gridDim.x) {
@@ -214,6 +223,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           if (r < k) cidx[r] = p.cached[(size_t)t * k + r];
       }
       float m_run = -INFINITY;
+      float s_run = 0.f;  // raw mode: online softmax denominator sum_e exp(l_e - m_run)
       bool nan_seen = false;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       float* lrow = p.logits + (size_t)t * n;
@@ -222,8 +232,26 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         if (c * 32 >= n) break;  // warp-uniform
         uint32_t r32[32];
         tmem_ld32(taddr + c * 32, r32);
-        if (!valid) continue;
-        if ((n & 3) == 0 && c * 32 + 32 <= n) {
+        if (p.tma_logits) {  // warp-uniform: two 32 x 16 boxes (rows >= T clipped by TMA)
+          uint8_t* stg = s_stg + q * GF_STG_BYTES;
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            if (c * 32 + h2 * 16 >= n) break;
+            if (lane == 0) tma_store_wait_read<0>();
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)  // 64-byte swizzle: chunk i of row r at i ^ ((r>>1)&3)
+              *reinterpret_cast<uint4*>(stg + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(r32[h2 * 16 + 4 * i], r32[h2 * 16 + 4 * i + 1],
+                             r32[h2 * 16 + 4 * i + 2], r32[h2 * 16 + 4 * i + 3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tma_store_2d(&tmL, stg, c * 32 + h2 * 16, tile * TC_BM + q * 32);
+          }
+        }
+        if (!valid || p.dbg) continue;
+        if (p.tma_logits) {
+        } else if ((n & 3) == 0 && c * 32 + 32 <= n) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
             *reinterpret_cast<uint4*>(lrow + c * 32 + j) = make_uint4(r32[j], r32[j + 1], r32[j + 2], r32[j + 3]);
@@ -257,11 +285,24 @@ __global__ void __launch_bounds__(G_THREADS, 1)
               ce = te;
             }
           }
-          m_run = fmaxf(m_run, v);  // row max for the raw-probability denominator
 #pragma unroll
           for (int r = 0; r < KM; ++r)
             if (cidx[r] == e) cval[r] = v;
           }
+        }
+        // row max and (raw mode) the softmax denominator from registers, rescaled per chunk
+        float cm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c * 32 + j < n) cm = fmaxf(cm, __uint_as_float(r32[j]));
+        if (cm > m_run) {
+          if (!p.renorm) s_run *= expf(m_run - cm);
+          m_run = cm;
+        }
+        if (!p.renorm) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j < n) s_run += expf(__uint_as_float(r32[j]) - m_run);
         }
       }
       tc_fence_before();
@@ -326,8 +367,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           for (int r = 0; r < KM; ++r)
             if (r < k) { wrow[r] = ev[r] / ssum; orow[r] = sel_e[r]; }
         } else {
-          float ssum = 0.f;
-          for (int e = 0; e < n; ++e) ssum += expf(lrow[e] - m_run);
+          const float ssum = s_run;
 #pragma unroll
           for (int r = 0; r < KM; ++r)
             if (r < k) { wrow[r] = expf(lv[r] - m_run) / ssum; orow[r] = sel_e[r]; }
@@ -335,6 +375,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       }
     }
   }
+  if (warp >= 4 && lane == 0 && p.tma_logits) tma_store_wait_all();
   teardown(tmem_base, 2 * BN, warp);
 }
 
@@ -712,22 +753,36 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
   CUtensorMap mx, mw;
   const int bn = n <= 64 ? 64 : (n <= 128 ? 128 : 256);
   if (!map2d(&mx, x, d, T, 64, 128) || !map2d(&mw, wg, d, n, 64, bn)) return cudaErrorInvalidValue;
+  CUtensorMap ml{};
+  int tma_logits = 0;
+  if (n % 16 == 0) {  // fp32 logits [T x n], 16 x 32 boxes, 64-byte swizzle
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)T};
+    cuuint64_t strides[1] = {(cuuint64_t)n * 4};
+    cuuint32_t box[2] = {16, 32};
+    cuuint32_t es[2] = {1, 1};
+    tma_logits = g_enc(&ml, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, b.logits, dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   GateFwdParams p{T, n, k, renorm, cached, b.logits, cached ? b.fresh_idx : b.idx, b.w,
-                  b.hit_count, b.flags, cached ? b.idx_fix : nullptr};
+                  b.hit_count, b.flags, cached ? b.idx_fix : nullptr,
+                  getenv("MOE_GATE_DBG") ? atoi(getenv("MOE_GATE_DBG")) : 0, tma_logits};
   const int MT = (T + 127) / 128;
-  const int grid = MT < g_sms ? MT : g_sms;
+  // two CTAs per SM (4-stage rings): twice the epilogue warps, which bound this kernel
+  const int grid = MT < 2 * g_sms ? MT : 2 * g_sms;
 #define GF(BN, ST)                                                                       \
   {                                                                                      \
     auto kf = k == 1 ? gate_fwd_tc_kernel<BN, ST, 1>                                     \
                      : (k == 2 ? gate_fwd_tc_kernel<BN, ST, 2>                           \
                                : (k <= 4 ? gate_fwd_tc_kernel<BN, ST, 4>                 \
                                          : gate_fwd_tc_kernel<BN, ST, 8>));              \
-    size_t sm = smem_for((128 + BN) * 64 * 2, ST);                                       \
+    size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 1024 + 4 * GF_STG_BYTES;             \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \
-    kf<<<grid, G_THREADS, sm, s>>>(mx, mw, p, d);                                        \
+    kf<<<grid, G_THREADS, sm, s>>>(mx, mw, ml, p, d);                                    \
   }
-  if (bn == 64) GF(64, 8) else if (bn == 128) GF(128, 6) else GF(256, 4)
+  if (bn == 64) GF(64, 4) else if (bn == 128) GF(128, 3) else GF(256, 2)
 #undef GF
   return cudaGetLastError();
 }

@@ -620,7 +620,7 @@ cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, 
 // logits, dy and O rows are all requested before the first use.
 // =====================================================================================
 template <typename T, int VPL, int KM>
-__global__ void __launch_bounds__(256) combine_bwd_kernel(
+__global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
     const T* __restrict__ dy, const T* __restrict__ obuf, const float* __restrict__ w,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of,
     const float* __restrict__ logits, CapTable ct, int Tn, int k, int n, int dout, int renorm,
