@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
                     help="expert-parallel exchange: peer = device-initiated through peer "
                          "memory over NVLink (N1, default); nccl = grouped send/recv")
+    ap.add_argument("--fusion", choices=["none", "combine", "all"], default="combine",
+                    help="N2 fusions: combine = y written by the second expert GEMM's epilogue "
+                         "(k = 1, default); all = also gather x rows in the expert GEMMs")
     return ap.parse_args()
 
 
@@ -177,18 +180,22 @@ def dist_setup(args):
 # ------------------------------------------------------------------------------------------
 # algorithmic work per kernel: bytes or FLOPs per launch
 # ------------------------------------------------------------------------------------------
-def kernel_work(cfg, T, A, s, A_tok=None):
+def kernel_work(cfg, T, A, s, A_tok=None, gather=False, fcomb=False):
     """A: kept rows of this GPU's experts (GEMM work); A_tok: kept pairs of this GPU's tokens
-    (dispatch / combine traffic).  Equal on one GPU."""
+    (dispatch / combine traffic).  Equal on one GPU.  gather: N2 fusion on (the dispatch
+    writes only routing tables + the y rows of dropped tokens; the combine is in FWD2)."""
     n, k, d, f, do = cfg.n_experts, cfg.top_k, cfg.d_model, cfg.d_ff, cfg.d_out
     gf = 2.0 * A * d * f  # one expert GEMM (fwd or dgrad or wgrad) = 2*A*d*f FLOPs
     A = A if A_tok is None else A_tok
+    disp = 8 * T * k + 4 * A + ((T - A) * do * s if fcomb else 0)  # routing tables, dropped y rows
+    if not gather:
+        disp += (T + A) * d * s                                     # + the X row copy
     return {
         # name: (kind, amount)   kind "flop" (tensor/alu) or "byte" (hbm)
         "gate_topk": ("byte", T * d * s + n * d * s + 4 * T * n + 8 * T * k),
         "route_hist": ("byte", 4 * T * k),
         "route_scan": ("byte", 8 * (T // 128 + 1) * n),
-        "dispatch": ("byte", (T + A) * d * s + 8 * T * k + 4 * A),
+        "dispatch": ("byte", disp),
         "zero_pad": ("byte", 0),
         "ffn_gemm1": ("flop", gf), "ffn_gemm2": ("flop", gf),
         "combine_fwd": ("byte", (A + T) * do * s + 8 * T * k),
@@ -244,6 +251,12 @@ def run_ours(args):
         else:
             layer.peer_attach([layer.peer_window()])
     layer.set_capacity_factors([alpha] * n, T * (ws if use_ep else 1))
+    # N2 fusions (moe_set_fusion): gather x rows in the expert GEMMs, combine in FWD2 (k = 1)
+    fflags = {"none": 0, "combine": 2, "all": 3}[args.fusion]
+    tc1 = not use_ep and cfg.dtype == "bf16" and getattr(layer, "uses_tcgen05", False)
+    gather = tc1 and bool(fflags & 1) and d % 128 == 0 and f % 128 == 0
+    fcomb = tc1 and bool(fflags & 2) and k == 1 and do % 128 == 0 and not args.cached
+    layer.set_fusion(fflags)
     tdt = layer.tdtype
     grads = dict(dx=torch.empty(T, d, dtype=tdt, device=dev),
                  dw_gate=torch.empty(n, d, dtype=tdt, device=dev),
@@ -331,7 +344,7 @@ def run_ours(args):
 
     # ---------------- per-kernel rooflines ----------------
     pk = peaks()
-    work = kernel_work(cfg, T, A, s, A_tok)
+    work = kernel_work(cfg, T, A, s, A_tok, gather=gather, fcomb=fcomb)
     sm_peak_tf = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
     kernels = {}
     for name, (cnt, tot) in ktimes.items():
@@ -445,6 +458,8 @@ def run_ours(args):
                                        + ("peer memory, device-initiated)" if peer else "NCCL)")
                                        if use_ep else "1 GPU"),
                        "l2": "inputs > L2 (x 134 MB + weights 1 GB), no flush",
+                       "fusion": "+".join([nm for nm, on in (("gather", gather), ("combine", fcomb))
+                                           if on]) or "none",
                        "kept_assignments": A, "drops": stats["drops"],
                        "padding_flops_avoided": padded_flops},
             "roofline": roofline,

@@ -322,6 +322,23 @@ MOE_API moe_status_t moe_peer_export(moe_handle_t h, void* ipc_handle /* host, 6
 MOE_API moe_status_t moe_peer_attach(moe_handle_t h, void* const* windows /* host [R] */);
 MOE_API moe_status_t moe_peer_import(moe_handle_t h, const void* handles /* host [R][64] */);
 
+/* N2 fusions of the single-GPU tcgen05 path, a bitmask of moe_fusion_t;
+   default MOE_FUSE_COMBINE (GATHER is opt-in: on B200 the TMA gather4 stream is slower than
+   the dispatch copy it replaces).  Results are bitwise identical with and
+   without them (same products, same accumulation order).
+   MOE_FUSE_GATHER: the expert GEMMs that read x rows (H = relu(X W1^T + b1) and
+     dW1 = dA^T X) load them straight from the caller's x by TMA gather4 through
+     token_of_slot, so the dispatch step (GroupBy) writes only the routing tables and
+     no X buffer is materialised.  Applies when world_size == 1 (no EP), dtype bf16, d and f
+     multiples of 128 and x 16-byte aligned; else the X buffer path runs.  x must stay
+     unchanged until moe_backward has been enqueued (already required above).
+   MOE_FUSE_COMBINE (k == 1, world_size == 1, bf16, no cached indices, no AggregateSpec
+     outputs, d_out a multiple of 128): the second expert GEMM's epilogue writes y[t] = w[t] O[row]
+     (Alg. 1 l.8) next to O and the dispatch zeroes the y rows of dropped tokens, so no
+     separate combine pass re-reads O.  Takes effect at the next moe_forward. */
+typedef enum { MOE_FUSE_GATHER = 1, MOE_FUSE_COMBINE = 2 } moe_fusion_t;
+MOE_API moe_status_t moe_set_fusion(moe_handle_t h, int32_t flags);
+
 /* Number of kernels the library launched since the handle was created (for bench
    accounting of "our kernels in the timed region"). */
 MOE_API moe_status_t moe_launch_count(moe_handle_t h, int64_t* out);

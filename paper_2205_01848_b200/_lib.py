@@ -89,6 +89,7 @@ EXPORTS = {
     "moe_get_stats_async": ([C.c_void_p, C.POINTER(Stats)], C.c_int),
     "moe_check_device_flags": ([C.c_void_p, C.POINTER(C.c_int32)], C.c_int),
     "moe_launch_count": ([C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
+    "moe_set_fusion": ([C.c_void_p, C.c_int32], C.c_int),
     "moe_last_error": ([C.c_void_p], C.c_char_p),
     "moe_profile_enable": ([C.c_void_p, C.c_int32], C.c_int),
     "moe_profile_read": ([C.c_void_p, C.POINTER(KernelTime), C.c_int32, C.POINTER(C.c_int32),

@@ -441,6 +441,11 @@ static bool use_2cta(int N, int kind) {
 
 void tc_plan_free(TcPlan* p) { (void)p; }
 
+bool tc_gather_supported(int d, int f) {
+  return use_2cta(f, TC_FWD1) && use_2cta(d, TC_WGRAD) && d % 64 == 0;
+}
+bool tc_combine_supported(int dout) { return use_2cta(dout, TC_FWD2); }
+
 // db[e][c] = sum of the DGRAD_A column-sum partials of expert e, fixed order (deterministic).
 __global__ void bias_part_reduce_kernel(const float* __restrict__ part,
                                         const int32_t* __restrict__ kept, int N,
@@ -486,11 +491,18 @@ template <int KIND>
 static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, int N,
                            int n_local, const void* bias, void* C, int ldc, const int32_t* kept,
                            const int32_t* prefix, const CapTable& ct, cudaStream_t s,
-                           uint32_t* mask = nullptr, float* bias_part = nullptr) {
+                           uint32_t* mask = nullptr, float* bias_part = nullptr,
+                           const TcFusion* fz = nullptr) {
   CUtensorMap ma, mb;
   const int bn = pick_bn(N);
   const bool two = use_2cta(N, KIND);
-  TC_TRY(make_map(&ma, A, K, rows, 64, 128));
+  const bool gat = KIND == TC_FWD1 && fz && fz->x;        // A rows gathered from x (N2)
+  const bool comb = KIND == TC_FWD2 && fz && fz->y;       // fused combine (N2, k = 1)
+  if ((gat || comb) && !two) return MOE_ERR_CONFIG;
+  if (gat)
+    TC_TRY(make_map(&ma, fz->x, K, (uint64_t)fz->T, 64, 1));
+  else
+    TC_TRY(make_map(&ma, A, K, rows, 64, 128));
   if (KindTraits<KIND>::b_mn)
     TC_TRY(make_map(&mb, B, N, (uint64_t)n_local * K, 64, 64));
   else
@@ -500,6 +512,16 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   p.bias = (const __nv_bfloat16*)bias; p.C = (__nv_bfloat16*)C; p.ldc = ldc; p.ct = ct;
   p.mask = mask;
   p.bias_part = two ? bias_part : nullptr;
+  if (gat || comb) {
+    p.gtos = fz->tos;
+    p.gk = fz->k;
+    p.grows = fz->T;
+  }
+  if (!gat) p.gtos = comb ? fz->tos : nullptr;
+  if (comb) {
+    p.y = (__nv_bfloat16*)fz->y;
+    p.wt = fz->w;
+  }
   p.sched = tc_sched();
   p.pf_kb = tc_pf();
   p.dbg = tc_dbg();
@@ -516,14 +538,25 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
 // WGRAD: Out_e[M x N] (+)= A_e^T B_e, A = Abuf[rows x M], B = Bbuf[rows x N] over kept_e rows.
 static moe_status_t wgrad(const void* Abuf, int M, const void* Bbuf, int N, int64_t rows,
                           int n_local, void* Out, void* bias_out, int accumulate,
-                          const int32_t* kept, const CapTable& ct, cudaStream_t s) {
+                          const int32_t* kept, const CapTable& ct, cudaStream_t s,
+                          const TcFusion* fz = nullptr) {
   CUtensorMap ma, mb;
+  const bool gat = fz && fz->x;   // B rows (tokens) gathered from x (N2)
+  if (gat && !use_2cta(N, TC_WGRAD)) return MOE_ERR_CONFIG;
   TC_TRY(make_map(&ma, Abuf, M, rows, 64, 64));
-  TC_TRY(make_map(&mb, Bbuf, N, rows, 64, 64));
+  if (gat)
+    TC_TRY(make_map(&mb, fz->x, N, (uint64_t)fz->T, 64, 1));
+  else
+    TC_TRY(make_map(&mb, Bbuf, N, rows, 64, 64));
   TcParams p{};
   p.kept = kept; p.mtile_prefix = nullptr; p.n_local = n_local; p.M = M; p.N = N; p.K = 0;
   p.C = (__nv_bfloat16*)Out; p.bias_out = (__nv_bfloat16*)bias_out; p.accumulate = accumulate;
   p.ct = ct;
+  if (gat) {
+    p.gtos = fz->tos;
+    p.gk = fz->k;
+    p.grows = fz->T;
+  }
   p.sched = tc_sched();
   p.pf_kb = tc_pf();
   p.dbg = tc_dbg();
@@ -542,19 +575,21 @@ moe_status_t tc_ffn_forward(TcPlan* plan, void* X, const void* w1, const void* b
                             int d, int f, int dout, const int32_t* kept,
                             const int32_t* mtile_prefix, int n_local, const CapTable& ct,
                             int max_cap, cudaStream_t s, int64_t* nlaunch, Prof* prof,
-                            uint32_t* mask) {
+                            uint32_t* mask, const TcFusion* fz) {
   (void)plan; (void)max_cap;
   if (!ensure_encode()) return MOE_ERR_CUDA;
   if (rows == 0 || n_local == 0) { *nlaunch = 0; return MOE_OK; }
   moe_status_t st;
   {
     ProfScope ps(prof, "ffn_gemm1", s);
-    st = mgroup<TC_FWD1>(X, rows, d, w1, f, n_local, b1, H, f, kept, mtile_prefix, ct, s, mask);
+    st = mgroup<TC_FWD1>(X, rows, d, w1, f, n_local, b1, H, f, kept, mtile_prefix, ct, s, mask,
+                         nullptr, fz);
   }
   if (st != MOE_OK) return st;
   {
     ProfScope ps(prof, "ffn_gemm2", s);
-    st = mgroup<TC_FWD2>(H, rows, f, w2, dout, n_local, b2, O, dout, kept, mtile_prefix, ct, s);
+    st = mgroup<TC_FWD2>(H, rows, f, w2, dout, n_local, b2, O, dout, kept, mtile_prefix, ct, s,
+                         nullptr, nullptr, fz);
   }
   *nlaunch = 2;
   return st;
@@ -565,7 +600,8 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
                              int accumulate, int64_t rows, int d, int f, int dout,
                              const int32_t* kept, const int32_t* mtile_prefix, int n_local,
                              const CapTable& ct, int max_cap, cudaStream_t s,
-                             int64_t* nlaunch, Prof* prof, uint32_t* mask, float* bias_part) {
+                             int64_t* nlaunch, Prof* prof, uint32_t* mask, float* bias_part,
+                             const TcFusion* fz) {
   (void)plan; (void)max_cap;
   // db1 from the DGRAD_A epilogue (2-CTA) instead of the weight-gradient bias warps
   const bool db1_in_dgrad = db1 && bias_part && use_2cta(f, TC_DGRAD_A);
@@ -600,7 +636,8 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   }
   if (dw1) {  // dW1_e = dA_e^T X_e (db1 fused here only when not produced by DGRAD_A)
     ProfScope ps(prof, "wgrad_w1", s);
-    st = wgrad(H, f, X, d, rows, n_local, dw1, db1_in_dgrad ? nullptr : db1, accumulate, kept, ct, s);
+    st = wgrad(H, f, X, d, rows, n_local, dw1, db1_in_dgrad ? nullptr : db1, accumulate, kept, ct, s,
+               fz);
     if (st != MOE_OK) return st;
     ++nl;
   } else if (db1 && !db1_in_dgrad) {

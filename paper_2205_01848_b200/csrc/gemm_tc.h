@@ -15,13 +15,27 @@ struct TcPlan {
 };
 void tc_plan_free(TcPlan* p);
 
+// N2 fusions of the single-GPU path: the expert GEMMs read the x rows of each
+// expert slot straight from x (TMA gather4 by token_of_slot) instead of a dispatched X buffer,
+// and (k = 1) the second forward GEMM writes y = w * O next to O instead of a combine pass.
+struct TcFusion {
+  const void* x = nullptr;        // x [T, d]; null = no gather (X buffer is used)
+  int T = 0;
+  const int32_t* tos = nullptr;   // token_of_slot by expert-region row (t * k + r)
+  int k = 1;
+  void* y = nullptr;              // y [T, d_out]; null = separate combine kernel
+  const float* w = nullptr;       // gate weights [T] (k = 1)
+};
+bool tc_gather_supported(int d, int f);     // 2-CTA kernels for FWD1 (N = f) and WGRAD_W1 (N = d)
+bool tc_combine_supported(int dout);        // 2-CTA kernel for FWD2 (N = d_out)
+
 // Forward: H = relu(X W1_e^T + b1_e), O = H W2_e^T + b2_e over kept_e rows per local expert.
 moe_status_t tc_ffn_forward(TcPlan* p, void* X, const void* w1, const void* b1,
                             const void* w2, const void* b2, void* H, void* O, int64_t rows,
                             int d, int f, int dout, const int32_t* kept,
                             const int32_t* mtile_prefix, int n_local, const CapTable& ct,
                             int max_cap, cudaStream_t s, int64_t* nlaunch, Prof* prof,
-                            uint32_t* mask);
+                            uint32_t* mask, const TcFusion* fz = nullptr);
 // Backward: dW2 = dO^T H, db2 = sum dO; dA = (dO W2) * 1[H>0] (into H);
 // dW1 = dA^T X, db1 = sum dA; dX = dA W1.
 moe_status_t tc_ffn_backward(TcPlan* p, void* X, void* H, void* dO, void* dX, const void* w1,
@@ -29,6 +43,7 @@ moe_status_t tc_ffn_backward(TcPlan* p, void* X, void* H, void* dO, void* dX, co
                              int accumulate, int64_t rows, int d, int f, int dout,
                              const int32_t* kept, const int32_t* mtile_prefix, int n_local,
                              const CapTable& ct, int max_cap, cudaStream_t s,
-                             int64_t* nlaunch, Prof* prof, uint32_t* mask, float* bias_part);
+                             int64_t* nlaunch, Prof* prof, uint32_t* mask, float* bias_part,
+                             const TcFusion* fz = nullptr);
 
 }  // namespace moe

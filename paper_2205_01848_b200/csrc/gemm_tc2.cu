@@ -56,6 +56,31 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
       : "memory");
 }
+// 4 rows (r0..r3) x box-width columns starting at column c0, into 4 consecutive 128-byte rows
+// of shared memory (swizzled like rows of a tile box); bytes land on the leader's barrier.
+__device__ __forceinline__ void tma_gather4_2sm(uint32_t dst, const CUtensorMap* map,
+                                                uint32_t bar_cluster, int c0, int4 r) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4"
+      ".mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w),
+      "r"(bar_cluster)
+      : "memory");
+}
+// x rows of expert slots [s0, s0 + 4) (slot s of the region at `base`): token_of_slot / k, or
+// `oob` (zero fill) for slots >= kept.  base and s0 are multiples of 4 (16-byte load).
+__device__ __forceinline__ int4 gather_rows4(const int32_t* tos, int base, int s0, int kept,
+                                             int k, int oob) {
+  int4 v = make_int4(oob, oob, oob, oob);
+  if (s0 < kept) {
+    v = __ldg(reinterpret_cast<const int4*>(tos + base + s0));
+    if (k != 1) { v.x /= k; v.y /= k; v.z /= k; v.w /= k; }
+    if (s0 + 1 >= kept) v.y = oob;
+    if (s0 + 2 >= kept) v.z = oob;
+    if (s0 + 3 >= kept) v.w = oob;
+  }
+  return v;
+}
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -185,7 +210,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   const bool nfast = p.sched == 1;
 
   if (warp == 0) {
-    if (lane == 0) {
+    if ((KIND == TC_FWD1 || KIND == TC_WGRAD) && p.gtos != nullptr) {
+      // ================ TMA producer with x-row gathers (N2, both CTAs, whole warp) ================
+      // FWD1: lane l gathers A rows [4l, 4l+4) of this CTA's 128 rows (the same rows for every
+      // k-block of the tile).  WGRAD: the B tile is 64 token rows x BNH columns in two 64-column
+      // boxes; lane l gathers token rows [4(l%16), +4) of box l/16, indices one k-block ahead.
+      int stage = 0;
+      uint32_t phase = 0;
+      const int sub = KIND == TC_FWD1 ? lane : (lane & 15);
+      for (int t = t_begin; t < t_end; t += t_step) {
+        int e, mt, nt;
+        if (!decode_tile_ord<Tr::kgroup>(t, s_prefix, n_local, MT, NT, nfast, e, mt, nt)) break;
+        const int m0 = mt * TC2_M + (int)crank * TC_BM;
+        const int n0 = nt * BN + (int)crank * BNH;
+        const int base = p.ct.base[e];
+        const int kept = p.kept[e];
+        const int nk = Tr::kgroup ? (kept + TC_BK - 1) / TC_BK : p.K / TC_BK;
+        int4 rows = make_int4(0, 0, 0, 0), nxt = rows;
+        if (KIND == TC_FWD1) rows = gather_rows4(p.gtos, base, m0 + 4 * sub, kept, p.gk, p.grows);
+        else nxt = gather_rows4(p.gtos, base, 4 * sub, kept, p.gk, p.grows);
+        for (int kb = 0; kb < nk; ++kb) {
+          if (KIND == TC_WGRAD) {
+            rows = nxt;
+            if (kb + 1 < nk)
+              nxt = gather_rows4(p.gtos, base, (kb + 1) * TC_BK + 4 * sub, kept, p.gk, p.grows);
+          }
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (fuse_bias) mbar_wait(&bias_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          const uint32_t fb = mapa_rank(smem_u32(&full_bar[stage]), 0);
+          const int k0 = kb * TC_BK;
+          if (lane == 0) {
+            if (leader) mbar_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
+            if (KIND == TC_FWD1) {  // B = W1_e rows [n0, n0 + BNH), K-major
+              tma_load_2d_2sm(sb, &tmB, fb, k0, e * p.N + n0);
+            } else {                // A = dA^T tile, MN-major, two 64-column boxes
+              tma_load_2d_2sm(sa, &tmA, fb, m0, base + k0);
+              tma_load_2d_2sm(sa + 8192, &tmA, fb, m0 + 64, base + k0);
+            }
+          }
+          __syncwarp();
+          if (KIND == TC_FWD1)
+            tma_gather4_2sm(smem_u32(sa) + lane * 512, &tmA, fb, k0, rows);
+          else if ((lane >> 4) < BNH / 64)
+            tma_gather4_2sm(smem_u32(sb) + (lane >> 4) * 8192 + sub * 512, &tmB, fb,
+                            n0 + (lane >> 4) * 64, rows);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    } else if (lane == 0) {
       // ============================ TMA producer (both CTAs) ============================
       int stage = 0;
       uint32_t phase = 0;
@@ -377,6 +451,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int cc = 0; cc < CH; ++cc) mbits[cc] = mrow[(n0 >> 5) + half * CH + cc];
       }
+      // N2 combine fusion (k = 1): this row's token and gate weight
+      int ytok = -1;
+      float yw = 0.f;
+      if (KIND == TC_FWD2 && p.y != nullptr && row_ok) {
+        ytok = p.gtos[p.ct.base[e] + row];
+        yw = p.wt[ytok];
+      }
       const bool need_side = ((KIND == TC_FWD1 || KIND == TC_FWD2) && row_ok) ||
                              (KIND == TC_WGRAD && row_ok && p.accumulate);
       if (need_side) {
@@ -501,6 +582,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           if (lane == 0)
             tma_store_2d(&tmC, stg, col0,
                          Tr::kgroup ? e * p.M + blk_row : p.ct.base[e] + blk_row);
+          if (KIND == TC_FWD2 && ytok >= 0) {
+            // Alg. 1 l.8 for k = 1: y[t] = 0 + w O[row] from the stored (bf16) O, the same
+            // arithmetic as the combine kernel (bitwise equal)
+            __nv_bfloat16* yrow = p.y + (size_t)ytok * p.N + col0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float o[8];
+              unpack(pk[i], o, __nv_bfloat16());
+#pragma unroll
+              for (int j = 0; j < 8; ++j) o[j] = fmaf(yw, o[j], 0.f);
+              st_v4(yrow + 8 * i, pack(o, __nv_bfloat16()));
+            }
+          }
           if (KIND == TC_FWD1) {  // bit j: the stored bf16 H is > 0 (relu output >= 0)
             uint32_t bits = 0;
 #pragma unroll

@@ -31,6 +31,16 @@ struct TcParams {
   int sched;                    // 2-CTA tile schedule: 0 round-robin (m fastest),
                                 // 1 contiguous chunk per CTA pair (n fastest), 2 chunk (m fastest)
   int dbg;                      // timing experiments (MOE_TC_DBG), 0 in production
+  // N2 gather fusion (2-CTA only).  gtos != null: the x rows of expert slot (base_e + s) are
+  // loaded by TMA tile::gather4 straight from x (row token_of_slot / gk) instead of from a
+  // dispatched X buffer -- FWD1: the A operand, WGRAD: the B operand (token rows).  Slots
+  // s >= kept_e use row grows (= T, out of bounds: TMA fills zeros).
+  const int32_t* gtos;
+  int gk;
+  int grows;
+  // N2 combine fusion (FWD2, k = 1): y[t] = w[t] * O[row] written by the epilogue next to O.
+  __nv_bfloat16* y;
+  const float* wt;
   CapTable ct;                  // base rows of each local expert region
 };
 

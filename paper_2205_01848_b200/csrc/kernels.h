@@ -58,7 +58,8 @@ cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T,
                             int n, int d, int64_t token_base, const CapTable& ct,
                             RouteBufs b, void* xbuf, const int32_t* pad_kept, cudaStream_t s,
                             int pad_e0 = 0, const PeerBufs& px = PeerBufs{},
-                            const PeerBufs& ptos = PeerBufs{}, const int32_t* pre_dev = nullptr);
+                            const PeerBufs& ptos = PeerBufs{}, const int32_t* pre_dev = nullptr,
+                            void* y_zero = nullptr, int dout = 0);
 cudaError_t launch_zero_pad(int dtype, void* buf, int cols, const int32_t* kept, int n,
                             const CapTable& ct, cudaStream_t s);
 cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, int k,

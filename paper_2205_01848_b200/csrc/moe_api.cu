@@ -56,6 +56,8 @@ struct moe_ctx {
   moe_fwd_args_t fa{};
   int64_t launches = 0;
   int use_tc = 0;             // tcgen05 path for bf16 (env MOE_FORCE_SIMT=1 disables)
+  int fusion = MOE_FUSE_COMBINE;  // N2 fusions allowed (moe_set_fusion; GATHER is opt-in)
+  int fused_gather = 0;       // the last forward gathered x rows in the GEMMs (no X buffer)
   TcPlan tc{};
   Prof prof;
   float balance_lambda = 0.f; // Eq. 3 balance term weight (0 = off)
@@ -456,6 +458,26 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   const bool cached = h->cached != nullptr || (tab && !fallback);
   const int32_t* cidx = tab ? rb.idx : h->cached;   // what the gate compares/weights against
   h->last_cached = cached || fallback;
+  // N2 (single GPU, tcgen05 path).  GATHER: the expert GEMMs gather x rows by
+  // token_of_slot (no X buffer; the dispatch writes only the routing tables).  COMBINE: with
+  // k = 1 and the gate weights known before the experts (not cached), FWD2's epilogue also
+  // writes y (no combine pass re-reading O).
+  const bool tc1 = h->use_tc && !h->use_ep && T > 0;
+  const bool gather = tc1 && (h->fusion & MOE_FUSE_GATHER) && ((uintptr_t)a->x % 16) == 0 &&
+                      tc_gather_supported(d, f);
+  const bool fcomb = tc1 && (h->fusion & MOE_FUSE_COMBINE) && k == 1 && !cached &&
+                     h->spec == nullptr && ((uintptr_t)a->y % 16) == 0 &&
+                     tc_combine_supported(dout);
+  h->fused_gather = gather;
+  TcFusion fz;
+  fz.T = T;
+  fz.tos = rb.token_of_slot;
+  fz.k = k;
+  if (gather) fz.x = a->x;
+  if (fcomb) {
+    fz.y = a->y;
+    fz.w = rb.w;
+  }
   CUDA_TRY(h, cudaMemsetAsync(rb.hit_count, 0, 4, s0));
   if (tab)  // idx[t] = table[sample_ids[t]] (before the fork: the side stream reads it)
     KL(h, T > 0, "cache_gather", s0, launch_cache_gather(h->ctab, h->ctab_num, k, h->cids, T,
@@ -492,7 +514,10 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   KL(h, T > 0, "route_hist", sd, launch_route_hist(rb.idx, T, k, n, rb.tile_hist, sd));
   KL(h, 1, "route_scan", sd, launch_route_scan(rb.tile_hist, ntiles, n, h->ct, rb, sd));
   if (!h->use_ep) {
-    KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->cts, rb, X, rb.kept, sd));
+    KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->cts, rb,
+                                                 gather ? nullptr : X, gather ? nullptr : rb.kept,
+                                                 sd, 0, PeerBufs{}, PeerBufs{}, nullptr,
+                                                 fcomb ? a->y : nullptr, dout));
   } else if (h->use_peer) {
     // N1: counts exchange + global plan on the device, then the dispatch stores every kept
     // row straight into its owner's X buffer; the barrier publishes "X rows landed".
@@ -542,7 +567,8 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     int64_t nk = 0;
     moe_status_t st = tc_ffn_forward(&h->tc, X, w1, b1, w2, b2, H, O, h->rows, d, f, dout,
                                      kept_local, rb.mtile_prefix, nl, h->ct, h->max_cap_local,
-                                     sd, &nk, &h->prof, (uint32_t*)(ws + h->L.mask));
+                                     sd, &nk, &h->prof, (uint32_t*)(ws + h->L.mask),
+                                     (gather || fcomb) ? &fz : nullptr);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 forward failed");
   } else {
@@ -594,7 +620,8 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   }
   rb.spec = h->spec;
   rb.spec_valid = h->spec_valid;
-  KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O_tok, rb, T, k, dout, h->cts, a->y, s0, po));
+  if (!fcomb)
+    KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O_tok, rb, T, k, dout, h->cts, a->y, s0, po));
   rb.spec = nullptr;
   rb.spec_valid = nullptr;
   if (!h->mq.empty()) {  // push this iteration's metric futures (App. B)
@@ -675,10 +702,18 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   char* db2 = a->db2 ? (char*)a->db2 + (size_t)h->e_lo * dout * h->s : nullptr;
   if (h->use_tc) {
     int64_t nk = 0;
+    TcFusion fz;  // N2: dW1 = dA^T X gathers the x rows like the forward did
+    if (h->fused_gather) {
+      fz.x = fa.x;
+      fz.T = T;
+      fz.tos = rb.token_of_slot;
+      fz.k = k;
+    }
     moe_status_t st = tc_ffn_backward(&h->tc, X, H, dO, dXb, w1, w2, dw1, db1, dw2, db2, acc,
                                       h->rows, d, f, dout, kept_local, rb.mtile_prefix, nl,
                                       h->ct, h->max_cap_local, s0, &nk, &h->prof,
-                                      (uint32_t*)(ws + h->L.mask), (float*)(ws + h->L.bpart));
+                                      (uint32_t*)(ws + h->L.mask), (float*)(ws + h->L.bpart),
+                                      h->fused_gather ? &fz : nullptr);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 backward failed");
   } else {
@@ -988,6 +1023,14 @@ moe_status_t moe_set_spec_grads(moe_handle_t h, const void* dspec, const float* 
 
 moe_status_t moe_vcomm_create(int32_t R, void** comm_out) { return vcomm_create(R, comm_out); }
 moe_status_t moe_vcomm_destroy(void* comm) { return vcomm_destroy(comm); }
+
+moe_status_t moe_set_fusion(moe_handle_t h, int32_t flags) {
+  if (!h) return MOE_ERR_INVALID_ARG;
+  if (flags & ~(MOE_FUSE_GATHER | MOE_FUSE_COMBINE))
+    return fail(h, MOE_ERR_INVALID_ARG, "unknown fusion flag");
+  h->fusion = flags;
+  return MOE_OK;
+}
 
 moe_status_t moe_launch_count(moe_handle_t h, int64_t* out) {
   if (!h || !out) return MOE_ERR_INVALID_ARG;

@@ -320,9 +320,12 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
     long long token_base, CapTable ct, const int32_t* __restrict__ tile_off,
     int32_t* __restrict__ slot_of, int32_t* __restrict__ token_of_slot, T* __restrict__ xbuf,
     const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs px, PeerBufs ptos,
-    const int32_t* __restrict__ pre_dev) {
+    const int32_t* __restrict__ pre_dev, T* __restrict__ yz, int dout) {
   // px.nl != 0 (peer EP, N1): rows go straight into the owners' X buffers over NVLink, the
   // global slot offsets come from the device plan (pre_dev), token_of_slot is the owner's.
+  // xbuf == null (N2 gather fusion): only the routing tables are written -- the expert GEMMs
+  // gather the x rows themselves; yz != null (N2 fused combine): y rows of tokens with every
+  // pair dropped are zeroed here (the GEMM epilogue writes the others).
   __shared__ uint32_t masks[MOE_MAX_E][MOE_ROUTE_TILE / 32];
   if (pad_kept)
     zero_pads_block(xbuf, d, pad_kept, ct, px.nl ? px.nl : n, pad_e0, blockIdx.x, gridDim.x);
@@ -385,11 +388,17 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
       dsts[r] = nullptr;
       if (r < k) {
         const int rw = srow[lt2 * k + r];
-        if (rw >= 0) dsts[r] = peer_row(xbuf, px, sexp[lt2 * k + r], (size_t)rw, d);
+        if (rw >= 0) {
+          any = true;
+          if (xbuf) dsts[r] = peer_row(xbuf, px, sexp[lt2 * k + r], (size_t)rw, d);
+        }
       }
-      any |= dsts[r] != nullptr;
     }
-    if (!any) continue;
+    if (!any && yz) {  // all pairs dropped: y[t] = 0
+      for (int v = lane; v < dout / VE; v += 32)
+        st_v4(yz + (size_t)tt * dout + (size_t)v * VE, make_uint4(0, 0, 0, 0));
+    }
+    if (!any || !xbuf) continue;
     const T* src = x + (size_t)tt * d;
     for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
       uint4 buf[4];
@@ -416,18 +425,20 @@ cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T,
                             int n, int d, int64_t token_base, const CapTable& ct,
                             RouteBufs b, void* xbuf, const int32_t* pad_kept, cudaStream_t s,
                             int pad_e0, const PeerBufs& px, const PeerBufs& ptos,
-                            const int32_t* pre_dev) {
+                            const int32_t* pre_dev, void* y_zero, int dout) {
   if (T == 0 && !(pad_kept && px.nl)) return cudaSuccess;  // peer EP: own pads still zeroed
   int ntiles = std::max(1, (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE);
   if (dtype == 1)
     dispatch_kernel<__nv_bfloat16><<<ntiles, 256, 0, s>>>(
         idx, (const __nv_bfloat16*)x, T, k, n, d, token_base, ct, b.tile_off, b.slot_of,
-        b.token_of_slot, (__nv_bfloat16*)xbuf, pad_kept, pad_e0, px, ptos, pre_dev);
+        b.token_of_slot, (__nv_bfloat16*)xbuf, pad_kept, pad_e0, px, ptos, pre_dev,
+        (__nv_bfloat16*)y_zero, dout);
   else
     dispatch_kernel<float><<<ntiles, 256, 0, s>>>(idx, (const float*)x, T, k, n, d,
                                                   token_base, ct, b.tile_off, b.slot_of,
                                                   b.token_of_slot, (float*)xbuf, pad_kept,
-                                                  pad_e0, px, ptos, pre_dev);
+                                                  pad_e0, px, ptos, pre_dev, (float*)y_zero,
+                                                  dout);
   return cudaGetLastError();
 }
 

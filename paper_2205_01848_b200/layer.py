@@ -163,6 +163,14 @@ class MoELayer:
             self._ctab_ref = None
             L.check(self.lib.moe_set_assignment_cache(self.h, None, 0, None, 0), self.h)
 
+    # -- N2 fusions ---------------------------------------------------------------------
+    FUSE_GATHER, FUSE_COMBINE = 1, 2
+
+    def set_fusion(self, flags: int):
+        """moe_set_fusion: bitmask of FUSE_GATHER (x rows gathered by the expert GEMMs, no X
+        buffer) and FUSE_COMBINE (k = 1: y written by the second GEMM's epilogue)."""
+        L.check(self.lib.moe_set_fusion(self.h, int(flags)), self.h)
+
     # -- loss variants (N3) -----------------------------------------------------------
     def set_balance_loss(self, lam: float):
         """Eq. 3 balance term weight (0 = off); the backward then includes dB/dl."""

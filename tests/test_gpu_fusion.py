@@ -1,0 +1,133 @@
+"""N2 fusions (moe_set_fusion): the expert GEMMs gather x rows by
+token_of_slot with TMA gather4 (no dispatched X buffer; opt-in) and, for k = 1, the second GEMM's
+epilogue writes y = w O (no combine pass).  Checked two ways on the same seeded inputs:
+against the fp64 oracle (values within the bf16 budget, routing bit-exact), and against the
+unfused path of the same library, which must be BITWISE equal (same products, same
+accumulation order) -- including at the bench's full c3 size."""
+import numpy as np
+import pytest
+import torch
+
+from parity_util import assert_routing_exact, assert_values, run_pair
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(layer, g, dy, fusion, y_fill=None):
+    layer.set_fusion(fusion)
+    y = None
+    if y_fill is not None:   # poison y: every row must be written (dropped tokens -> 0)
+        y = torch.full((g["x"].shape[0], layer.d_out), y_fill, dtype=layer.tdtype,
+                       device=layer.device)
+    y = layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"], y=y)
+    grads = layer.backward(dy)
+    torch.cuda.synchronize()
+    return y.clone(), {k: v.clone() for k, v in grads.items()}
+
+
+def _bitwise(a, b, what):
+    assert a.dtype == b.dtype and a.shape == b.shape
+    ai = a.view(torch.int16) if a.dtype == torch.bfloat16 else a.view(torch.int32)
+    bi = b.view(torch.int16) if b.dtype == torch.bfloat16 else b.view(torch.int32)
+    nbad = int((ai != bi).sum())
+    assert nbad == 0, f"{what}: {nbad} elements differ between fused and unfused paths"
+
+
+CASES = [  # n, k, d, f, T, renorm, regime, alpha
+    (8, 1, 256, 512, 1000, 0, "uniform", 1.0),    # gather + fused combine, drops
+    (8, 1, 256, 512, 1001, 1, "uniform", 1.25),   # renorm (w = 1), ragged T
+    (8, 2, 256, 384, 777, 1, "uniform", 1.0),     # k = 2: gather only
+    (16, 1, 128, 256, 1500, 0, "skewed", 1.0),    # heavy drops: y rows of dropped tokens = 0
+    (4, 1, 128, 128, 3, 0, "uniform", 1.0),       # T < 4 (gather rows past T are OOB)
+]
+
+
+@pytest.mark.parametrize("fusion", [2, 3])
+@pytest.mark.parametrize("n,k,d,f,T,renorm,regime,alpha", CASES)
+def test_fused_vs_oracle(n, k, d, f, T, renorm, regime, alpha, fusion):
+    from paper_2205_01848_b200 import capacity_from_factors
+    caps = capacity_from_factors([alpha] * n, T, k)
+    from paper_2205_01848_b200 import MoELayer
+    layer = MoELayer(n, k, d, f, 0, T, "bf16", renorm, device="cuda")
+    layer.set_fusion(fusion)
+    layer, gpu, st, gr, own = run_pair(n, k, d, f, T, "bf16", caps, renorm=renorm,
+                                       regime=regime, layer=layer)
+    assert_routing_exact(gpu, st, k)
+    assert_values(gpu, st, gr, own, "bf16")
+    if regime == "skewed":
+        assert st.routing.drops > 0
+
+
+@pytest.mark.parametrize("n,k,d,f,T,renorm,regime,alpha", CASES)
+def test_fused_bitwise_equals_unfused(n, k, d, f, T, renorm, regime, alpha):
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer
+    g = {kk: v.cuda() for kk, v in make_layer(n, d, f, d, T, "bf16", regime).items()}
+    dy = make_dy(T, d, "bf16").cuda()
+    layer = MoELayer(n, k, d, f, 0, T, "bf16", renorm, device="cuda")
+    layer.set_capacities(capacity_from_factors([alpha] * n, T, k))
+    y0, g0 = _run(layer, g, dy, 0, y_fill=float("nan"))
+    assert not torch.isnan(y0).any()
+    for fusion in (2, 1, 3):   # combine only, gather only, both
+        y1, g1 = _run(layer, g, dy, fusion, y_fill=float("nan"))
+        assert not torch.isnan(y1).any()
+        _bitwise(y1, y0, f"y (fusion {fusion})")
+        for key in g0:
+            _bitwise(g1[key], g0[key], f"{key} (fusion {fusion})")
+
+
+def test_fused_cached_mode_bitwise():
+    """Cached indices: the gate runs concurrently with the experts, so only the gather is
+    fused (the combine waits for the gate weights); results equal the unfused path."""
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer
+    n, k, d, f, T = 8, 1, 256, 256, 999
+    g = {kk: v.cuda() for kk, v in make_layer(n, d, f, d, T, "bf16").items()}
+    dy = make_dy(T, d, "bf16").cuda()
+    gen = torch.Generator(device="cpu").manual_seed(5)
+    cidx = torch.randint(0, n, (T, k), generator=gen, dtype=torch.int32).cuda()
+    layer = MoELayer(n, k, d, f, 0, T, "bf16", 0, device="cuda")
+    layer.set_capacities(capacity_from_factors([1.0] * n, T, k))
+    layer.set_cached_assignment(cidx)
+    y0, g0 = _run(layer, g, dy, 0)
+    y1, g1 = _run(layer, g, dy, 3)
+    _bitwise(y1, y0, "y")
+    for key in g0:
+        _bitwise(g1[key], g0[key], key)
+
+
+def test_fused_bitwise_at_bench_size():
+    """c3 (the bench workload: 64 experts, top-1, d 1024, f 4096, 65,536 tokens, alpha 1) in
+    the launch configuration bench.py times: fused == unfused bitwise, and sampled tokens
+    of y equal the plain fp32 definition within the bf16 budget."""
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer
+    n, k, d, f, T = 64, 1, 1024, 4096, 65536
+    g = make_layer(n, d, f, d, T, "bf16", device="cuda")
+    dy = make_dy(T, d, "bf16", device="cuda")
+    layer = MoELayer(n, k, d, f, 0, T, "bf16", 0, device="cuda")
+    layer.set_capacities(capacity_from_factors([1.0] * n, T, k))
+    y0, g0 = _run(layer, g, dy, 0)
+    for fusion in (3, 2):   # end with the default (combine only) for the sampled check
+        y1, g1 = _run(layer, g, dy, fusion, y_fill=float("nan"))
+        _bitwise(y1, y0, f"y (fusion {fusion})")
+        for key in g0:
+            _bitwise(g1[key], g0[key], f"{key} (fusion {fusion})")
+    # sampled tokens against the definition (fp32 from the same bf16 inputs)
+    r = layer.routing(T)
+    idx = r["idx"][:, 0].long()
+    slot = r["slot_of"][:, 0].long()
+    w = r["w"][:, 0]
+    rng = np.random.default_rng(0)
+    for t in rng.choice(T, 48, replace=False).tolist():
+        if slot[t] < 0:
+            assert y1[t].abs().max().item() == 0.0
+            continue
+        e = int(idx[t])
+        xt = g["x"][t].float()
+        h = torch.relu(xt @ g["w1"][e].float().T + g["b1"][e].float())
+        h = h.bfloat16().float()
+        o = (h @ g["w2"][e].float().T + g["b2"][e].float()).bfloat16().float()
+        ref = float(w[t]) * o
+        err = (y1[t].float() - ref).abs().max() / ref.abs().max()
+        assert err < 2e-2, (t, float(err))

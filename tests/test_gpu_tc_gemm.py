@@ -13,6 +13,7 @@ def test_tc_forward_buffers(n, k, d, f, T):
     from synth import make_layer
     g = {kk: v.cuda() for kk, v in make_layer(n, d, f, d, T, "bf16").items()}
     layer = MoELayer(n, k, d, f, 0, T, "bf16", 1, device="cuda")
+    layer.set_fusion(0)   # this test inspects the dispatched X buffer (N2 gathers x instead)
     layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
     torch.cuda.synchronize()
     r = layer.routing(T)
