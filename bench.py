@@ -305,8 +305,8 @@ def run_ours(args):
         return float(t.item())
 
     # ---------------- timed region (device events on the launching stream) ----------------
-    layer.profile(True)
-    layer.profile_read(reset=True)
+    # The headline runs with the library's per-kernel events OFF; a second pass of the same
+    # K steps with them on gives the per-kernel table (roofline) below.
     l0 = layer.launch_count()
     clk = ClockSampler(local, dev)
     barrier()
@@ -321,11 +321,29 @@ def run_ours(args):
     clocks = clk.stop()
     barrier()
     launches = layer.launch_count() - l0
-    ktimes = layer.profile_read(reset=True)
-    layer.profile(False)
+    _, dev_flags = layer.check_flags()   # NaN logits / peer-barrier timeout: the run is invalid
+    if dev_flags:
+        print(f"bench: device error flags {dev_flags} raised in the timed region", file=sys.stderr)
     ms = max_over_ranks(ms)
     ms_step = ms / args.steps
     value = T * ws * args.steps / (ms / 1e3)
+
+    # same starting power state as the headline pass: the B200 drops from 1965 MHz to ~1.25 GHz
+    # within ~0.1 s of sustained expert-GEMM load (sw_power_cap), so let it recover first
+    time.sleep(2.0)
+    layer.profile(True)
+    layer.profile_read(reset=True)
+    barrier()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        step()
+    p1.record(stream)
+    torch.cuda.synchronize(dev)
+    prof_ms_step = max_over_ranks(p0.elapsed_time(p1)) / args.steps
+    barrier()
+    ktimes = layer.profile_read(reset=True)
+    layer.profile(False)
 
     graph_ms = None
     if args.graph and not (use_ep and not peer):  # NCCL EP syncs the host per forward
@@ -463,6 +481,8 @@ def run_ours(args):
                        "kept_assignments": A, "drops": stats["drops"],
                        "padding_flops_avoided": padded_flops},
             "roofline": roofline,
+            "device_flags": dev_flags,
+            "ms_per_step_profiled": round(prof_ms_step, 4),
             "hbm_gbs": hbm,
             "kernels": kernels,
             "cpu_baseline": cpu_base,

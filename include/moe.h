@@ -224,7 +224,9 @@ typedef struct {
 MOE_API moe_status_t moe_get_stats_async(moe_handle_t h, const moe_stats_t* dst);
 
 /* Synchronises the stream and reports (then clears) the device error flags:
-   bit 0 = NaN gate logit, bit 1 = invalid cached index.  flags_out may be NULL. */
+   bit 0 = NaN gate logit, bit 1 = invalid cached index, bit 2 = sample id out of range,
+   bit 3 = a peer-transport barrier timed out (a rank never arrived within 20 s; the
+   iteration's results are invalid).  flags_out may be NULL. */
 MOE_API moe_status_t moe_check_device_flags(moe_handle_t h, int32_t* flags_out);
 
 /* ----------------------------------------------------------------------------------- *

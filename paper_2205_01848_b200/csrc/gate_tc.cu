@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(G_THREADS, 2)
     gate_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmX,
                        const __grid_constant__ CUtensorMap tmW,
                        const __grid_constant__ CUtensorMap tmL, GateFwdParams p, int K) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   constexpr int A_BYTES = TC_BM * TC_BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + BN * TC_BK * 2;
   constexpr uint32_t IDESC = make_idesc(BN, 0, 0);
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
     gate_dx_tc_kernel(const __grid_constant__ CUtensorMap tmHi,
                       const __grid_constant__ CUtensorMap tmLo,
                       const __grid_constant__ CUtensorMap tmW, GateDxParams p) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   constexpr int A_BYTES = TC_BM * TC_BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + BN * TC_BK * 2;
   constexpr uint32_t IDESC = make_idesc(BN, 0, 1);
@@ -588,6 +590,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     gate_dw_tc_kernel(const __grid_constant__ CUtensorMap tmHi,
                       const __grid_constant__ CUtensorMap tmLo,
                       const __grid_constant__ CUtensorMap tmX, GateDwParams p) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   constexpr int A_BYTES = TC_BM * TC_BK * 2;  // one of hi / lo
   constexpr int STAGE_BYTES = 2 * A_BYTES + BN * TC_BK * 2;
   constexpr uint32_t IDESC = make_idesc(BN, 1, 1);
@@ -780,7 +783,7 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
     size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 1024 + 4 * GF_STG_BYTES;             \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \
-    kf<<<grid, G_THREADS, sm, s>>>(mx, mw, ml, p, d);                                    \
+    launch_pdl(kf, grid, G_THREADS, sm, s, mx, mw, ml, p, d);                                    \
   }
   if (bn == 64) GF(64, 4) else if (bn == 128) GF(128, 3) else GF(256, 2)
 #undef GF
@@ -814,7 +817,7 @@ cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb
     size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 8 * 2 * 2 * 32 * (BN + 16);          \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \
-    kf<<<grid, GX_THREADS, sm, s>>>(mhi, mlo, mw, p);                                     \
+    launch_pdl(kf, grid, GX_THREADS, sm, s, mhi, mlo, mw, p);                                     \
   }
   if (bn == 128) GX(128, 2) else GX(64, 4)
 #undef GX
@@ -860,7 +863,7 @@ cudaError_t launch_gate_dw_tc(const void* dlb, int maxT, int n_pad, const void* 
     size_t sm = smem_for((2 * 128 + BN) * 64 * 2, ST);                                   \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \
-    kf<<<grid, G_THREADS, sm, s>>>(mhi, mlo, mx, p);                                     \
+    launch_pdl(kf, grid, G_THREADS, sm, s, mhi, mlo, mx, p);                                     \
   }
   if (bn == 256) GW(256, 3) else if (bn == 128) GW(128, 4) else GW(64, 5)
 #undef GW

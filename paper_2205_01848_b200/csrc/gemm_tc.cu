@@ -40,6 +40,7 @@ template <int KIND, int BN, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    TcParams p) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   using Tr = KindTraits<KIND>;
   constexpr int A_BYTES = TC_BM * TC_BK * 2;
   constexpr int B_BYTES = BN * TC_BK * 2;
@@ -384,7 +385,7 @@ static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const T
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kf<<<g_num_sms, TC_THREADS, smem, s>>>(a, b, p);
+  launch_pdl(kf, g_num_sms, TC_THREADS, smem, s, a, b, p);
   return cudaGetLastError();
 }
 
@@ -450,6 +451,7 @@ bool tc_combine_supported(int dout) { return use_2cta(dout, TC_FWD2); }
 __global__ void bias_part_reduce_kernel(const float* __restrict__ part,
                                         const int32_t* __restrict__ kept, int N,
                                         __nv_bfloat16* __restrict__ db, int accumulate) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const int e = blockIdx.y;
   __shared__ int s_pre, s_mt;
   if (threadIdx.x < 32) {
@@ -629,7 +631,7 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   ++nl;
   if (db1_in_dgrad) {
     ProfScope ps(prof, "bias_grad", s);
-    bias_part_reduce_kernel<<<dim3((f + 255) / 256, n_local), 256, 0, s>>>(
+    launch_pdl(bias_part_reduce_kernel, dim3((f + 255) / 256, n_local), 256, 0, s, 
         bias_part, kept, f, (__nv_bfloat16*)db1, accumulate);
     TC_CUDA(cudaGetLastError());
     ++nl;

@@ -127,6 +127,7 @@ template <int KIND, int BN, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC, TcParams p) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   using Tr = KindTraits<KIND>;
   constexpr int BNH = BN / 2;                    // B columns held by each CTA
   constexpr int A_BYTES = TC_BM * TC_BK * 2;     // 16 KB: this CTA's 128 rows
@@ -648,7 +649,7 @@ static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const CUt
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kf<<<grid, TC_THREADS, smem, s>>>(a, b, c, p);
+  launch_pdl(kf, grid, TC_THREADS, smem, s, a, b, c, p);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,15 @@
 
 using namespace moe;
 
+int moe::pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_PDL");
+    v = e ? (atoi(e) != 0) : 1;
+  }
+  return v;
+}
+
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
       xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, grow, ep_all, sendbuf, oret, dwg32,
@@ -528,7 +537,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
                                              h->cts, rb, X, rb.kept, sd, h->e_lo,
                                              peer_bufs(h, h->PL.x), peer_bufs(h, h->PL.tos),
                                              pre_dev));
-    KL(h, 1, "peer_barrier", sd, launch_peer_barrier(h->wins, h->R, h->rank, PH_X, sd));
+    KL(h, 1, "peer_barrier", sd, launch_peer_barrier(h->wins, h->R, h->rank, PH_X, sd, (uint32_t*)rb.flags));
   } else {
     // C1 + the single host sync of EP v1: all-gather the per-rank pre-drop counts, then every
     // rank derives the same global slot offsets, kept counts and message sizes (reading 12).
@@ -580,7 +589,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   void* O_tok = O;  // expert outputs as the token side indexes them
   PeerBufs po{};    // peer EP: combine reads O rows from the owners
   if (h->use_peer) {
-    KL(h, 1, "peer_barrier", sd, launch_peer_barrier(h->wins, h->R, h->rank, PH_O, sd));
+    KL(h, 1, "peer_barrier", sd, launch_peer_barrier(h->wins, h->R, h->rank, PH_O, sd, (uint32_t*)rb.flags));
     po = peer_bufs(h, h->PL.o);
   } else if (h->use_ep) {
     std::string err;
@@ -605,7 +614,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     if (h->use_peer) {  // column sums through the windows, summed in rank order
       KL(h, T > 0 ? 2 : 1, "balance", s0, launch_balance_partial(rb.logits, T, n, bal,
                                                                  (float*)(h->pwin + h->PL.bal), s0));
-      KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_BAL, s0));
+      KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_BAL, s0, (uint32_t*)rb.flags));
       KL(h, 1, "peer_sum", s0, launch_peer_sum(h->wins, h->PL.bal, h->R, (size_t)n, 2, gsum, 0, s0));
     } else {
       KL(h, T > 0 ? 2 : 1, "balance", s0, launch_balance_partial(rb.logits, T, n, bal, gsum, s0));
@@ -688,7 +697,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   rb.dw_ext = nullptr;
   rb.bal_g = nullptr;
   if (peer) {  // N1: dO rows were stored into the owners by the combine backward
-    KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DO, s0));
+    KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DO, s0, (uint32_t*)rb.flags));
   } else if (h->use_ep) {  // C4: dO rows to the expert owners
     moe_status_t st = ep_to_experts(h->ep, h->plan, dO_tok, dO, h->ct, dout, (int)h->s, s0, &err);
     if (st != MOE_OK) return fail(h, st, err);
@@ -734,7 +743,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   void* dX_tok = dXb;
   PeerBufs pdx{};
   if (peer) {  // N1: the gate-input gradient reads dX rows from the owners
-    KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DX, s0));
+    KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DX, s0, (uint32_t*)rb.flags));
     pdx = peer_bufs(h, h->PL.dxb);
   } else if (h->use_ep) {  // C5: dX rows back to the token owners (send layout, reuses the send buffer)
     dX_tok = ws + h->L.sendbuf;
@@ -762,7 +771,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
     }
     if (T == 0 && f32) CUDA_TRY(h, cudaMemsetAsync(f32, 0, (size_t)n * d * 4, s0));  // no tokens
     if (peer) {  // N1: sum of every rank's fp32 partial in rank order
-      KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DW, s0));
+      KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DW, s0, (uint32_t*)rb.flags));
       KL(h, 1, "gate_dw", s0, launch_peer_sum(h->wins, h->PL.dwg, h->R, (size_t)n * d, dt,
                                               a->dw_gate, acc, s0));
     } else if (h->use_ep) {  // C6
@@ -875,7 +884,8 @@ moe_status_t moe_check_device_flags(moe_handle_t h, int32_t* flags_out) {
     return fail(h, MOE_ERR_DEVICE_FLAG,
                 std::string("device flags: ") + ((fl & 1) ? "NaN logit " : "") +
                     ((fl & 2) ? "invalid cached index " : "") +
-                    ((fl & 4) ? "sample id out of range" : ""));
+                    ((fl & 4) ? "sample id out of range " : "") +
+                    ((fl & 8) ? "peer barrier timeout" : ""));
   }
   return MOE_OK;
 }

@@ -24,17 +24,32 @@ __device__ __forceinline__ int32_t ld_volatile(const int32_t* p) {
   return *reinterpret_cast<const volatile int32_t*>(p);
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Threads 0..R-1: publish epoch `ep` for `phase` into every rank's flag slot of this rank,
 // then wait until every rank published >= ep into ours.  Called by all threads of the block.
+// A peer that never arrives (dead rank, mismatched call sequence) does not hang the GPU: after
+// MOE_PEER_TIMEOUT_NS the wait gives up and raises device flag 8 (moe_check_device_flags).
 __device__ __forceinline__ void barrier_block(const PeerBufs& win, int R, int rank, int phase,
-                                              uint32_t ep) {
+                                              uint32_t ep, uint32_t* err_flags) {
   __threadfence_system();
   __syncthreads();
   const int j = threadIdx.x;
   if (j < R) {
     st_release_sys(flag_ptr(win.p[j], phase, rank), ep);
     const uint32_t* mine = flag_ptr(win.p[rank], phase, j);
-    while ((int32_t)(ld_acquire_sys(mine) - ep) < 0) __nanosleep(64);
+    const uint64_t t0 = globaltimer_ns();
+    while ((int32_t)(ld_acquire_sys(mine) - ep) < 0) {
+      __nanosleep(64);
+      if (globaltimer_ns() - t0 > MOE_PEER_TIMEOUT_NS) {
+        if (err_flags) atomicOr(err_flags, MOE_FLAG_PEER_TIMEOUT);
+        break;
+      }
+    }
   }
   __syncthreads();
 }
@@ -43,7 +58,8 @@ __global__ void __launch_bounds__(256) peer_plan_kernel(PeerBufs win, int R, int
                                                         int nl, const int32_t* __restrict__ lc,
                                                         CapTable ct, int32_t* counts_out,
                                                         int32_t* kept_out, int32_t* mtile_prefix,
-                                                        int64_t* drops_out, int32_t* pre_out) {
+                                                        int64_t* drops_out, int32_t* pre_out,
+                                                        uint32_t* err_flags) {
   __shared__ uint32_t s_ep;
   __shared__ long long s_drops[8];
   __shared__ int32_t s_tiles[MOE_MAX_E];
@@ -62,7 +78,7 @@ __global__ void __launch_bounds__(256) peer_plan_kernel(PeerBufs win, int R, int
     for (int j = 0; j < R; ++j)
       reinterpret_cast<int32_t*>(win.p[j] + 512)[rank * MOE_MAX_E + e] = c;
   }
-  barrier_block(win, R, rank, PH_CNT, ep);
+  barrier_block(win, R, rank, PH_CNT, ep, err_flags);
   // global plan (reading 12: global capacity, slots in ascending global token order, so
   // rank r's pairs of e start after those of ranks < r)
   long long drop = 0;
@@ -113,9 +129,10 @@ __global__ void __launch_bounds__(256) peer_plan_kernel(PeerBufs win, int R, int
   }
 }
 
-__global__ void peer_barrier_kernel(PeerBufs win, int R, int rank, int phase) {
+__global__ void peer_barrier_kernel(PeerBufs win, int R, int rank, int phase,
+                                    uint32_t* err_flags) {
   const uint32_t ep = *reinterpret_cast<const volatile uint32_t*>(win.p[rank]);
-  barrier_block(win, R, rank, phase, ep);
+  barrier_block(win, R, rank, phase, ep, err_flags);
 }
 
 template <typename T>
@@ -171,12 +188,14 @@ cudaError_t launch_peer_plan(const PeerBufs& win, int R, int rank, int n, int n_
                              const int32_t* local_counts, const CapTable& ct, RouteBufs b,
                              int32_t* pre_out, cudaStream_t s) {
   peer_plan_kernel<<<1, 256, 0, s>>>(win, R, rank, n, n_local, local_counts, ct, b.counts,
-                                     b.kept, b.mtile_prefix, b.drops, pre_out);
+                                     b.kept, b.mtile_prefix, b.drops, pre_out,
+                                     reinterpret_cast<uint32_t*>(b.flags));
   return cudaGetLastError();
 }
 
-cudaError_t launch_peer_barrier(const PeerBufs& win, int R, int rank, int phase, cudaStream_t s) {
-  peer_barrier_kernel<<<1, 32, 0, s>>>(win, R, rank, phase);
+cudaError_t launch_peer_barrier(const PeerBufs& win, int R, int rank, int phase, cudaStream_t s,
+                                uint32_t* err_flags) {
+  peer_barrier_kernel<<<1, 32, 0, s>>>(win, R, rank, phase, err_flags);
   return cudaGetLastError();
 }
 

@@ -51,7 +51,13 @@ cudaError_t launch_peer_plan(const PeerBufs& win, int R, int rank, int n, int n_
                              const int32_t* local_counts, const CapTable& ct, RouteBufs b,
                              int32_t* pre_out, cudaStream_t s);
 // Exchange barrier of `phase` at the current epoch (one block of 32 threads).
-cudaError_t launch_peer_barrier(const PeerBufs& win, int R, int rank, int phase, cudaStream_t s);
+cudaError_t launch_peer_barrier(const PeerBufs& win, int R, int rank, int phase, cudaStream_t s,
+                                uint32_t* err_flags);
+// bounded wait of the barrier kernels (a peer that never arrives raises device flag 8)
+#ifndef MOE_PEER_TIMEOUT_NS
+#define MOE_PEER_TIMEOUT_NS 20000000000ull
+#endif
+#define MOE_FLAG_PEER_TIMEOUT 8u
 // out[i] (dtype; accumulate) = sum over ranks j = 0..R-1 of ((float*)(win[j] + off))[i].
 // dtype 2 = fp32 output.
 cudaError_t launch_peer_sum(const PeerBufs& win, size_t off, int R, size_t count, int dtype,

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(
     int renorm, const int32_t* __restrict__ cached, float* __restrict__ logits,
     int32_t* __restrict__ idx_out, float* __restrict__ w_out, int32_t* __restrict__ hit,
     int32_t* __restrict__ flags, int32_t* __restrict__ idx_fix) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   extern __shared__ float smem[];
   float* xs = smem;                              // [GATE_TOK][GATE_DK+1]
   float* ws = xs + GATE_TOK * (GATE_DK + 1);     // [n][GATE_DK+1]
@@ -156,13 +157,13 @@ cudaError_t launch_gate_topk(int dtype, const void* x, const void* wg, int T, in
     if (dtype == 1) {                                                                      \
       auto kf = gate_topk_kernel<__nv_bfloat16, NJ>;                                       \
       cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
-      kf<<<grid, 256, smem, s>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)wg, T, n,  \
+      launch_pdl(kf, grid, 256, smem, s, (const __nv_bfloat16*)x, (const __nv_bfloat16*)wg, T, n,  \
                                  d, k, renorm, cached, b.logits, idx_out, b.w,             \
                                  b.hit_count, b.flags, cached ? b.idx_fix : nullptr);      \
     } else {                                                                               \
       auto kf = gate_topk_kernel<float, NJ>;                                               \
       cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
-      kf<<<grid, 256, smem, s>>>((const float*)x, (const float*)wg, T, n, d, k, renorm,    \
+      launch_pdl(kf, grid, 256, smem, s, (const float*)x, (const float*)wg, T, n, d, k, renorm,    \
                                  cached, b.logits, idx_out, b.w, b.hit_count, b.flags,     \
                                  cached ? b.idx_fix : nullptr);                            \
     }                                                                                      \
@@ -178,6 +179,7 @@ cudaError_t launch_gate_topk(int dtype, const void* x, const void* wg, int T, in
 // =====================================================================================
 __global__ void route_hist_kernel(const int32_t* __restrict__ idx, int Tn, int k, int n,
                                   int32_t* __restrict__ hist) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   __shared__ int32_t h[MOE_MAX_E];
   for (int e = threadIdx.x; e < n; e += blockDim.x) h[e] = 0;
   __syncthreads();
@@ -195,7 +197,7 @@ cudaError_t launch_route_hist(const int32_t* idx, int T, int k, int n, int32_t* 
                               cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   int ntiles = (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE;
-  route_hist_kernel<<<ntiles, MOE_ROUTE_TILE, 0, s>>>(idx, T, k, n, hist);
+  launch_pdl(route_hist_kernel, ntiles, MOE_ROUTE_TILE, 0, s, idx, T, k, n, hist);
   return cudaGetLastError();
 }
 
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
     int32_t* __restrict__ tile_off, int32_t* __restrict__ counts, int32_t* __restrict__ kept,
     int32_t* __restrict__ mtile_prefix, int64_t* __restrict__ drops,
     uint32_t* __restrict__ ticket) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const int e = blockIdx.x;
   __shared__ int32_t warp_tot[8];
   __shared__ int32_t carry;
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
 
 cudaError_t launch_route_scan(const int32_t* hist, int ntiles, int n, const CapTable& ct,
                               RouteBufs b, cudaStream_t s) {
-  route_scan_kernel<<<n, 256, 0, s>>>(hist, ntiles, n, ct, b.tile_off, b.counts, b.kept,
+  launch_pdl(route_scan_kernel, n, 256, 0, s, hist, ntiles, n, ct, b.tile_off, b.counts, b.kept,
                                       b.mtile_prefix, b.drops, b.ticket);
   return cudaGetLastError();
 }
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
     int32_t* __restrict__ slot_of, int32_t* __restrict__ token_of_slot, T* __restrict__ xbuf,
     const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs px, PeerBufs ptos,
     const int32_t* __restrict__ pre_dev, T* __restrict__ yz, int dout) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   // px.nl != 0 (peer EP, N1): rows go straight into the owners' X buffers over NVLink, the
   // global slot offsets come from the device plan (pre_dev), token_of_slot is the owner's.
   // xbuf == null (N2 gather fusion): only the routing tables are written -- the expert GEMMs
@@ -429,12 +433,12 @@ cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T,
   if (T == 0 && !(pad_kept && px.nl)) return cudaSuccess;  // peer EP: own pads still zeroed
   int ntiles = std::max(1, (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE);
   if (dtype == 1)
-    dispatch_kernel<__nv_bfloat16><<<ntiles, 256, 0, s>>>(
+    launch_pdl(dispatch_kernel<__nv_bfloat16>, ntiles, 256, 0, s, 
         idx, (const __nv_bfloat16*)x, T, k, n, d, token_base, ct, b.tile_off, b.slot_of,
         b.token_of_slot, (__nv_bfloat16*)xbuf, pad_kept, pad_e0, px, ptos, pre_dev,
         (__nv_bfloat16*)y_zero, dout);
   else
-    dispatch_kernel<float><<<ntiles, 256, 0, s>>>(idx, (const float*)x, T, k, n, d,
+    launch_pdl(dispatch_kernel<float>, ntiles, 256, 0, s, idx, (const float*)x, T, k, n, d,
                                                   token_base, ct, b.tile_off, b.slot_of,
                                                   b.token_of_slot, (float*)xbuf, pad_kept,
                                                   pad_e0, px, ptos, pre_dev, (float*)y_zero,
@@ -447,6 +451,7 @@ cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T,
 template <typename T>
 __global__ void zero_pad_kernel(T* __restrict__ buf, int cols, const int32_t* __restrict__ kept,
                                 CapTable ct) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const int e = blockIdx.x;
   const int kp = kept[e];
   const int r0 = ct.base[e] + kp;
@@ -462,9 +467,9 @@ __global__ void zero_pad_kernel(T* __restrict__ buf, int cols, const int32_t* __
 cudaError_t launch_zero_pad(int dtype, void* buf, int cols, const int32_t* kept, int n,
                             const CapTable& ct, cudaStream_t s) {
   if (dtype == 1)
-    zero_pad_kernel<__nv_bfloat16><<<n, 256, 0, s>>>((__nv_bfloat16*)buf, cols, kept, ct);
+    launch_pdl(zero_pad_kernel<__nv_bfloat16>, n, 256, 0, s, (__nv_bfloat16*)buf, cols, kept, ct);
   else
-    zero_pad_kernel<float><<<n, 256, 0, s>>>((float*)buf, cols, kept, ct);
+    launch_pdl(zero_pad_kernel<float>, n, 256, 0, s, (float*)buf, cols, kept, ct);
   return cudaGetLastError();
 }
 
@@ -479,6 +484,7 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
     const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
     T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid, PeerBufs po) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
@@ -553,6 +559,7 @@ __global__ void __launch_bounds__(256) combine_fwd_generic_kernel(
     const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
     T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid, PeerBufs po) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
@@ -602,14 +609,14 @@ static cudaError_t combine_fwd_t(const void* obuf, RouteBufs b, int T_, int k, i
   dim3 grid((T_ + 7) / 8);
   const int vpl = (d_out / Vec<T>::N + 31) / 32;
 #define CF(V, K)                                                                            \
-  combine_fwd_kernel<T, V, K><<<grid, 256, 0, s>>>((const T*)obuf, b.w, b.idx, b.slot_of, ct, \
+  launch_pdl(combine_fwd_kernel<T, V, K>, grid, 256, 0, s, (const T*)obuf, b.w, b.idx, b.slot_of, ct, \
                                                    T_, k, d_out, (T*)y, spec, valid, po)
   if (k <= 2) {
     if (vpl <= 2) { if (k == 1) CF(2, 1); else CF(2, 2); }
     else if (vpl <= 4) { if (k == 1) CF(4, 1); else CF(4, 2); }
     else { if (k == 1) CF(8, 1); else CF(8, 2); }
   } else {
-    combine_fwd_generic_kernel<T><<<grid, 256, 0, s>>>((const T*)obuf, b.w, b.idx, b.slot_of, ct,
+    launch_pdl(combine_fwd_generic_kernel<T>, grid, 256, 0, s, (const T*)obuf, b.w, b.idx, b.slot_of, ct,
                                                        T_, k, d_out, (T*)y, spec, valid, po);
   }
 #undef CF
@@ -640,6 +647,7 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
     const float* __restrict__ dw_ext, const float* __restrict__ bal_g,
     int32_t* __restrict__ grow, const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs po,
     PeerBufs pdo) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   // peer EP (N1): O rows are read from, and dO rows written to, the experts' owners
   if (pad_kept)
     zero_pads_block(dobuf, dout, pad_kept, ct, pdo.nl ? pdo.nl : n, pad_e0, blockIdx.x, gridDim.x);
@@ -809,7 +817,7 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
   dim3 grid(std::max(1, (T_ + 7) / 8));
   const int vpl = (d_out / Vec<T>::N + 31) / 32;  // > 8: the kernel loops over 4 KB blocks
 #define CB(V, K)                                                                               \
-  combine_bwd_kernel<T, V, K><<<grid, 256, 0, s>>>((const T*)dy, (const T*)obuf, b.w, b.idx,   \
+  launch_pdl(combine_bwd_kernel<T, V, K>, grid, 256, 0, s, (const T*)dy, (const T*)obuf, b.w, b.idx,   \
                                                    b.slot_of, b.logits, ct, T_, k, n, d_out,   \
                                                    renorm, (T*)dobuf, b.dw, b.dl,              \
                                                    (__nv_bfloat16*)dlb, maxT, n_pad,           \
@@ -846,6 +854,7 @@ __global__ void __launch_bounds__(256) gate_dx_kernel(
     const float* __restrict__ dl, const T* __restrict__ wg, const T* __restrict__ dxbuf,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of, CapTable ct, int Tn,
     int k, int n, int d, T* __restrict__ dx, int accumulate, PeerBufs pdx) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   __shared__ float dls[32][33];
   __shared__ float wgs[32][128];
   const int tid = threadIdx.x;
@@ -918,11 +927,11 @@ cudaError_t launch_gate_dx(int dtype, const void* wg, const void* dxbuf, RouteBu
   if (T == 0) return cudaSuccess;
   dim3 grid((d + 127) / 128, (T + 31) / 32);
   if (dtype == 1)
-    gate_dx_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+    launch_pdl(gate_dx_kernel<__nv_bfloat16>, grid, 256, 0, s, 
         b.dl, (const __nv_bfloat16*)wg, (const __nv_bfloat16*)dxbuf, b.idx, b.slot_of, ct, T, k,
         n, d, (__nv_bfloat16*)dx, accumulate, pdx);
   else
-    gate_dx_kernel<float><<<grid, 256, 0, s>>>(b.dl, (const float*)wg, (const float*)dxbuf,
+    launch_pdl(gate_dx_kernel<float>, grid, 256, 0, s, b.dl, (const float*)wg, (const float*)dxbuf,
                                                b.idx, b.slot_of, ct, T, k, n, d, (float*)dx,
                                                accumulate, pdx);
   return cudaGetLastError();
@@ -938,6 +947,7 @@ __global__ void __launch_bounds__(256) gate_dw_kernel(const float* __restrict__ 
                                                       const T* __restrict__ x, int Tn, int n,
                                                       int d, int chunk,
                                                       float* __restrict__ partial) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   extern __shared__ float sm[];
   float* xs = sm;                 // [32][64]
   float* ls = sm + 32 * 64;       // [32][n]
@@ -983,6 +993,7 @@ __global__ void __launch_bounds__(256) gate_dw_kernel(const float* __restrict__ 
 template <typename T>
 __global__ void reduce_partials_kernel(const float* __restrict__ partial, int splits,
                                        size_t count, T* __restrict__ out, int accumulate) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   float s = 0.f;
@@ -995,10 +1006,10 @@ cudaError_t launch_reduce_partials(int dtype, const float* partial, int splits, 
                                    void* out, int accumulate, cudaStream_t s) {
   int rb = (int)((count + 255) / 256);
   if (dtype == 1)
-    reduce_partials_kernel<__nv_bfloat16><<<rb, 256, 0, s>>>(partial, splits, count,
+    launch_pdl(reduce_partials_kernel<__nv_bfloat16>, rb, 256, 0, s, partial, splits, count,
                                                              (__nv_bfloat16*)out, accumulate);
   else
-    reduce_partials_kernel<float><<<rb, 256, 0, s>>>(partial, splits, count, (float*)out,
+    launch_pdl(reduce_partials_kernel<float>, rb, 256, 0, s, partial, splits, count, (float*)out,
                                                      accumulate);
   return cudaGetLastError();
 }
@@ -1029,11 +1040,11 @@ cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int
     if (dtype == 1) {                                                                       \
       auto kf = gate_dw_kernel<__nv_bfloat16, NJ>;                                          \
       cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-      kf<<<grid, 256, smem, s>>>(dl, (const __nv_bfloat16*)x, T, n, d, chunk, partial);     \
+      launch_pdl(kf, grid, 256, smem, s, dl, (const __nv_bfloat16*)x, T, n, d, chunk, partial);     \
     } else {                                                                                \
       auto kf = gate_dw_kernel<float, NJ>;                                                  \
       cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-      kf<<<grid, 256, smem, s>>>(dl, (const float*)x, T, n, d, chunk, partial);             \
+      launch_pdl(kf, grid, 256, smem, s, dl, (const float*)x, T, n, d, chunk, partial);             \
     }                                                                                       \
   } else
   GDW_CASE(2) GDW_CASE(4) GDW_CASE(8) GDW_CASE(16) GDW_CASE(32) GDW_CASE(64) {
@@ -1049,6 +1060,7 @@ cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int
 template <typename T>
 __global__ void f32_to_kernel(const float* __restrict__ in, size_t count, T* __restrict__ out,
                               int accumulate) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   float v = in[i];
@@ -1060,9 +1072,9 @@ cudaError_t launch_f32_to(int dtype, const float* in, size_t count, void* out, i
                           cudaStream_t s) {
   int rb = (int)((count + 255) / 256);
   if (dtype == 1)
-    f32_to_kernel<__nv_bfloat16><<<rb, 256, 0, s>>>(in, count, (__nv_bfloat16*)out, accumulate);
+    launch_pdl(f32_to_kernel<__nv_bfloat16>, rb, 256, 0, s, in, count, (__nv_bfloat16*)out, accumulate);
   else
-    f32_to_kernel<float><<<rb, 256, 0, s>>>(in, count, (float*)out, accumulate);
+    launch_pdl(f32_to_kernel<float>, rb, 256, 0, s, in, count, (float*)out, accumulate);
   return cudaGetLastError();
 }
 
@@ -1074,6 +1086,7 @@ template <typename T>
 __global__ void colsum_kernel(const T* __restrict__ buf, int cols,
                               const int32_t* __restrict__ kept, CapTable ct,
                               T* __restrict__ out, int accumulate) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const int e = blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= cols) return;
@@ -1089,10 +1102,10 @@ cudaError_t launch_colsum(int dtype, const void* buf, int cols, const int32_t* k
                           const CapTable& ct, void* out, int accumulate, cudaStream_t s) {
   dim3 grid((cols + 255) / 256, n);
   if (dtype == 1)
-    colsum_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)buf, cols, kept,
+    launch_pdl(colsum_kernel<__nv_bfloat16>, grid, 256, 0, s, (const __nv_bfloat16*)buf, cols, kept,
                                                       ct, (__nv_bfloat16*)out, accumulate);
   else
-    colsum_kernel<float><<<grid, 256, 0, s>>>((const float*)buf, cols, kept, ct, (float*)out,
+    launch_pdl(colsum_kernel<float>, grid, 256, 0, s, (const float*)buf, cols, kept, ct, (float*)out,
                                               accumulate);
   return cudaGetLastError();
 }
