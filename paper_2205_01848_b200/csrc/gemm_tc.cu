@@ -411,7 +411,8 @@ static int tc_pf() {  // MOE_TC_PF: k-blocks of B prefetched to L2 for the next 
   return v;
 }
 
-static int tc_dbg() {  // MOE_TC_DBG: timing experiments only (1: skip epilogue stores)
+static int tc_dbg() {  // MOE_TC_DBG: timing experiments only (1: skip epilogue stores,
+                       // 2: skip the db1 partials, 4: skip the relu-mask loads)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("MOE_TC_DBG");
@@ -467,9 +468,9 @@ __global__ void bias_part_reduce_kernel(const float* __restrict__ part,
   __syncthreads();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
-  const float* pp = part + (size_t)s_pre * 8 * N + c;
+  const float* pp = part + (size_t)s_pre * 2 * N + c;
   float v = 0.f;
-  for (int j = 0; j < s_mt * 8; ++j) v += pp[(size_t)j * N];
+  for (int j = 0; j < s_mt * 2; ++j) v += pp[(size_t)j * N];
   if (accumulate) v += __bfloat162float(db[(size_t)e * N + c]);
   db[(size_t)e * N + c] = __float2bfloat16_rn(v);
 }

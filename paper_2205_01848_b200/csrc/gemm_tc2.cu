@@ -148,6 +148,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   float* s_bias = reinterpret_cast<float*>(s_prefix + MOE_MAX_E + 4);  // [4][128]
   uint8_t* s_stg = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(s_bias + 4 * 128) + 1023) & ~uintptr_t(1023));  // [8][2 KB]
+  // DGRAD_A db1 column sums: [tile parity][column half][row quarter][BN / 2]
+  float* s_red = reinterpret_cast<float*>(s_stg + 8 * TC2_NBUF * TC2_STG_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank();
@@ -445,10 +447,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       uint32_t mbits[CH];
       uint32_t mout[CH];
 #pragma unroll
-      for (int cc = 0; cc < CH; ++cc) mout[cc] = 0u;
+      for (int cc = 0; cc < CH; ++cc) mout[cc] = 0u, mbits[cc] = ~0u;
       const int mask_ld = p.N >> 5;
       uint32_t* mrow = p.mask ? p.mask + (size_t)(p.ct.base[e] + row) * mask_ld : nullptr;
-      if (KIND == TC_DGRAD_A && row_ok) {  // relu' mask bits written by FWD1 (not H itself)
+      if (KIND == TC_DGRAD_A && row_ok && !(p.dbg & 4)) {  // relu' mask bits written by FWD1
 #pragma unroll
         for (int cc = 0; cc < CH; ++cc) mbits[cc] = mrow[(n0 >> 5) + half * CH + cc];
       }
@@ -519,11 +521,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.f;
           }
-          if (p.bias_part) {
+          if (p.bias_part && !(p.dbg & 2)) {
             // db1 = sum over kept tokens of dA (the stored bf16 values): column sums of this
             // warp's 32 rows by a transpose-reduce over the lanes (31 shuffles; lane j ends
-            // with column j), written as a per-(m-tile, CTA, quarter) partial row that a
-            // fixed-order kernel reduces per expert: deterministic, no atomics.
+            // with column j), parked in shared memory; after the tile the 4 row-quarter warps
+            // of this column half are summed in fixed order (below) into one partial row per
+            // (m-tile, CTA) that a fixed-order kernel reduces per expert: deterministic.
             float cs[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) cs[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
@@ -537,8 +540,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                 cs[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
               }
             }
-            const size_t prow = ((size_t)(s_prefix[e] + mt) * 2 + crank) * 4 + q;
-            p.bias_part[prow * p.N + col0 + lane] = cs[0];
+            s_red[(((it & 1) * 2 + half) * 4 + q) * (CH * 32) + cc * 32 + lane] = cs[0];
           }
         } else if (KIND == TC_DGRAD_X) {
           store = row_ok;
@@ -611,6 +613,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           }
         }
       }
+      if (KIND == TC_DGRAD_A && p.bias_part && !(p.dbg & 2)) {
+        // fixed-order sum of the 4 row quarters of this column half -> one partial row per
+        // (m-tile, CTA); s_red is double-buffered by tile parity, so one barrier per tile
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
+        if (q == 0) {
+          const float* rb = s_red + (((it & 1) * 2 + half) * 4) * (CH * 32);
+          const size_t prow = (size_t)(s_prefix[e] + mt) * 2 + crank;
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int c = j * 32 + lane;
+            const float sum = ((rb[c] + rb[CH * 32 + c]) + rb[2 * CH * 32 + c]) + rb[3 * CH * 32 + c];
+            const int col = n0 + half * CH * 32 + c;
+            if (col < p.N) p.bias_part[prow * p.N + col] = sum;
+          }
+        }
+      }
       if (KIND == TC_FWD1 && mrow && (row_ok || row_pad)) {  // one vector store per thread
         uint32_t* mdst = mrow + (n0 >> 5) + half * CH;
         if (CH == 4)
@@ -641,7 +659,8 @@ static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const CUt
   constexpr int STAGES = (BN == 256) ? (TC2_NBUF > 1 ? 5 : 6) : 8;
   constexpr int STAGE_BYTES = (TC_BM + BN / 2) * TC_BK * 2;
   const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 512 + 4 * (MOE_MAX_E + 8) + 2048 +
-                      1024 + 8 * TC2_NBUF * TC2_STG_BYTES;
+                      1024 + 8 * TC2_NBUF * TC2_STG_BYTES +
+                      (KIND == TC_DGRAD_A ? 2 * 2 * 4 * (BN / 2) * 4 : 0);
   auto kf = tc_gemm2_kernel<KIND, BN, STAGES>;
   static bool attr = false;
   if (!attr) {

@@ -23,8 +23,8 @@ struct TcParams {
   __nv_bfloat16* C;             // output base (buffer or weight-gradient tensor)
   int ldc;                      // leading dim of C (M-grouped buffers)
   int accumulate;               // WGRAD
-  float* bias_part;             // 2-CTA DGRAD_A: per-(256-row m-tile, CTA, quarter) column sums
-                                // of dA, [sum_e ceil(kept_e/256) * 8][N] fp32 (db1 partials)
+  float* bias_part;             // 2-CTA DGRAD_A: per-(256-row m-tile, CTA) column sums of dA,
+                                // [sum_e ceil(kept_e/256) * 2][N] fp32 (db1 partials)
   uint32_t* mask;               // FWD1 writes / DGRAD_A reads: bit j of word [row][c] = (H > 0)
                                 // for column 32c + j (relu' mask, 16x fewer bytes than H)
   int pf_kb;                    // 2-CTA: k-blocks of the next wave's B tile to prefetch to L2

@@ -150,7 +150,7 @@ void compute_layout(moe_ctx* h) {
   // balance term: partial column sums [ceil(T/64) x n], gsum [n], g [n], aux [1]
   L.bal = take(((T + 63) / 64 + 3) * n * 4 + 256);
   L.grow = take(T * k * 4);
-  L.bpart = take(h->dtype == MOE_BF16 ? ((size_t)h->rows / 256 + h->n_local) * 8 * h->f * 4 : 0);
+  L.bpart = take(h->dtype == MOE_BF16 ? ((size_t)h->rows / 256 + h->n_local) * 2 * h->f * 4 : 0);
   const bool ep = h->use_ep && !h->use_peer;  // NCCL transport buffers
   L.pre_dev = take(n * 4);
   L.ep_all = take(ep ? (size_t)h->R * n * 4 : 0);
