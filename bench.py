@@ -46,9 +46,11 @@ def parse():
     ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
                     help="expert-parallel exchange: peer = device-initiated through peer "
                          "memory over NVLink (N1, default); nccl = grouped send/recv")
-    ap.add_argument("--fusion", choices=["none", "combine", "all"], default="combine",
-                    help="N2 fusions: combine = y written by the second expert GEMM's epilogue "
-                         "(k = 1, default); all = also gather x rows in the expert GEMMs")
+    ap.add_argument("--fusion", choices=["none", "combine", "dx", "default", "all"],
+                    default="default",
+                    help="N2 fusions (k = 1): combine = y written by the second expert GEMM's "
+                         "epilogue; dx = dispatch backward inside the dX GEMM; default = both; "
+                         "all = also gather x rows in the expert GEMMs (TMA gather4)")
     return ap.parse_args()
 
 
@@ -180,7 +182,7 @@ def dist_setup(args):
 # ------------------------------------------------------------------------------------------
 # algorithmic work per kernel: bytes or FLOPs per launch
 # ------------------------------------------------------------------------------------------
-def kernel_work(cfg, T, A, s, A_tok=None, gather=False, fcomb=False):
+def kernel_work(cfg, T, A, s, A_tok=None, gather=False, fcomb=False, fdx=False):
     """A: kept rows of this GPU's experts (GEMM work); A_tok: kept pairs of this GPU's tokens
     (dispatch / combine traffic).  Equal on one GPU.  gather: N2 fusion on (the dispatch
     writes only routing tables + the y rows of dropped tokens; the combine is in FWD2)."""
@@ -204,7 +206,9 @@ def kernel_work(cfg, T, A, s, A_tok=None, gather=False, fcomb=False):
         "wgrad_w1": ("flop", gf), "dgrad_dX": ("flop", gf),
         # db1 partial reduction (fixed order over 8 partial rows per 256-row m-tile)
         "bias_grad": ("byte", ((A // 256) + n) * 8 * f * 4 + n * f * s),
-        "gate_dx": ("byte", (A + T) * d * s + 4 * T * n + 8 * T * k),
+        # fused (dx): only the dropped tokens, dx = dl W_g (dl row + W_g from L2 + dx row)
+        "gate_dx": ("byte", ((T - A) * (d * s + 4 * n) + 4 * T * k) if fdx
+                    else ((A + T) * d * s + 4 * T * n + 8 * T * k)),
         "gate_dw": ("byte", T * d * s + 4 * T * n),
     }
 
@@ -252,10 +256,11 @@ def run_ours(args):
             layer.peer_attach([layer.peer_window()])
     layer.set_capacity_factors([alpha] * n, T * (ws if use_ep else 1))
     # N2 fusions (moe_set_fusion): gather x rows in the expert GEMMs, combine in FWD2 (k = 1)
-    fflags = {"none": 0, "combine": 2, "all": 3}[args.fusion]
+    fflags = {"none": 0, "combine": 2, "dx": 4, "default": 6, "all": 7}[args.fusion]
     tc1 = not use_ep and cfg.dtype == "bf16" and getattr(layer, "uses_tcgen05", False)
     gather = tc1 and bool(fflags & 1) and d % 128 == 0 and f % 128 == 0
     fcomb = tc1 and bool(fflags & 2) and k == 1 and do % 128 == 0 and not args.cached
+    fdx = tc1 and bool(fflags & 4) and k == 1 and d % 128 == 0
     layer.set_fusion(fflags)
     tdt = layer.tdtype
     grads = dict(dx=torch.empty(T, d, dtype=tdt, device=dev),
@@ -362,7 +367,7 @@ def run_ours(args):
 
     # ---------------- per-kernel rooflines ----------------
     pk = peaks()
-    work = kernel_work(cfg, T, A, s, A_tok, gather=gather, fcomb=fcomb)
+    work = kernel_work(cfg, T, A, s, A_tok, gather=gather, fcomb=fcomb, fdx=fdx)
     sm_peak_tf = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
     kernels = {}
     for name, (cnt, tot) in ktimes.items():
@@ -476,8 +481,8 @@ def run_ours(args):
                                        + ("peer memory, device-initiated)" if peer else "NCCL)")
                                        if use_ep else "1 GPU"),
                        "l2": "inputs > L2 (x 134 MB + weights 1 GB), no flush",
-                       "fusion": "+".join([nm for nm, on in (("gather", gather), ("combine", fcomb))
-                                           if on]) or "none",
+                       "fusion": "+".join([nm for nm, on in (("gather", gather), ("combine", fcomb),
+                                                             ("dx", fdx)) if on]) or "none",
                        "kept_assignments": A, "drops": stats["drops"],
                        "padding_flops_avoided": padded_flops},
             "roofline": roofline,

@@ -325,9 +325,9 @@ MOE_API moe_status_t moe_peer_attach(moe_handle_t h, void* const* windows /* hos
 MOE_API moe_status_t moe_peer_import(moe_handle_t h, const void* handles /* host [R][64] */);
 
 /* N2 fusions of the single-GPU tcgen05 path, a bitmask of moe_fusion_t;
-   default MOE_FUSE_COMBINE (GATHER is opt-in: on B200 the TMA gather4 stream is slower than
-   the dispatch copy it replaces).  Results are bitwise identical with and
-   without them (same products, same accumulation order).
+   default MOE_FUSE_COMBINE | MOE_FUSE_DX (GATHER is opt-in: on B200 the TMA gather4 stream
+   is slower than the dispatch copy it replaces).  GATHER and COMBINE give
+   bitwise identical results (same products, same accumulation order); DX see below.
    MOE_FUSE_GATHER: the expert GEMMs that read x rows (H = relu(X W1^T + b1) and
      dW1 = dA^T X) load them straight from the caller's x by TMA gather4 through
      token_of_slot, so the dispatch step (GroupBy) writes only the routing tables and
@@ -337,8 +337,15 @@ MOE_API moe_status_t moe_peer_import(moe_handle_t h, const void* handles /* host
    MOE_FUSE_COMBINE (k == 1, world_size == 1, bf16, no cached indices, no AggregateSpec
      outputs, d_out a multiple of 128): the second expert GEMM's epilogue writes y[t] = w[t] O[row]
      (Alg. 1 l.8) next to O and the dispatch zeroes the y rows of dropped tokens, so no
-     separate combine pass re-reads O.  Takes effect at the next moe_forward. */
-typedef enum { MOE_FUSE_GATHER = 1, MOE_FUSE_COMBINE = 2 } moe_fusion_t;
+     separate combine pass re-reads O.  Takes effect at the next moe_forward.
+   MOE_FUSE_DX (k == 1, world_size == 1, bf16, d a multiple of 128, dx requested): the
+     dispatch backward (dx[t] = dX[row] + dl[t] W_g) runs inside the dX = dA W1 GEMM --
+     extra k-blocks accumulate [hi|lo](dl) [W_g; W_g] into the same fp32 accumulator and the
+     epilogue writes dx rows directly (no dX buffer, no separate pass); tokens whose pair was
+     dropped get dx = dl W_g from a small kernel.  NOT bitwise equal to the unfused path (dX
+     is no longer rounded to bf16 before the sum -- one rounding instead of two); within the
+     bf16 tolerance of the oracle. */
+typedef enum { MOE_FUSE_GATHER = 1, MOE_FUSE_COMBINE = 2, MOE_FUSE_DX = 4 } moe_fusion_t;
 MOE_API moe_status_t moe_set_fusion(moe_handle_t h, int32_t flags);
 
 /* Number of kernels the library launched since the handle was created (for bench

@@ -51,6 +51,9 @@ struct GateDxParams {
   int accumulate;
   CapTable ct;
   PeerBufs pdx;                // peer EP (N1): dX rows read from the owners; grow encodes owner
+  int drop_only;               // fused dX GEMM (k = 1): only tokens with every pair dropped
+                               // (dx = dl W_g); the others were written by the dX GEMM
+  const int32_t* tile_drop;    // [T / 128] routing tiles holding a dropped token (drop_only)
 };
 
 // dX row of a gather-table entry (peer EP: owner in the top bits, see MOE_GROW_SHIFT)
@@ -404,10 +407,29 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
   }
   Bars b = setup_bars<STAGES>(smem + STAGES * STAGE_BYTES, 2 * BN, warp, lane, 256);
   const uint32_t tmem_base = *b.tmem;
-  const int MT = (p.T + TC_BM - 1) / TC_BM;
+  int MT = (p.T + TC_BM - 1) / TC_BM;
   const int NT = p.d / BN;
   const int nb = p.n_pad / TC_BK;
   const int nk = 2 * nb;
+  // drop_only: only the 128-token tiles that hold a dropped token, in order (the same list
+  // in every role); s_mt[i] = token tile of the i-th
+  __shared__ int32_t s_mt[MOE_MAX_DROP_TILES];
+  __shared__ int32_t s_nmt;
+  if (p.drop_only) {
+    if (warp == 3) {
+      int cnt = 0;
+      for (int b0 = 0; b0 < MT; b0 += 32) {
+        const bool f = b0 + lane < MT && p.tile_drop[b0 + lane] != 0;
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (f) s_mt[cnt + __popc(m & ((1u << lane) - 1u))] = b0 + lane;
+        cnt += __popc(m);
+      }
+      if (lane == 0) s_nmt = cnt;
+    }
+    __syncthreads();
+    MT = s_nmt;
+  }
+  auto mtile = [&](int t) { return p.drop_only ? s_mt[t % MT] : t % MT; };
   const int total = MT * NT;
 
   if (warp == 0) {
@@ -415,7 +437,7 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int mt = t % MT, nt = t / MT;
+        const int mt = mtile(t), nt = t / MT;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&b.empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -475,7 +497,7 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
     const int kk = p.k;
     auto stg = [&](int par, int r) { return stg_w + (par * KS + r) * 32 * RS; };
     auto load_rows = [&](int tile, int* rows) {
-      const int t = (tile % MT) * TC_BM + q * 32 + lane;
+      const int t = (tile < total ? mtile(tile) : 0) * TC_BM + q * 32 + lane;
 #pragma unroll
       for (int r = 0; r < MOE_MAX_K; ++r)
         rows[r] = (tile < total && t < p.T && r < kk) ? p.grow[(size_t)t * kk + r] : -1;
@@ -489,7 +511,7 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; i += RPI) {
             const int rowid = __shfl_sync(0xffffffffu, rows[r], i + sub);
-            if (rowid >= 0)
+            if (rowid >= 0 && !p.drop_only)
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                                smem_u32(stg(par, r) + (i + sub) * RS + seg * 16)),
                            "l"(gdx_row<PEER>(p, rowid) + col_base + seg * 8)
@@ -505,7 +527,7 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
     issue_gather(tile, 0, rows_cur);
     for (int it = 0; tile < total; tile += gridDim.x, ++it) {
       const int acc = it & 1, par = it & 1;
-      const int mt = tile % MT, nt = tile / MT;
+      const int mt = mtile(tile), nt = tile / MT;
       const int t0w = mt * TC_BM + q * 32;
       const int t = t0w + lane;
       const bool valid = t < p.T;
@@ -520,7 +542,7 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
 #pragma unroll
       for (int r = 0; r < MOE_MAX_K; ++r) {  // expert path first, r order (as the SIMT form)
         if (r >= kk) break;
-        if (rows_cur[r] < 0) continue;
+        if (rows_cur[r] < 0 || p.drop_only) continue;
         if (r < KS) {
 #pragma unroll
           for (int c = 0; c < HC / 8; ++c) {
@@ -569,7 +591,8 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
 #pragma unroll
       for (int i = 0; i < 32; i += RPI) {
         const int tok = t0w + i + sub;
-        if (tok < p.T)
+        const bool mine = !p.drop_only || __shfl_sync(0xffffffffu, rows_cur[0], i + sub) < 0;
+        if (tok < p.T && mine)
           st_v4(p.dx + (size_t)tok * p.d + col_base + seg * 8,
                 *reinterpret_cast<const uint4*>(stg(par, 0) + (i + sub) * RS + seg * 16));
       }
@@ -793,7 +816,7 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
 cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb, int maxT,
                               int n_pad, RouteBufs b, int T, int k, int n, int d,
                               const CapTable& ct, void* dx, int accumulate, cudaStream_t s,
-                              const PeerBufs& pdx) {
+                              const PeerBufs& pdx, int drop_only) {
   if (T == 0) return cudaSuccess;
   if (!enc_init()) return cudaErrorNotSupported;
   CUtensorMap mhi, mlo, mw;
@@ -807,6 +830,8 @@ cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb
   p.dxbuf = (const __nv_bfloat16*)dxbuf; p.dx = (__nv_bfloat16*)dx; p.accumulate = accumulate;
   p.ct = ct;
   p.pdx = pdx;
+  p.drop_only = drop_only;
+  p.tile_drop = b.tile_drop;
   const int bn = d % 128 == 0 ? 128 : 64;
   const int total = ((T + 127) / 128) * (d / bn);
   const int grid = total < g_sms ? total : g_sms;

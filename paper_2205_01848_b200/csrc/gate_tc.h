@@ -11,7 +11,7 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
 cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb, int maxT,
                               int n_pad, RouteBufs b, int T, int k, int n, int d,
                               const CapTable& ct, void* dx, int accumulate, cudaStream_t s,
-                              const PeerBufs& pdx = PeerBufs{});
+                              const PeerBufs& pdx = PeerBufs{}, int drop_only = 0);
 cudaError_t launch_gate_dw_tc(const void* dlb, int maxT, int n_pad, const void* x, int T, int n,
                               int d, float* partial, void* dwg, int accumulate, cudaStream_t s,
                               float* f32_out = nullptr);

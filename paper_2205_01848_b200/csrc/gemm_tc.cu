@@ -400,7 +400,8 @@ static cudaError_t launch_tc_bn(int N, const CUtensorMap& a, const CUtensorMap& 
 static int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64); }
 
 cudaError_t launch_tc2_kind(int kind, int BN, const CUtensorMap& a, const CUtensorMap& b,
-                            const CUtensorMap& c, const TcParams& p, int grid, cudaStream_t s);
+                            const CUtensorMap& c, const TcParams& p, int grid, cudaStream_t s,
+                            const CUtensorMap* a2 = nullptr, const CUtensorMap* b2 = nullptr);
 
 static int tc_pf() {  // MOE_TC_PF: k-blocks of B prefetched to L2 for the next wave
   static int v = -1;
@@ -412,7 +413,8 @@ static int tc_pf() {  // MOE_TC_PF: k-blocks of B prefetched to L2 for the next 
 }
 
 static int tc_dbg() {  // MOE_TC_DBG: timing experiments only (1: skip epilogue stores,
-                       // 2: skip the db1 partials, 4: skip the relu-mask loads)
+                       // 2: skip the db1 partials, 4: skip the relu-mask loads,
+                       // 8: skip only the TMA store instruction, 16: all stores to rows 0..127)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("MOE_TC_DBG");
@@ -447,6 +449,7 @@ bool tc_gather_supported(int d, int f) {
   return use_2cta(f, TC_FWD1) && use_2cta(d, TC_WGRAD) && d % 64 == 0;
 }
 bool tc_combine_supported(int dout) { return use_2cta(dout, TC_FWD2); }
+bool tc_dx_fusion_supported(int d) { return use_2cta(d, TC_DGRAD_X); }
 
 // db[e][c] = sum of the DGRAD_A column-sum partials of expert e, fixed order (deterministic).
 __global__ void bias_part_reduce_kernel(const float* __restrict__ part,
@@ -501,7 +504,13 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   const bool two = use_2cta(N, KIND);
   const bool gat = KIND == TC_FWD1 && fz && fz->x;        // A rows gathered from x (N2)
   const bool comb = KIND == TC_FWD2 && fz && fz->y;       // fused combine (N2, k = 1)
-  if ((gat || comb) && !two) return MOE_ERR_CONFIG;
+  const bool fdx = KIND == TC_DGRAD_X && fz && fz->dx;    // fused dispatch backward (k = 1)
+  if ((gat || comb || fdx) && !two) return MOE_ERR_CONFIG;
+  CUtensorMap ma2, mb2;
+  if (fdx) {
+    TC_TRY(make_map(&ma2, fz->dlr, 2 * fz->n_pad, rows, 64, 128));
+    TC_TRY(make_map(&mb2, fz->wg, N, fz->n, 64, 64));
+  }
   if (gat)
     TC_TRY(make_map(&ma, fz->x, K, (uint64_t)fz->T, 64, 1));
   else
@@ -525,13 +534,21 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
     p.y = (__nv_bfloat16*)fz->y;
     p.wt = fz->w;
   }
+  if (fdx) {
+    p.gtos = fz->tos;
+    p.dxo = (__nv_bfloat16*)fz->dx;
+    p.nkx = 2 * fz->n_pad / 64;
+    p.nbx = fz->n_pad / 64;
+    p.accumulate = fz->accumulate;
+  }
   p.sched = tc_sched();
   p.pf_kb = tc_pf();
   p.dbg = tc_dbg();
   if (two) {
     CUtensorMap mc;
     TC_TRY(make_store_map(&mc, C, ldc, rows));
-    TC_CUDA(launch_tc2_kind(KIND, bn, ma, mb, mc, p, g_num_sms & ~1, s));
+    TC_CUDA(launch_tc2_kind(KIND, bn, ma, mb, mc, p, g_num_sms & ~1, s, fdx ? &ma2 : nullptr,
+                            fdx ? &mb2 : nullptr));
   } else {
     TC_CUDA(launch_tc_bn<KIND>(N, ma, mb, p, s));
   }
@@ -651,7 +668,8 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   // dX = dA W1_e, W1_e stored [f x d] = [K x N]
   {
     ProfScope ps(prof, "dgrad_dX", s);
-    st = mgroup<TC_DGRAD_X>(H, rows, f, w1, d, n_local, nullptr, dX, d, kept, mtile_prefix, ct, s);
+    st = mgroup<TC_DGRAD_X>(H, rows, f, w1, d, n_local, nullptr, dX, d, kept, mtile_prefix, ct, s,
+                            nullptr, nullptr, fz);
   }
   if (st != MOE_OK) return st;
   ++nl;

@@ -25,9 +25,15 @@ struct TcFusion {
   int k = 1;
   void* y = nullptr;              // y [T, d_out]; null = separate combine kernel
   const float* w = nullptr;       // gate weights [T] (k = 1)
+  // dispatch backward in the dX GEMM (k = 1): dx[t] = dA[row] W1 + [hi|lo](dl)[row] [W_g;W_g]
+  void* dx = nullptr;             // dx [T, d]; null = dX buffer + gate_dx kernel
+  const void* dlr = nullptr;      // [rows, 2 n_pad] bf16 hi | lo of dl in expert-row order
+  const void* wg = nullptr;       // W_g [n, d]
+  int n = 0, n_pad = 64, accumulate = 0;
 };
 bool tc_gather_supported(int d, int f);     // 2-CTA kernels for FWD1 (N = f) and WGRAD_W1 (N = d)
 bool tc_combine_supported(int dout);        // 2-CTA kernel for FWD2 (N = d_out)
+bool tc_dx_fusion_supported(int d);         // 2-CTA kernel for DGRAD_X (N = d)
 
 // Forward: H = relu(X W1_e^T + b1_e), O = H W2_e^T + b2_e over kept_e rows per local expert.
 moe_status_t tc_ffn_forward(TcPlan* p, void* X, const void* w1, const void* b1,

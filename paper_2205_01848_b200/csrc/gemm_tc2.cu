@@ -126,7 +126,8 @@ constexpr int TC2_NBUF = MOE_TC2_NBUF;  // staging buffers per epilogue warp
 template <int KIND, int BN, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmC, TcParams p) {
+                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
+                    const __grid_constant__ CUtensorMap tmB2, TcParams p) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   using Tr = KindTraits<KIND>;
   constexpr int BNH = BN / 2;                    // B columns held by each CTA
@@ -176,6 +177,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (KIND == TC_DGRAD_X && p.nkx) {
+      prefetch_tmap(&tmA2);
+      prefetch_tmap(&tmB2);
+    }
     prefetch_tmap(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -292,7 +297,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             }
           }
         }
-        for (int kb = 0; kb < nk; ++kb) {
+        const int nkt = nk + (KIND == TC_DGRAD_X ? p.nkx : 0);
+        for (int kb = 0; kb < nkt; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           // the bias warps observe every use of every stage (in lockstep with empty[s], so
           // parities cannot alias); the stage is refilled only after they released it
@@ -302,18 +308,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           const uint32_t fb = mapa_rank(smem_u32(&full_bar[stage]), 0);
           if (leader) mbar_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
           const int k0 = kb * TC_BK;
-          if (Tr::a_mn) {
-            tma_load_2d_2sm(sa, &tmA, fb, m0, base + k0);
-            tma_load_2d_2sm(sa + 8192, &tmA, fb, m0 + 64, base + k0);
-          } else {
-            tma_load_2d_2sm(sa, &tmA, fb, k0, base + m0);
-          }
-          if (Tr::b_mn) {
-            const int krow = Tr::kgroup ? base + k0 : e * p.K + k0;
+          if (KIND == TC_DGRAD_X && kb >= nk) {  // gate term: [hi|lo](dl) rows x [W_g ; W_g]
+            const int kx = kb - nk;
+            tma_load_2d_2sm(sa, &tmA2, fb, kx * TC_BK, base + m0);
 #pragma unroll
-            for (int j = 0; j < BNH / 64; ++j) tma_load_2d_2sm(sb + j * 8192, &tmB, fb, n0 + j * 64, krow);
+            for (int j = 0; j < BNH / 64; ++j)
+              tma_load_2d_2sm(sb + j * 8192, &tmB2, fb, n0 + j * 64, (kx % p.nbx) * TC_BK);
           } else {
-            tma_load_2d_2sm(sb, &tmB, fb, k0, e * p.N + n0);
+            if (Tr::a_mn) {
+              tma_load_2d_2sm(sa, &tmA, fb, m0, base + k0);
+              tma_load_2d_2sm(sa + 8192, &tmA, fb, m0 + 64, base + k0);
+            } else {
+              tma_load_2d_2sm(sa, &tmA, fb, k0, base + m0);
+            }
+            if (Tr::b_mn) {
+              const int krow = Tr::kgroup ? base + k0 : e * p.K + k0;
+#pragma unroll
+              for (int j = 0; j < BNH / 64; ++j)
+                tma_load_2d_2sm(sb + j * 8192, &tmB, fb, n0 + j * 64, krow);
+            } else {
+              tma_load_2d_2sm(sb, &tmB, fb, k0, e * p.N + n0);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -330,7 +345,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         int e, mt, nt;
         if (!decode_tile_ord<Tr::kgroup>(t, s_prefix, n_local, MT, NT, nfast, e, mt, nt)) break;
         const int acc = it & 1;
-        const int nk = Tr::kgroup ? (p.kept[e] + TC_BK - 1) / TC_BK : p.K / TC_BK;
+        const int nk = (Tr::kgroup ? (p.kept[e] + TC_BK - 1) / TC_BK : p.K / TC_BK) +
+                       (KIND == TC_DGRAD_X ? p.nkx : 0);
         mbar_wait_cluster(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
@@ -461,6 +477,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         ytok = p.gtos[p.ct.base[e] + row];
         yw = p.wt[ytok];
       }
+      if (KIND == TC_DGRAD_X && p.dxo != nullptr && row_ok) ytok = p.gtos[p.ct.base[e] + row];
       const bool need_side = ((KIND == TC_FWD1 || KIND == TC_FWD2) && row_ok) ||
                              (KIND == TC_WGRAD && row_ok && p.accumulate);
       if (need_side) {
@@ -521,29 +538,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.f;
           }
-          if (p.bias_part && !(p.dbg & 2)) {
-            // db1 = sum over kept tokens of dA (the stored bf16 values): column sums of this
-            // warp's 32 rows by a transpose-reduce over the lanes (31 shuffles; lane j ends
-            // with column j), parked in shared memory; after the tile the 4 row-quarter warps
-            // of this column half are summed in fixed order (below) into one partial row per
-            // (m-tile, CTA) that a fixed-order kernel reduces per expert: deterministic.
-            float cs[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) cs[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
-              const bool up = (lane & off) != 0;
-#pragma unroll
-              for (int i = 0; i < off; ++i) {
-                const float send = up ? cs[i] : cs[i + off];
-                const float keep = up ? cs[i + off] : cs[i];
-                cs[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-              }
-            }
-            s_red[(((it & 1) * 2 + half) * 4 + q) * (CH * 32) + cc * 32 + lane] = cs[0];
-          }
         } else if (KIND == TC_DGRAD_X) {
           store = row_ok;
+          if (p.dxo != nullptr && p.accumulate && ytok >= 0) {
+            // dispatch backward (k = 1), accumulating: add the old dx before the one rounding
+            const __nv_bfloat16* drow = p.dxo + (size_t)ytok * p.N + col0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              float o[8];
+              unpack(ld_v4(drow + i), o, __nv_bfloat16());
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[i + j] += o[j];
+            }
+          }
         } else {  // WGRAD
           store = row_ok;
           if (row_ok && p.accumulate) {
@@ -562,6 +569,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         // it: padded kinds (FWD1, DGRAD_A) store boxes below roundup(M_e, 64) (rows >= M_e are
         // zeros), the others boxes below roundup(M_e, 32) (rows >= M_e: zeros, never read).
         bool box;
+        const bool red_on = KIND == TC_DGRAD_A && p.bias_part != nullptr && !(p.dbg & 2);
         if (Tr::kgroup) box = blk_row < p.M;
         else if (KIND == TC_FWD1 || KIND == TC_DGRAD_A) box = blk_row < ((Me + 63) & ~63);
         else box = blk_row < Me;
@@ -570,6 +578,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           for (int i = 0; i < 32; ++i) v[i] = 0.f;
         }
         if (p.dbg & 1) box = false;
+        if (red_on && !box && lane < 16)  // rows of this warp all past the padded end: zeros
+          *reinterpret_cast<float2*>(s_red + (((it & 1) * 2 + half) * 4 + q) * (CH * 32) +
+                                     cc * 32 + 2 * lane) = make_float2(0.f, 0.f);
         if (box) {
           uint4 pk[4];
 #pragma unroll
@@ -582,21 +593,73 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             *reinterpret_cast<uint4*>(stg + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4)) = pk[i];
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0)
+          const bool rowstore = KIND == TC_DGRAD_X && p.dxo != nullptr;  // token rows instead
+          if (rowstore) {
+            // dispatch backward (k = 1): dx[t] = dX[row] + dl[t] W_g, both in this fp32
+            // accumulator, rounded once; the staged box leaves as 64-byte row segments to the
+            // tokens' dx rows (lane: row 8i + l/4, 16-byte chunk l%4; token from its lane)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = i * 8 + (lane >> 2), c = lane & 3;
+              const int tok = __shfl_sync(0xffffffffu, ytok, r);
+              if (tok >= 0)
+                st_v4(p.dxo + (size_t)tok * p.N + col0 + c * 8,
+                      *reinterpret_cast<const uint4*>(stg + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)));
+            }
+          }
+          if (lane == 0 && !(p.dbg & 8) && !rowstore)
             tma_store_2d(&tmC, stg, col0,
-                         Tr::kgroup ? e * p.M + blk_row : p.ct.base[e] + blk_row);
-          if (KIND == TC_FWD2 && ytok >= 0) {
+                         (p.dbg & 16) ? (blk_row & 127)
+                                      : (Tr::kgroup ? e * p.M + blk_row : p.ct.base[e] + blk_row));
+          if (KIND == TC_DGRAD_A && red_on) {
+            // db1 = sum over kept tokens of dA (the stored bf16 values, rows >= kept are 0):
+            // column sums of this warp's 32 rows read back from the staged box.  Lane l sums
+            // columns 2(l%16), 2(l%16)+1 over rows 2i + l/16 (conflict-free), then the two row
+            // halves; parked in shared memory for the fixed-order quarter sum after the tile.
+            const int cp = lane & 15, rh = lane >> 4;
+            float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int r = 2 * i + rh;
+              const uint32_t w = *reinterpret_cast<const uint32_t*>(
+                  stg + r * 64 + (((cp >> 2) ^ ((r >> 1) & 3)) << 4) + (cp & 3) * 4);
+              s0 += __uint_as_float(w << 16);
+              s1 += __uint_as_float(w & 0xffff0000u);
+            }
+            s0 += __shfl_down_sync(0xffffffffu, s0, 16);
+            s1 += __shfl_down_sync(0xffffffffu, s1, 16);
+            if (lane < 16)
+              *reinterpret_cast<float2*>(s_red + (((it & 1) * 2 + half) * 4 + q) * (CH * 32) +
+                                         cc * 32 + 2 * cp) = make_float2(s0, s1);
+          }
+          if (KIND == TC_FWD2 && p.y != nullptr) {
             // Alg. 1 l.8 for k = 1: y[t] = 0 + w O[row] from the stored (bf16) O, the same
-            // arithmetic as the combine kernel (bitwise equal)
-            __nv_bfloat16* yrow = p.y + (size_t)ytok * p.N + col0;
+            // arithmetic as the combine kernel (bitwise equal).  Staged in the box buffer once
+            // the O store has read it, then written as 64-byte row segments of y.
+            uint4 yk[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               float o[8];
               unpack(pk[i], o, __nv_bfloat16());
 #pragma unroll
               for (int j = 0; j < 8; ++j) o[j] = fmaf(yw, o[j], 0.f);
-              st_v4(yrow + 8 * i, pack(o, __nv_bfloat16()));
+              yk[i] = pack(o, __nv_bfloat16());
             }
+            if (lane == 0) tma_store_wait_read<0>();
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              *reinterpret_cast<uint4*>(stg + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4)) = yk[i];
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = i * 8 + (lane >> 2), c = lane & 3;
+              const int tok = __shfl_sync(0xffffffffu, ytok, r);
+              if (tok >= 0)
+                st_v4(p.y + (size_t)tok * p.N + col0 + c * 8,
+                      *reinterpret_cast<const uint4*>(stg + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)));
+            }
+            __syncwarp();
           }
           if (KIND == TC_FWD1) {  // bit j: the stored bf16 H is > 0 (relu output >= 0)
             uint32_t bits = 0;
@@ -655,7 +718,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 // ------------------------------------------------------------------------------ host side
 template <int KIND, int BN>
 static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                           const TcParams& p, int grid, cudaStream_t s) {
+                           const CUtensorMap& a2, const CUtensorMap& b2, const TcParams& p,
+                           int grid, cudaStream_t s) {
   constexpr int STAGES = (BN == 256) ? (TC2_NBUF > 1 ? 5 : 6) : 8;
   constexpr int STAGE_BYTES = (TC_BM + BN / 2) * TC_BK * 2;
   const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 512 + 4 * (MOE_MAX_E + 8) + 2048 +
@@ -668,16 +732,19 @@ static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const CUt
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  launch_pdl(kf, grid, TC_THREADS, smem, s, a, b, c, p);
+  launch_pdl(kf, grid, TC_THREADS, smem, s, a, b, c, a2, b2, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tc2_kind(int kind, int BN, const CUtensorMap& a, const CUtensorMap& b,
-                            const CUtensorMap& c, const TcParams& p, int grid, cudaStream_t s) {
+                            const CUtensorMap& c, const TcParams& p, int grid, cudaStream_t s,
+                            const CUtensorMap* a2, const CUtensorMap* b2) {
+  const CUtensorMap& A2 = a2 ? *a2 : a;
+  const CUtensorMap& B2 = b2 ? *b2 : b;
 #define K2(KD)                                                                         \
   case KD:                                                                             \
-    return BN == 256 ? launch2<KD, 256>(a, b, c, p, grid, s)                           \
-                     : launch2<KD, 128>(a, b, c, p, grid, s);
+    return BN == 256 ? launch2<KD, 256>(a, b, c, A2, B2, p, grid, s)                   \
+                     : launch2<KD, 128>(a, b, c, A2, B2, p, grid, s);
   switch (kind) {
     K2(TC_FWD1) K2(TC_FWD2) K2(TC_DGRAD_A) K2(TC_DGRAD_X) K2(TC_WGRAD)
     default: return cudaErrorInvalidValue;

@@ -41,6 +41,11 @@ struct TcParams {
   // N2 combine fusion (FWD2, k = 1): y[t] = w[t] * O[row] written by the epilogue next to O.
   __nv_bfloat16* y;
   const float* wt;
+  // N2 dispatch-backward fusion (DGRAD_X, k = 1): nkx extra k-blocks accumulate the gate term
+  // dl[t] W_g (A2 = [hi | lo](dl) rows in expert-row order, B2 = W_g, nbx = n_pad / 64), and
+  // the epilogue writes dx[t] (token order, via gtos) instead of the dX buffer.
+  __nv_bfloat16* dxo;
+  int nkx, nbx;
   CapTable ct;                  // base rows of each local expert region
 };
 

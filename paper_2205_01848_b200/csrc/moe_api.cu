@@ -34,7 +34,7 @@ int moe::pdl_enabled() {
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
       xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, grow, ep_all, sendbuf, oret, dwg32,
-      pre_dev, total;
+      pre_dev, dlr, tdrop, total;
 };
 
 struct moe_ctx {
@@ -65,7 +65,7 @@ struct moe_ctx {
   moe_fwd_args_t fa{};
   int64_t launches = 0;
   int use_tc = 0;             // tcgen05 path for bf16 (env MOE_FORCE_SIMT=1 disables)
-  int fusion = MOE_FUSE_COMBINE;  // N2 fusions allowed (moe_set_fusion; GATHER is opt-in)
+  int fusion = MOE_FUSE_COMBINE | MOE_FUSE_DX;  // N2 fusions (moe_set_fusion; GATHER opt-in)
   int fused_gather = 0;       // the last forward gathered x rows in the GEMMs (no X buffer)
   TcPlan tc{};
   Prof prof;
@@ -151,6 +151,9 @@ void compute_layout(moe_ctx* h) {
   L.bal = take(((T + 63) / 64 + 3) * n * 4 + 256);
   L.grow = take(T * k * 4);
   L.bpart = take(h->dtype == MOE_BF16 ? ((size_t)h->rows / 256 + h->n_local) * 2 * h->f * 4 : 0);
+  // fused dispatch backward (k = 1, one GPU): [hi | lo](dl) by expert row
+  L.tdrop = take(ntiles * 4);
+  L.dlr = take(h->dtype == MOE_BF16 && k == 1 && !h->use_ep ? (size_t)h->rows * 2 * h->n_pad * 2 : 0);
   const bool ep = h->use_ep && !h->use_peer;  // NCCL transport buffers
   L.pre_dev = take(n * 4);
   L.ep_all = take(ep ? (size_t)h->R * n * 4 : 0);
@@ -183,6 +186,7 @@ void bind_buffers(moe_ctx* h) {
   r.ticket = (uint32_t*)(meta + 782);
   r.token_of_slot = h->use_peer ? (int32_t*)(h->pwin + h->PL.tos) : (int32_t*)(b + L.token_of_slot);
   r.grow = (int32_t*)(b + L.grow);
+  r.tile_drop = (int32_t*)(b + L.tdrop);
 }
 
 void relayout(moe_ctx* h) {
@@ -687,6 +691,13 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   rb.bal_g = h->balance_lambda != 0.f
                  ? (const float*)(ws + h->L.bal) + (size_t)((h->maxT + 63) / 64) * n + n
                  : nullptr;
+  // N2 dispatch backward fused into the dX GEMM (k = 1, one GPU, tcgen05): the combine
+  // backward also writes [hi|lo](dl) by expert row, the GEMM adds dl W_g and writes dx rows
+  const bool fdx = h->use_tc && !h->use_ep && k == 1 && (h->fusion & MOE_FUSE_DX) && T > 0 &&
+                   a->dx != nullptr && ((uintptr_t)a->dx % 16) == 0 && tc_dx_fusion_supported(d) &&
+                   (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE <= MOE_MAX_DROP_TILES;
+  rb.dlr = fdx ? (__nv_bfloat16*)(ws + h->L.dlr) : nullptr;
+
   KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O_tok, rb, T, k, n, dout, h->renorm, h->cts,
                                                      dO_tok, dlb, h->maxT, h->n_pad,
                                                      nccl_ep ? nullptr : rb.kept, s0,
@@ -696,6 +707,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   rb.dspec = nullptr;
   rb.dw_ext = nullptr;
   rb.bal_g = nullptr;
+  rb.dlr = nullptr;
   if (peer) {  // N1: dO rows were stored into the owners by the combine backward
     KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DO, s0, (uint32_t*)rb.flags));
   } else if (h->use_ep) {  // C4: dO rows to the expert owners
@@ -712,17 +724,23 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   if (h->use_tc) {
     int64_t nk = 0;
     TcFusion fz;  // N2: dW1 = dA^T X gathers the x rows like the forward did
-    if (h->fused_gather) {
-      fz.x = fa.x;
-      fz.T = T;
-      fz.tos = rb.token_of_slot;
-      fz.k = k;
+    fz.T = T;
+    fz.tos = rb.token_of_slot;
+    fz.k = k;
+    if (h->fused_gather) fz.x = fa.x;
+    if (fdx) {
+      fz.dx = a->dx;
+      fz.dlr = ws + h->L.dlr;
+      fz.wg = fa.w_gate;
+      fz.n = n;
+      fz.n_pad = h->n_pad;
+      fz.accumulate = acc;
     }
     moe_status_t st = tc_ffn_backward(&h->tc, X, H, dO, dXb, w1, w2, dw1, db1, dw2, db2, acc,
                                       h->rows, d, f, dout, kept_local, rb.mtile_prefix, nl,
                                       h->ct, h->max_cap_local, s0, &nk, &h->prof,
                                       (uint32_t*)(ws + h->L.mask), (float*)(ws + h->L.bpart),
-                                      h->fused_gather ? &fz : nullptr);
+                                      (h->fused_gather || fdx) ? &fz : nullptr);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 backward failed");
   } else {
@@ -750,10 +768,10 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
     moe_status_t st = ep_from_experts(h->ep, h->plan, dXb, dX_tok, h->ct, d, (int)h->s, s0, &err);
     if (st != MOE_OK) return fail(h, st, err);
   }
-  if (a->dx) {
+  if (a->dx) {  // fused dX GEMM: it wrote the kept tokens, this pass only the dropped ones
     if (h->use_tc)
       KL(h, T > 0, "gate_dx", s0, launch_gate_dx_tc(fa.w_gate, dX_tok, dlb, h->maxT, h->n_pad, rb, T, k, n, d,
-                                                    h->cts, a->dx, acc, s0, pdx));
+                                                    h->cts, a->dx, acc, s0, pdx, fdx ? 1 : 0));
     else
       KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dX_tok, rb, T, k, n, d, h->cts, a->dx, acc, s0,
                                                  pdx));
@@ -1036,7 +1054,7 @@ moe_status_t moe_vcomm_destroy(void* comm) { return vcomm_destroy(comm); }
 
 moe_status_t moe_set_fusion(moe_handle_t h, int32_t flags) {
   if (!h) return MOE_ERR_INVALID_ARG;
-  if (flags & ~(MOE_FUSE_GATHER | MOE_FUSE_COMBINE))
+  if (flags & ~(MOE_FUSE_GATHER | MOE_FUSE_COMBINE | MOE_FUSE_DX))
     return fail(h, MOE_ERR_INVALID_ARG, "unknown fusion flag");
   h->fusion = flags;
   return MOE_OK;

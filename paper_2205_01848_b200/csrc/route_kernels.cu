@@ -323,7 +323,8 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
     long long token_base, CapTable ct, const int32_t* __restrict__ tile_off,
     int32_t* __restrict__ slot_of, int32_t* __restrict__ token_of_slot, T* __restrict__ xbuf,
     const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs px, PeerBufs ptos,
-    const int32_t* __restrict__ pre_dev, T* __restrict__ yz, int dout) {
+    const int32_t* __restrict__ pre_dev, T* __restrict__ yz, int dout,
+    int32_t* __restrict__ tile_drop) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   // px.nl != 0 (peer EP, N1): rows go straight into the owners' X buffers over NVLink, the
   // global slot offsets come from the device plan (pre_dev), token_of_slot is the owner's.
@@ -377,7 +378,15 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
       srow[lt * k + r] = row;
     }
   }
-  __syncthreads();
+  {  // does this tile hold a token with every pair dropped? (the fused dX drop pass)
+    bool dtok = false;
+    if (lt < MOE_ROUTE_TILE && t < Tn) {
+      dtok = true;
+      for (int r = 0; r < k; ++r) dtok &= srow[lt * k + r] < 0;
+    }
+    const int any_drop = __syncthreads_or(dtok);
+    if (tile_drop && threadIdx.x == 0) tile_drop[tile] = any_drop;
+  }
   // row copies: warp per token
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int VE = Vec<T>::N;
@@ -436,13 +445,13 @@ cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T,
     launch_pdl(dispatch_kernel<__nv_bfloat16>, ntiles, 256, 0, s, 
         idx, (const __nv_bfloat16*)x, T, k, n, d, token_base, ct, b.tile_off, b.slot_of,
         b.token_of_slot, (__nv_bfloat16*)xbuf, pad_kept, pad_e0, px, ptos, pre_dev,
-        (__nv_bfloat16*)y_zero, dout);
+        (__nv_bfloat16*)y_zero, dout, b.tile_drop);
   else
     launch_pdl(dispatch_kernel<float>, ntiles, 256, 0, s, idx, (const float*)x, T, k, n, d,
                                                   token_base, ct, b.tile_off, b.slot_of,
                                                   b.token_of_slot, (float*)xbuf, pad_kept,
                                                   pad_e0, px, ptos, pre_dev, (float*)y_zero,
-                                                  dout);
+                                                  dout, b.tile_drop);
   return cudaGetLastError();
 }
 
@@ -646,7 +655,7 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
     __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad, const T* __restrict__ dspec,
     const float* __restrict__ dw_ext, const float* __restrict__ bal_g,
     int32_t* __restrict__ grow, const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs po,
-    PeerBufs pdo) {
+    PeerBufs pdo, __nv_bfloat16* __restrict__ dlr) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   // peer EP (N1): O rows are read from, and dO rows written to, the experts' owners
   if (pad_kept)
@@ -804,6 +813,11 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
           __floats2bfloat162_rn(v2[0] - __low2float(hi), v2[1] - __high2float(hi));
       *reinterpret_cast<__nv_bfloat162*>(dlb + (size_t)t * n_pad + e0) = hi;
       *reinterpret_cast<__nv_bfloat162*>(dlb + ((size_t)maxT + t) * n_pad + e0) = lo;
+      if (dlr && rows[0] >= 0) {  // k = 1 fused dispatch backward: the pair by expert row
+        __nv_bfloat16* rr = dlr + (size_t)rows[0] * 2 * n_pad;
+        *reinterpret_cast<__nv_bfloat162*>(rr + e0) = hi;
+        *reinterpret_cast<__nv_bfloat162*>(rr + n_pad + e0) = lo;
+      }
     }
   }
 }
@@ -822,7 +836,7 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
                                                    renorm, (T*)dobuf, b.dw, b.dl,              \
                                                    (__nv_bfloat16*)dlb, maxT, n_pad,           \
                                                    (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow, pad_kept, \
-                                                   pad_e0, po, pdo)
+                                                   pad_e0, po, pdo, b.dlr)
   const int km = k == 1 ? 1 : (k == 2 ? 2 : 8);
   if (vpl <= 2) { if (km == 1) CB(2, 1); else if (km == 2) CB(2, 2); else CB(2, 8); }
   else if (vpl <= 4) { if (km == 1) CB(4, 1); else if (km == 2) CB(4, 2); else CB(4, 8); }

@@ -164,11 +164,12 @@ class MoELayer:
             L.check(self.lib.moe_set_assignment_cache(self.h, None, 0, None, 0), self.h)
 
     # -- N2 fusions ---------------------------------------------------------------------
-    FUSE_GATHER, FUSE_COMBINE = 1, 2
+    FUSE_GATHER, FUSE_COMBINE, FUSE_DX = 1, 2, 4
 
     def set_fusion(self, flags: int):
         """moe_set_fusion: bitmask of FUSE_GATHER (x rows gathered by the expert GEMMs, no X
-        buffer) and FUSE_COMBINE (k = 1: y written by the second GEMM's epilogue)."""
+        buffer), FUSE_COMBINE (k = 1: y written by the second GEMM's epilogue) and FUSE_DX
+        (k = 1: dx = dX + dl W_g written by the dX GEMM).  Default COMBINE | DX."""
         L.check(self.lib.moe_set_fusion(self.h, int(flags)), self.h)
 
     # -- loss variants (N3) -----------------------------------------------------------

@@ -1,9 +1,11 @@
 """N2 fusions (moe_set_fusion): the expert GEMMs gather x rows by
-token_of_slot with TMA gather4 (no dispatched X buffer; opt-in) and, for k = 1, the second GEMM's
-epilogue writes y = w O (no combine pass).  Checked two ways on the same seeded inputs:
-against the fp64 oracle (values within the bf16 budget, routing bit-exact), and against the
-unfused path of the same library, which must be BITWISE equal (same products, same
-accumulation order) -- including at the bench's full c3 size."""
+token_of_slot with TMA gather4 (no dispatched X buffer; opt-in, flag 1); for k = 1 the second
+GEMM's epilogue writes y = w O (no combine pass, flag 2) and the dX GEMM writes
+dx = dX + dl W_g (no dispatch-backward pass, flag 4).  Checked against the fp64 oracle
+(values within the bf16 budget, routing bit-exact) and against the unfused path of the same
+library: BITWISE equal for flags 1 and 2 (same products, same accumulation order); for flag 4
+every output but dx is bitwise equal and dx agrees within the bf16 budget (one rounding
+instead of two) -- including at the bench's full c3 size."""
 import numpy as np
 import pytest
 import torch
@@ -20,7 +22,13 @@ def _run(layer, g, dy, fusion, y_fill=None):
         y = torch.full((g["x"].shape[0], layer.d_out), y_fill, dtype=layer.tdtype,
                        device=layer.device)
     y = layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"], y=y)
-    grads = layer.backward(dy)
+    grads = None
+    if y_fill is not None:   # poison every gradient: all rows must be written
+        shapes = dict(dx=g["x"].shape, dw_gate=g["w_gate"].shape, dw1=g["w1"].shape,
+                      db1=g["b1"].shape, dw2=g["w2"].shape, db2=g["b2"].shape)
+        grads = {kk: torch.full(sh, y_fill, dtype=layer.tdtype, device=layer.device)
+                 for kk, sh in shapes.items()}
+    grads = layer.backward(dy, grads=grads)
     torch.cuda.synchronize()
     return y.clone(), {k: v.clone() for k, v in grads.items()}
 
@@ -33,6 +41,16 @@ def _bitwise(a, b, what):
     assert nbad == 0, f"{what}: {nbad} elements differ between fused and unfused paths"
 
 
+def _close(a, b, what, tol=2e-2):
+    """dx of the fused dispatch backward: one bf16 rounding instead of two (reading 13)."""
+    a, b = a.float(), b.float()
+    den = b.abs().max().item()
+    err = (a - b).abs().max().item() / (den if den > 0 else 1.0)
+    assert err <= tol, f"{what}: rel err {err}"
+    # and far tighter than the budget in practice: a few bf16 ulps
+    assert err <= 1e-2, f"{what}: rel err {err}"
+
+
 CASES = [  # n, k, d, f, T, renorm, regime, alpha
     (8, 1, 256, 512, 1000, 0, "uniform", 1.0),    # gather + fused combine, drops
     (8, 1, 256, 512, 1001, 1, "uniform", 1.25),   # renorm (w = 1), ragged T
@@ -42,7 +60,7 @@ CASES = [  # n, k, d, f, T, renorm, regime, alpha
 ]
 
 
-@pytest.mark.parametrize("fusion", [2, 3])
+@pytest.mark.parametrize("fusion", [2, 3, 4, 7])
 @pytest.mark.parametrize("n,k,d,f,T,renorm,regime,alpha", CASES)
 def test_fused_vs_oracle(n, k, d, f, T, renorm, regime, alpha, fusion):
     from paper_2205_01848_b200 import capacity_from_factors
@@ -68,12 +86,15 @@ def test_fused_bitwise_equals_unfused(n, k, d, f, T, renorm, regime, alpha):
     layer.set_capacities(capacity_from_factors([alpha] * n, T, k))
     y0, g0 = _run(layer, g, dy, 0, y_fill=float("nan"))
     assert not torch.isnan(y0).any()
-    for fusion in (2, 1, 3):   # combine only, gather only, both
+    for fusion in (2, 1, 3, 4, 7):   # combine, gather, both, dx, all
         y1, g1 = _run(layer, g, dy, fusion, y_fill=float("nan"))
         assert not torch.isnan(y1).any()
         _bitwise(y1, y0, f"y (fusion {fusion})")
         for key in g0:
-            _bitwise(g1[key], g0[key], f"{key} (fusion {fusion})")
+            if key == "dx" and fusion & 4 and k == 1:
+                _close(g1[key], g0[key], f"dx (fusion {fusion})")
+            else:
+                _bitwise(g1[key], g0[key], f"{key} (fusion {fusion})")
 
 
 def test_fused_cached_mode_bitwise():
@@ -94,6 +115,10 @@ def test_fused_cached_mode_bitwise():
     _bitwise(y1, y0, "y")
     for key in g0:
         _bitwise(g1[key], g0[key], key)
+    y1, g1 = _run(layer, g, dy, 7, y_fill=float("nan"))
+    _bitwise(y1, y0, "y")
+    for key in g0:
+        (_close if key == "dx" else _bitwise)(g1[key], g0[key], f"{key} (fusion 7)")
 
 
 def test_fused_bitwise_at_bench_size():
@@ -108,11 +133,14 @@ def test_fused_bitwise_at_bench_size():
     layer = MoELayer(n, k, d, f, 0, T, "bf16", 0, device="cuda")
     layer.set_capacities(capacity_from_factors([1.0] * n, T, k))
     y0, g0 = _run(layer, g, dy, 0)
-    for fusion in (3, 2):   # end with the default (combine only) for the sampled check
+    for fusion in (7, 6):   # end with the default (combine + dx) for the sampled check
         y1, g1 = _run(layer, g, dy, fusion, y_fill=float("nan"))
         _bitwise(y1, y0, f"y (fusion {fusion})")
         for key in g0:
-            _bitwise(g1[key], g0[key], f"{key} (fusion {fusion})")
+            if key == "dx":
+                _close(g1[key], g0[key], f"dx (fusion {fusion})")
+            else:
+                _bitwise(g1[key], g0[key], f"{key} (fusion {fusion})")
     # sampled tokens against the definition (fp32 from the same bf16 inputs)
     r = layer.routing(T)
     idx = r["idx"][:, 0].long()
