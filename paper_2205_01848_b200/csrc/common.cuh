@@ -10,7 +10,6 @@
 #define MOE_ROUTE_TILE 128     // tokens per routing tile (histogram / scan granularity)
 #define MOE_ROW_ALIGN 128      // expert buffer regions start at multiples of this many rows
 #define MOE_PAD_ROWS 64        // rows [kept, roundup(kept, PAD)) are zeroed (token-K GEMMs)
-#define MOE_MAX_DROP_TILES 4096 // routing tiles of the fused-dX drop pass (T <= 524288)
 
 namespace moe {
 

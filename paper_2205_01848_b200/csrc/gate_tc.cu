@@ -53,7 +53,8 @@ struct GateDxParams {
   PeerBufs pdx;                // peer EP (N1): dX rows read from the owners; grow encodes owner
   int drop_only;               // fused dX GEMM (k = 1): only tokens with every pair dropped
                                // (dx = dl W_g); the others were written by the dX GEMM
-  const int32_t* tile_drop;    // [T / 128] routing tiles holding a dropped token (drop_only)
+  const int32_t* drop_tok;     // drop_only: [count] token of each compacted dropped row
+  const int32_t* drop_cnt;     // drop_only: [1] number of dropped tokens (combine_bwd)
 };
 
 // dX row of a gather-table entry (peer EP: owner in the top bits, see MOE_GROW_SHIFT)
@@ -411,25 +412,19 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
   const int NT = p.d / BN;
   const int nb = p.n_pad / TC_BK;
   const int nk = 2 * nb;
-  // drop_only: only the 128-token tiles that hold a dropped token, in order (the same list
-  // in every role); s_mt[i] = token tile of the i-th
-  __shared__ int32_t s_mt[MOE_MAX_DROP_TILES];
-  __shared__ int32_t s_nmt;
+  // drop_only: the rows are the dropped tokens compacted by the combine backward (A = their
+  // [hi|lo](dl) rows, token of row i = drop_tok[i]); the same count in every role
+  __shared__ int32_t s_cnt;
+  int rows_valid = p.T;
   if (p.drop_only) {
-    if (warp == 3) {
-      int cnt = 0;
-      for (int b0 = 0; b0 < MT; b0 += 32) {
-        const bool f = b0 + lane < MT && p.tile_drop[b0 + lane] != 0;
-        const unsigned m = __ballot_sync(0xffffffffu, f);
-        if (f) s_mt[cnt + __popc(m & ((1u << lane) - 1u))] = b0 + lane;
-        cnt += __popc(m);
-      }
-      if (lane == 0) s_nmt = cnt;
-    }
+    if (threadIdx.x == 0) s_cnt = *reinterpret_cast<const volatile int32_t*>(p.drop_cnt);
     __syncthreads();
-    MT = s_nmt;
+    rows_valid = s_cnt;
+    MT = (rows_valid + TC_BM - 1) / TC_BM;
   }
-  auto mtile = [&](int t) { return p.drop_only ? s_mt[t % MT] : t % MT; };
+  auto mtile = [&](int t) { return t % MT; };
+  // token of compacted row i (identity unless drop_only), -1 past the end
+  auto tok_of = [&](int i) { return i < rows_valid ? (p.drop_only ? p.drop_tok[i] : i) : -1; };
   const int total = MT * NT;
 
   if (warp == 0) {
@@ -500,7 +495,7 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
       const int t = (tile < total ? mtile(tile) : 0) * TC_BM + q * 32 + lane;
 #pragma unroll
       for (int r = 0; r < MOE_MAX_K; ++r)
-        rows[r] = (tile < total && t < p.T && r < kk) ? p.grow[(size_t)t * kk + r] : -1;
+        rows[r] = (tile < total && !p.drop_only && t < p.T && r < kk) ? p.grow[(size_t)t * kk + r] : -1;
     };
     auto issue_gather = [&](int tile, int par, const int* rows) {
       if (tile < total) {
@@ -529,8 +524,8 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
       const int acc = it & 1, par = it & 1;
       const int mt = mtile(tile), nt = tile / MT;
       const int t0w = mt * TC_BM + q * 32;
-      const int t = t0w + lane;
-      const bool valid = t < p.T;
+      const int t = tok_of(t0w + lane);   // this lane's token (drop_only: compacted row)
+      const bool valid = t >= 0;
       const int col_base = nt * BN + half * HC;
       load_rows(tile + gridDim.x, rows_nxt);
       issue_gather(tile + gridDim.x, par ^ 1, rows_nxt);
@@ -590,9 +585,8 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < 32; i += RPI) {
-        const int tok = t0w + i + sub;
-        const bool mine = !p.drop_only || __shfl_sync(0xffffffffu, rows_cur[0], i + sub) < 0;
-        if (tok < p.T && mine)
+        const int tok = __shfl_sync(0xffffffffu, t, i + sub);
+        if (tok >= 0)
           st_v4(p.dx + (size_t)tok * p.d + col_base + seg * 8,
                 *reinterpret_cast<const uint4*>(stg(par, 0) + (i + sub) * RS + seg * 16));
       }
@@ -831,7 +825,8 @@ cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb
   p.ct = ct;
   p.pdx = pdx;
   p.drop_only = drop_only;
-  p.tile_drop = b.tile_drop;
+  p.drop_tok = b.drop_tok;
+  p.drop_cnt = b.drop_cnt;
   const int bn = d % 128 == 0 ? 128 : 64;
   const int total = ((T + 127) / 128) * (d / bn);
   const int grid = total < g_sms ? total : g_sms;

@@ -33,7 +33,10 @@ struct RouteBufs {
   const float* bal_g;     // [n] balance-term coefficients lambda*n*T_i/T_g (backward)
   int32_t* grow;          // [T x k] token-side dO/dX row of each pair or -1 (combine_bwd)
   __nv_bfloat16* dlr;     // [rows x 2 n_pad] hi | lo of dl by expert row (fused dX, k = 1)
-  int32_t* tile_drop;     // [T / 128] 1 if the routing tile holds a token with every pair dropped
+  __nv_bfloat16* dropb;   // fused dX (k = 1): [2 maxT x n_pad] dl pairs of dropped tokens,
+                          // compacted (dlb layout); null = off
+  int32_t* drop_tok;      // [maxT] token of each compacted row
+  int32_t* drop_cnt;      // [1] rows in the list (reset by route_scan, counted by combine_bwd)
   int32_t* idx_fix;       // cache fallback mode: the gate writes the fresh top-k of unknown
                           // samples (cached row with -1) into these dispatch-index rows
 };

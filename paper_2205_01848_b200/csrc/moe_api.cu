@@ -34,7 +34,7 @@ int moe::pdl_enabled() {
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
       xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, grow, ep_all, sendbuf, oret, dwg32,
-      pre_dev, dlr, tdrop, total;
+      pre_dev, dlr, dropb, droptok, total;
 };
 
 struct moe_ctx {
@@ -152,7 +152,8 @@ void compute_layout(moe_ctx* h) {
   L.grow = take(T * k * 4);
   L.bpart = take(h->dtype == MOE_BF16 ? ((size_t)h->rows / 256 + h->n_local) * 2 * h->f * 4 : 0);
   // fused dispatch backward (k = 1, one GPU): [hi | lo](dl) by expert row
-  L.tdrop = take(ntiles * 4);
+  L.dropb = take(h->dtype == MOE_BF16 && k == 1 && !h->use_ep ? 2 * T * (size_t)h->n_pad * 2 : 0);
+  L.droptok = take(k == 1 ? T * 4 : 0);
   L.dlr = take(h->dtype == MOE_BF16 && k == 1 && !h->use_ep ? (size_t)h->rows * 2 * h->n_pad * 2 : 0);
   const bool ep = h->use_ep && !h->use_peer;  // NCCL transport buffers
   L.pre_dev = take(n * 4);
@@ -186,7 +187,9 @@ void bind_buffers(moe_ctx* h) {
   r.ticket = (uint32_t*)(meta + 782);
   r.token_of_slot = h->use_peer ? (int32_t*)(h->pwin + h->PL.tos) : (int32_t*)(b + L.token_of_slot);
   r.grow = (int32_t*)(b + L.grow);
-  r.tile_drop = (int32_t*)(b + L.tdrop);
+  r.dropb = nullptr;  // set per backward (fused dX only)
+  r.drop_tok = (int32_t*)(b + L.droptok);
+  r.drop_cnt = meta + 783;
 }
 
 void relayout(moe_ctx* h) {
@@ -694,9 +697,9 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   // N2 dispatch backward fused into the dX GEMM (k = 1, one GPU, tcgen05): the combine
   // backward also writes [hi|lo](dl) by expert row, the GEMM adds dl W_g and writes dx rows
   const bool fdx = h->use_tc && !h->use_ep && k == 1 && (h->fusion & MOE_FUSE_DX) && T > 0 &&
-                   a->dx != nullptr && ((uintptr_t)a->dx % 16) == 0 && tc_dx_fusion_supported(d) &&
-                   (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE <= MOE_MAX_DROP_TILES;
+                   a->dx != nullptr && ((uintptr_t)a->dx % 16) == 0 && tc_dx_fusion_supported(d);
   rb.dlr = fdx ? (__nv_bfloat16*)(ws + h->L.dlr) : nullptr;
+  rb.dropb = fdx ? (__nv_bfloat16*)(ws + h->L.dropb) : nullptr;
 
   KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O_tok, rb, T, k, n, dout, h->renorm, h->cts,
                                                      dO_tok, dlb, h->maxT, h->n_pad,
@@ -708,6 +711,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   rb.dw_ext = nullptr;
   rb.bal_g = nullptr;
   rb.dlr = nullptr;
+  rb.dropb = nullptr;
   if (peer) {  // N1: dO rows were stored into the owners by the combine backward
     KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DO, s0, (uint32_t*)rb.flags));
   } else if (h->use_ep) {  // C4: dO rows to the expert owners
@@ -770,8 +774,10 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   }
   if (a->dx) {  // fused dX GEMM: it wrote the kept tokens, this pass only the dropped ones
     if (h->use_tc)
-      KL(h, T > 0, "gate_dx", s0, launch_gate_dx_tc(fa.w_gate, dX_tok, dlb, h->maxT, h->n_pad, rb, T, k, n, d,
-                                                    h->cts, a->dx, acc, s0, pdx, fdx ? 1 : 0));
+      KL(h, T > 0, "gate_dx", s0, launch_gate_dx_tc(fa.w_gate, dX_tok,
+                                                    fdx ? (void*)(ws + h->L.dropb) : dlb, h->maxT,
+                                                    h->n_pad, rb, T, k, n, d, h->cts, a->dx, acc,
+                                                    s0, pdx, fdx ? 1 : 0));
     else
       KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dX_tok, rb, T, k, n, d, h->cts, a->dx, acc, s0,
                                                  pdx));

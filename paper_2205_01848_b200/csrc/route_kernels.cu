@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
     const int32_t* __restrict__ hist, int ntiles, int n, CapTable ct,
     int32_t* __restrict__ tile_off, int32_t* __restrict__ counts, int32_t* __restrict__ kept,
     int32_t* __restrict__ mtile_prefix, int64_t* __restrict__ drops,
-    uint32_t* __restrict__ ticket) {
+    uint32_t* __restrict__ ticket, int32_t* __restrict__ drop_cnt) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const int e = blockIdx.x;
   __shared__ int32_t warp_tot[8];
@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
       mtile_prefix[n] = carry;
       *drops = dr;
       *ticket = 0u;  // self-reset for the next launch
+      if (drop_cnt) *drop_cnt = 0;  // the combine backward's dropped-token list starts empty
     }
   }
 }
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
 cudaError_t launch_route_scan(const int32_t* hist, int ntiles, int n, const CapTable& ct,
                               RouteBufs b, cudaStream_t s) {
   launch_pdl(route_scan_kernel, n, 256, 0, s, hist, ntiles, n, ct, b.tile_off, b.counts, b.kept,
-                                      b.mtile_prefix, b.drops, b.ticket);
+                                      b.mtile_prefix, b.drops, b.ticket, b.drop_cnt);
   return cudaGetLastError();
 }
 
@@ -323,8 +324,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
     long long token_base, CapTable ct, const int32_t* __restrict__ tile_off,
     int32_t* __restrict__ slot_of, int32_t* __restrict__ token_of_slot, T* __restrict__ xbuf,
     const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs px, PeerBufs ptos,
-    const int32_t* __restrict__ pre_dev, T* __restrict__ yz, int dout,
-    int32_t* __restrict__ tile_drop) {
+    const int32_t* __restrict__ pre_dev, T* __restrict__ yz, int dout) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   // px.nl != 0 (peer EP, N1): rows go straight into the owners' X buffers over NVLink, the
   // global slot offsets come from the device plan (pre_dev), token_of_slot is the owner's.
@@ -378,15 +378,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
       srow[lt * k + r] = row;
     }
   }
-  {  // does this tile hold a token with every pair dropped? (the fused dX drop pass)
-    bool dtok = false;
-    if (lt < MOE_ROUTE_TILE && t < Tn) {
-      dtok = true;
-      for (int r = 0; r < k; ++r) dtok &= srow[lt * k + r] < 0;
-    }
-    const int any_drop = __syncthreads_or(dtok);
-    if (tile_drop && threadIdx.x == 0) tile_drop[tile] = any_drop;
-  }
+  __syncthreads();
   // row copies: warp per token
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int VE = Vec<T>::N;
@@ -445,13 +437,13 @@ cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T,
     launch_pdl(dispatch_kernel<__nv_bfloat16>, ntiles, 256, 0, s, 
         idx, (const __nv_bfloat16*)x, T, k, n, d, token_base, ct, b.tile_off, b.slot_of,
         b.token_of_slot, (__nv_bfloat16*)xbuf, pad_kept, pad_e0, px, ptos, pre_dev,
-        (__nv_bfloat16*)y_zero, dout, b.tile_drop);
+        (__nv_bfloat16*)y_zero, dout);
   else
     launch_pdl(dispatch_kernel<float>, ntiles, 256, 0, s, idx, (const float*)x, T, k, n, d,
                                                   token_base, ct, b.tile_off, b.slot_of,
                                                   b.token_of_slot, (float*)xbuf, pad_kept,
                                                   pad_e0, px, ptos, pre_dev, (float*)y_zero,
-                                                  dout, b.tile_drop);
+                                                  dout);
   return cudaGetLastError();
 }
 
@@ -655,7 +647,8 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
     __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad, const T* __restrict__ dspec,
     const float* __restrict__ dw_ext, const float* __restrict__ bal_g,
     int32_t* __restrict__ grow, const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs po,
-    PeerBufs pdo, __nv_bfloat16* __restrict__ dlr) {
+    PeerBufs pdo, __nv_bfloat16* __restrict__ dlr, __nv_bfloat16* __restrict__ dropb,
+    int32_t* __restrict__ drop_tok, int32_t* __restrict__ drop_cnt) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   // peer EP (N1): O rows are read from, and dO rows written to, the experts' owners
   if (pad_kept)
@@ -685,6 +678,16 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
         odst[r] = peer_row(dobuf, pdo, er[r], (size_t)rows[r], dout);
       }
     }
+  }
+  // fused dX (k = 1): a token whose pair was dropped gets a row of the compacted drop list
+  // (its dl pair is the A operand of the drop-only gate-dx pass); order is immaterial
+  int dpos = -1;
+  if (KM == 1 && dropb != nullptr && rows[0] < 0) {
+    if (lane == 0) {
+      dpos = atomicAdd(drop_cnt, 1);
+      drop_tok[dpos] = t;
+    }
+    dpos = __shfl_sync(0xffffffffu, dpos, 0);
   }
   // this lane's experts: pairs e = 2*lane + 64*j (+1)
   float lg[NL][2];
@@ -818,6 +821,10 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
         *reinterpret_cast<__nv_bfloat162*>(rr + e0) = hi;
         *reinterpret_cast<__nv_bfloat162*>(rr + n_pad + e0) = lo;
       }
+      if (dpos >= 0) {  // dropped token: its pair in the compacted drop list (dlb layout)
+        *reinterpret_cast<__nv_bfloat162*>(dropb + (size_t)dpos * n_pad + e0) = hi;
+        *reinterpret_cast<__nv_bfloat162*>(dropb + ((size_t)maxT + dpos) * n_pad + e0) = lo;
+      }
     }
   }
 }
@@ -836,7 +843,8 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
                                                    renorm, (T*)dobuf, b.dw, b.dl,              \
                                                    (__nv_bfloat16*)dlb, maxT, n_pad,           \
                                                    (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow, pad_kept, \
-                                                   pad_e0, po, pdo, b.dlr)
+                                                   pad_e0, po, pdo, b.dlr, b.dropb,    \
+                                                   b.drop_tok, b.drop_cnt)
   const int km = k == 1 ? 1 : (k == 2 ? 2 : 8);
   if (vpl <= 2) { if (km == 1) CB(2, 1); else if (km == 2) CB(2, 2); else CB(2, 8); }
   else if (vpl <= 4) { if (km == 1) CB(4, 1); else if (km == 2) CB(4, 2); else CB(4, 8); }
