@@ -164,16 +164,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
+# MOE_BENCH_SHARE_GPU=1: run the N > 1 path with every rank on cuda:0 and a gloo process group
+# (NCCL refuses two ranks on one device) -- a smoke test of the multi-process bench on one GPU;
+# the numbers it prints are not scaling numbers.
+SHARE_GPU = os.environ.get("MOE_BENCH_SHARE_GPU", "0") == "1"
+
+
 def dist_setup(args):
     import torch
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     pg = None
+    if SHARE_GPU:  # test hook: every rank on cuda:0 (peer transport over IPC on one device)
+        local = 0
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local) if torch.cuda.is_available() else None
-        backend = "nccl" if torch.cuda.is_available() and args.impl == "ours" else "gloo"
+        backend = ("nccl" if torch.cuda.is_available() and args.impl == "ours" and not SHARE_GPU
+                   else "gloo")
         dist.init_process_group(backend=backend)
         pg = dist
     return ws, rank, local, pg
@@ -305,7 +314,7 @@ def run_ours(args):
     def max_over_ranks(v):
         if dist is None:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if SHARE_GPU else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
