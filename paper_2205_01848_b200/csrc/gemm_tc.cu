@@ -450,6 +450,9 @@ bool tc_gather_supported(int d, int f) {
 }
 bool tc_combine_supported(int dout) { return use_2cta(dout, TC_FWD2); }
 bool tc_dx_fusion_supported(int d) { return use_2cta(d, TC_DGRAD_X); }
+bool tc_peer_return_supported(int d, int dout) {
+  return use_2cta(dout, TC_FWD2) && use_2cta(d, TC_DGRAD_X);
+}
 
 // db[e][c] = sum of the DGRAD_A column-sum partials of expert e, fixed order (deterministic).
 __global__ void bias_part_reduce_kernel(const float* __restrict__ part,
@@ -505,7 +508,10 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   const bool gat = KIND == TC_FWD1 && fz && fz->x;        // A rows gathered from x (N2)
   const bool comb = KIND == TC_FWD2 && fz && fz->y;       // fused combine (N2, k = 1)
   const bool fdx = KIND == TC_DGRAD_X && fz && fz->dx;    // fused dispatch backward (k = 1)
-  if ((gat || comb || fdx) && !two) return MOE_ERR_CONFIG;
+  const PeerBufs* pr = !fz ? nullptr
+                       : KIND == TC_FWD2 ? &fz->pret_o : KIND == TC_DGRAD_X ? &fz->pret_dx : nullptr;
+  const bool ret = pr && pr->nl != 0;                     // peer EP return rows (N1)
+  if ((gat || comb || fdx || ret) && !two) return MOE_ERR_CONFIG;
   CUtensorMap ma2, mb2;
   if (fdx) {
     TC_TRY(make_map(&ma2, fz->dlr, 2 * fz->n_pad, rows, 64, 128));
@@ -533,6 +539,12 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   if (comb) {
     p.y = (__nv_bfloat16*)fz->y;
     p.wt = fz->w;
+  }
+  if (ret) {
+    p.gtos = fz->tos;
+    p.gk = fz->k;
+    p.pret = *pr;
+    p.tpr = fz->tpr;
   }
   if (fdx) {
     p.gtos = fz->tos;

@@ -30,10 +30,15 @@ struct TcFusion {
   const void* dlr = nullptr;      // [rows, 2 n_pad] bf16 hi | lo of dl in expert-row order
   const void* wg = nullptr;       // W_g [n, d]
   int n = 0, n_pad = 64, accumulate = 0;
+  // peer EP return rows (N1): O (FWD2) / dX (DGRAD_X) rows stored by the epilogue into the
+  // token owners' windows in (token, choice) order; nl == 0 = off
+  PeerBufs pret_o{}, pret_dx{};
+  int tpr = 0;
 };
 bool tc_gather_supported(int d, int f);     // 2-CTA kernels for FWD1 (N = f) and WGRAD_W1 (N = d)
 bool tc_combine_supported(int dout);        // 2-CTA kernel for FWD2 (N = d_out)
 bool tc_dx_fusion_supported(int d);         // 2-CTA kernel for DGRAD_X (N = d)
+bool tc_peer_return_supported(int d, int dout);  // N1 return rows from FWD2 / DGRAD_X
 
 // Forward: H = relu(X W1_e^T + b1_e), O = H W2_e^T + b2_e over kept_e rows per local expert.
 moe_status_t tc_ffn_forward(TcPlan* p, void* X, const void* w1, const void* b1,

@@ -478,6 +478,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         yw = p.wt[ytok];
       }
       if (KIND == TC_DGRAD_X && p.dxo != nullptr && row_ok) ytok = p.gtos[p.ct.base[e] + row];
+      // row-scatter stores (the staged box leaves as row segments to per-row destinations):
+      //  * fused dispatch backward: dx row of the token;
+      //  * peer EP return (N1): the (token, choice) row of the token owner's O / dX return
+      //    buffer, in that rank's window over NVLink -- the exchange rides on the epilogue
+      __nv_bfloat16* rdst = nullptr;
+      if (KIND == TC_DGRAD_X && p.dxo != nullptr && row_ok) rdst = p.dxo + (size_t)ytok * p.N;
+      if ((KIND == TC_FWD2 || KIND == TC_DGRAD_X) && p.pret.nl != 0 && row_ok) {
+        const int gp = p.gtos[p.ct.base[e] + row];  // global pair id t_g * k + r
+        const int owner = (gp / p.gk) / p.tpr;
+        const int lp = gp - owner * p.tpr * p.gk;
+        char* b = nullptr;
+#pragma unroll
+        for (int j = 0; j < MOE_MAX_R; ++j)
+          if (owner == j) b = p.pret.p[j];
+        rdst = reinterpret_cast<__nv_bfloat16*>(b) + (size_t)lp * p.N;
+      }
       const bool need_side = ((KIND == TC_FWD1 || KIND == TC_FWD2) && row_ok) ||
                              (KIND == TC_WGRAD && row_ok && p.accumulate);
       if (need_side) {
@@ -593,17 +609,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             *reinterpret_cast<uint4*>(stg + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4)) = pk[i];
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          const bool rowstore = KIND == TC_DGRAD_X && p.dxo != nullptr;  // token rows instead
+          const bool rowstore = (KIND == TC_DGRAD_X && p.dxo != nullptr) ||
+                                ((KIND == TC_FWD2 || KIND == TC_DGRAD_X) && p.pret.nl != 0);
           if (rowstore) {
-            // dispatch backward (k = 1): dx[t] = dX[row] + dl[t] W_g, both in this fp32
-            // accumulator, rounded once; the staged box leaves as 64-byte row segments to the
-            // tokens' dx rows (lane: row 8i + l/4, 16-byte chunk l%4; token from its lane)
+            // 64-byte row segments (lane: row 8i + l/4, 16-byte chunk l%4) to the row's
+            // destination from its lane: dx[t] = dX[row] + dl[t] W_g (fused dispatch
+            // backward, one rounding) or the token owner's return row (peer EP)
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int r = i * 8 + (lane >> 2), c = lane & 3;
-              const int tok = __shfl_sync(0xffffffffu, ytok, r);
-              if (tok >= 0)
-                st_v4(p.dxo + (size_t)tok * p.N + col0 + c * 8,
+              const unsigned long long dst = __shfl_sync(
+                  0xffffffffu, reinterpret_cast<unsigned long long>(rdst), r);
+              if (dst != 0ull)
+                st_v4(reinterpret_cast<__nv_bfloat16*>(dst) + col0 + c * 8,
                       *reinterpret_cast<const uint4*>(stg + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)));
             }
           }

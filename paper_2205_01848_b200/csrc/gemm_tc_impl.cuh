@@ -46,6 +46,10 @@ struct TcParams {
   // the epilogue writes dx[t] (token order, via gtos) instead of the dX buffer.
   __nv_bfloat16* dxo;
   int nkx, nbx;
+  // N1 return rows (peer EP, FWD2 / DGRAD_X): pret.p[j] = rank j's return buffer; output row
+  // of global pair gp = t_g k + r goes to rank gp / (k tpr) at pair gp mod (k tpr); nl != 0 = on
+  PeerBufs pret;
+  int tpr;
   CapTable ct;                  // base rows of each local expert region
 };
 

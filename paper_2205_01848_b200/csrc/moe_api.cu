@@ -67,6 +67,7 @@ struct moe_ctx {
   int use_tc = 0;             // tcgen05 path for bf16 (env MOE_FORCE_SIMT=1 disables)
   int fusion = MOE_FUSE_COMBINE | MOE_FUSE_DX;  // N2 fusions (moe_set_fusion; GATHER opt-in)
   int fused_gather = 0;       // the last forward gathered x rows in the GEMMs (no X buffer)
+  int peer_ret = 0;           // peer EP: O / dX rows returned by the GEMM epilogues (N1)
   TcPlan tc{};
   Prof prof;
   float balance_lambda = 0.f; // Eq. 3 balance term weight (0 = off)
@@ -188,6 +189,8 @@ void bind_buffers(moe_ctx* h) {
   r.token_of_slot = h->use_peer ? (int32_t*)(h->pwin + h->PL.tos) : (int32_t*)(b + L.token_of_slot);
   r.grow = (int32_t*)(b + L.grow);
   r.dropb = nullptr;  // set per backward (fused dX only)
+  r.dlr = nullptr;
+  r.o_pair = 0;
   r.drop_tok = (int32_t*)(b + L.droptok);
   r.drop_cnt = meta + 783;
 }
@@ -295,6 +298,11 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
   h->stream = (cudaStream_t)c.stream;
   const char* fs = getenv("MOE_FORCE_SIMT");
   h->use_tc = (c.dtype == MOE_BF16) && !(fs && fs[0] == '1');
+  {
+    const char* pr = getenv("MOE_PEER_RET");  // 0: combine / gate-dx read the owners' rows
+    h->peer_ret = h->use_peer && h->use_tc && tc_peer_return_supported(h->d, h->dout) &&
+                  !(pr && pr[0] == '0');
+  }
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -313,9 +321,13 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
       wrows = max_owner_rows(h, c8);
     }
     wrows = (wrows + MOE_ROW_ALIGN - 1) / MOE_ROW_ALIGN * MOE_ROW_ALIGN;
-    peer_layout(h->PL, wrows, h->n, h->d, h->dout, h->s);
+    peer_layout(h->PL, wrows, h->n, h->d, h->dout, h->s, (int64_t)h->maxT * h->k);
+    // zeroed and COMPLETE before any rank can see the window: the epoch / flag words start at
+    // 0, and a memset still in flight (legacy stream) could race with a peer's first count
+    // push or with kernels on non-blocking streams
     if (cudaMalloc((void**)&h->pwin, h->PL.total) != cudaSuccess ||
-        cudaMemset(h->pwin, 0, h->PL.total) != cudaSuccess) {
+        cudaMemset(h->pwin, 0, h->PL.total) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
       if (h->pwin) cudaFree(h->pwin);
       cudaEventDestroy(h->ev_fork);
       cudaEventDestroy(h->ev_join);
@@ -494,6 +506,10 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     fz.y = a->y;
     fz.w = rb.w;
   }
+  if (h->peer_ret) {  // N1: FWD2's epilogue stores O rows into the token owners' windows
+    fz.pret_o = peer_bufs(h, h->PL.oret);
+    fz.tpr = T;
+  }
   CUDA_TRY(h, cudaMemsetAsync(rb.hit_count, 0, 4, s0));
   if (tab)  // idx[t] = table[sample_ids[t]] (before the fork: the side stream reads it)
     KL(h, T > 0, "cache_gather", s0, launch_cache_gather(h->ctab, h->ctab_num, k, h->cids, T,
@@ -584,7 +600,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     moe_status_t st = tc_ffn_forward(&h->tc, X, w1, b1, w2, b2, H, O, h->rows, d, f, dout,
                                      kept_local, rb.mtile_prefix, nl, h->ct, h->max_cap_local,
                                      sd, &nk, &h->prof, (uint32_t*)(ws + h->L.mask),
-                                     (gather || fcomb) ? &fz : nullptr);
+                                     (gather || fcomb || h->peer_ret) ? &fz : nullptr);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 forward failed");
   } else {
@@ -597,7 +613,10 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   PeerBufs po{};    // peer EP: combine reads O rows from the owners
   if (h->use_peer) {
     KL(h, 1, "peer_barrier", sd, launch_peer_barrier(h->wins, h->R, h->rank, PH_O, sd, (uint32_t*)rb.flags));
-    po = peer_bufs(h, h->PL.o);
+    if (h->peer_ret)
+      O_tok = h->pwin + h->PL.oret;  // this rank's (token, choice) rows, stored by the owners
+    else
+      po = peer_bufs(h, h->PL.o);
   } else if (h->use_ep) {
     std::string err;
     O_tok = ws + h->L.oret;
@@ -636,10 +655,12 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   }
   rb.spec = h->spec;
   rb.spec_valid = h->spec_valid;
+  rb.o_pair = h->peer_ret;
   if (!fcomb)
     KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O_tok, rb, T, k, dout, h->cts, a->y, s0, po));
   rb.spec = nullptr;
   rb.spec_valid = nullptr;
+  rb.o_pair = 0;
   if (!h->mq.empty()) {  // push this iteration's metric futures (App. B)
     auto& sl = h->mq[(h->mq_head + h->mq_count) % h->mq.size()];
     sl.host->iteration = h->mq_iter;
@@ -686,7 +707,8 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
 
   // K6 combine backward -> dO rows (local or, in EP, returned to the expert owners), dw, dl
   void* dlb = h->use_tc ? (void*)(ws + h->L.dlb) : nullptr;
-  void* O_tok = nccl_ep ? (void*)(ws + h->L.oret) : O;
+  void* O_tok = nccl_ep ? (void*)(ws + h->L.oret)
+                : (peer && h->peer_ret) ? (void*)(h->pwin + h->PL.oret) : O;
   void* dO_tok = nccl_ep ? (void*)(ws + h->L.sendbuf) : dO;
   std::string err;
   rb.dspec = h->dspec;
@@ -701,12 +723,14 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   rb.dlr = fdx ? (__nv_bfloat16*)(ws + h->L.dlr) : nullptr;
   rb.dropb = fdx ? (__nv_bfloat16*)(ws + h->L.dropb) : nullptr;
 
+  rb.o_pair = peer && h->peer_ret;
   KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O_tok, rb, T, k, n, dout, h->renorm, h->cts,
                                                      dO_tok, dlb, h->maxT, h->n_pad,
                                                      nccl_ep ? nullptr : rb.kept, s0,
                                                      peer ? h->e_lo : 0,
-                                                     peer ? peer_bufs(h, h->PL.o) : PeerBufs{},
+                                                     peer && !h->peer_ret ? peer_bufs(h, h->PL.o) : PeerBufs{},
                                                      peer ? peer_bufs(h, h->PL.dob) : PeerBufs{}));
+  rb.o_pair = 0;
   rb.dspec = nullptr;
   rb.dw_ext = nullptr;
   rb.bal_g = nullptr;
@@ -732,6 +756,10 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
     fz.tos = rb.token_of_slot;
     fz.k = k;
     if (h->fused_gather) fz.x = fa.x;
+    if (peer && h->peer_ret) {  // N1: DGRAD_X's epilogue returns dX rows to the token owners
+      fz.pret_dx = peer_bufs(h, h->PL.dxret);
+      fz.tpr = T;
+    }
     if (fdx) {
       fz.dx = a->dx;
       fz.dlr = ws + h->L.dlr;
@@ -744,7 +772,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                                       h->rows, d, f, dout, kept_local, rb.mtile_prefix, nl,
                                       h->ct, h->max_cap_local, s0, &nk, &h->prof,
                                       (uint32_t*)(ws + h->L.mask), (float*)(ws + h->L.bpart),
-                                      (h->fused_gather || fdx) ? &fz : nullptr);
+                                      (h->fused_gather || fdx || (peer && h->peer_ret)) ? &fz : nullptr);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 backward failed");
   } else {
@@ -764,9 +792,13 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   // B4: dx = gather(dX) + dl W_g ;  B5: dW_g = dl^T x
   void* dX_tok = dXb;
   PeerBufs pdx{};
-  if (peer) {  // N1: the gate-input gradient reads dX rows from the owners
+  if (peer) {  // N1: the gate-input gradient reads dX rows from the owners (or, with return
+               // rows, this rank's own (token, choice) rows the owners stored)
     KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DX, s0, (uint32_t*)rb.flags));
-    pdx = peer_bufs(h, h->PL.dxb);
+    if (h->peer_ret)
+      dX_tok = h->pwin + h->PL.dxret;
+    else
+      pdx = peer_bufs(h, h->PL.dxb);
   } else if (h->use_ep) {  // C5: dX rows back to the token owners (send layout, reuses the send buffer)
     dX_tok = ws + h->L.sendbuf;
     moe_status_t st = ep_from_experts(h->ep, h->plan, dXb, dX_tok, h->ct, d, (int)h->s, s0, &err);

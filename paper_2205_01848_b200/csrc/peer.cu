@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(256) peer_sum_kernel(PeerBufs win, size_t off,
 
 }  // namespace
 
-void peer_layout(PeerLayout& L, int64_t rows, int n, int d, int dout, size_t elem) {
+void peer_layout(PeerLayout& L, int64_t rows, int n, int d, int dout, size_t elem,
+                 int64_t pair_rows) {
   L.rows = rows;
   L.epoch = 0;
   L.flags = 256;
@@ -181,6 +182,8 @@ void peer_layout(PeerLayout& L, int64_t rows, int n, int d, int dout, size_t ele
   L.o = take((size_t)rows * dout * elem);
   L.dob = take((size_t)rows * dout * elem);
   L.dxb = take((size_t)rows * d * elem);
+  L.oret = take((size_t)pair_rows * dout * elem);
+  L.dxret = take((size_t)pair_rows * d * elem);
   L.total = o;
 }
 

@@ -38,12 +38,15 @@ enum PeerPhase { PH_CNT = 0, PH_X = 1, PH_O = 2, PH_BAL = 3, PH_DO = 4, PH_DX = 
 
 struct PeerLayout {
   size_t epoch = 0, flags = 256, cnt = 512, bal = 0, dwg = 0, tos = 0, x = 0, o = 0, dob = 0,
-         dxb = 0, total = 0;
+         dxb = 0, oret = 0, dxret = 0, total = 0;
   int64_t rows = 0;  // rows of each expert buffer
 };
 
 // Byte layout of a window with `rows` expert-buffer rows.
-void peer_layout(PeerLayout& L, int64_t rows, int n, int d, int dout, size_t elem);
+// oret / dxret: [pair_rows x d_out] / [pair_rows x d] expert outputs and input gradients of
+// THIS rank's tokens in (token, choice) order, stored there by the owners' GEMM epilogues.
+void peer_layout(PeerLayout& L, int64_t rows, int n, int d, int dout, size_t elem,
+                 int64_t pair_rows);
 
 // Plan (one block): publish local counts, barrier, derive the global plan into b.counts
 // (global pre-drop counts), b.kept / b.mtile_prefix (local experts), b.drops and pre_out[n].

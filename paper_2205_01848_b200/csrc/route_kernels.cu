@@ -484,7 +484,8 @@ template <typename T, int VPL, int KM>
 __global__ void __launch_bounds__(256) combine_fwd_kernel(
     const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
-    T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid, PeerBufs po) {
+    T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid, PeerBufs po,
+    int o_pair) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -501,7 +502,9 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
       const int sl = slot_of[(size_t)t * k + r];
       if (sl >= 0) {
         const int e = idx[(size_t)t * k + r];
-        src[r] = peer_row(obuf, po, e, (size_t)(ct.base[e] + sl), dout);
+        // o_pair (peer EP return rows): the owner's GEMM stored O at this (token, choice) row
+        src[r] = o_pair ? obuf + ((size_t)t * k + r) * dout
+                        : peer_row(obuf, po, e, (size_t)(ct.base[e] + sl), dout);
         wr[r] = w[(size_t)t * k + r];
       }
     }
@@ -559,7 +562,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) combine_fwd_generic_kernel(
     const T* __restrict__ obuf, const float* __restrict__ w, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ slot_of, CapTable ct, int Tn, int k, int dout,
-    T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid, PeerBufs po) {
+    T* __restrict__ y, T* __restrict__ spec, uint8_t* __restrict__ valid, PeerBufs po,
+    int o_pair) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -573,7 +577,8 @@ __global__ void __launch_bounds__(256) combine_fwd_generic_kernel(
     rsel[r] = nullptr;
     if (sl >= 0) {
       const int e = idx[(size_t)t * k + r];
-      rows[nk] = peer_row(obuf, po, e, (size_t)(ct.base[e] + sl), dout);
+      rows[nk] = o_pair ? obuf + ((size_t)t * k + r) * dout
+                        : peer_row(obuf, po, e, (size_t)(ct.base[e] + sl), dout);
       rsel[r] = rows[nk];
       wr[nk] = w[(size_t)t * k + r];
       ++nk;
@@ -611,14 +616,14 @@ static cudaError_t combine_fwd_t(const void* obuf, RouteBufs b, int T_, int k, i
   const int vpl = (d_out / Vec<T>::N + 31) / 32;
 #define CF(V, K)                                                                            \
   launch_pdl(combine_fwd_kernel<T, V, K>, grid, 256, 0, s, (const T*)obuf, b.w, b.idx, b.slot_of, ct, \
-                                                   T_, k, d_out, (T*)y, spec, valid, po)
+                                                   T_, k, d_out, (T*)y, spec, valid, po, b.o_pair)
   if (k <= 2) {
     if (vpl <= 2) { if (k == 1) CF(2, 1); else CF(2, 2); }
     else if (vpl <= 4) { if (k == 1) CF(4, 1); else CF(4, 2); }
     else { if (k == 1) CF(8, 1); else CF(8, 2); }
   } else {
     launch_pdl(combine_fwd_generic_kernel<T>, grid, 256, 0, s, (const T*)obuf, b.w, b.idx, b.slot_of, ct,
-                                                       T_, k, d_out, (T*)y, spec, valid, po);
+                                                       T_, k, d_out, (T*)y, spec, valid, po, b.o_pair);
   }
 #undef CF
   return cudaGetLastError();
@@ -648,7 +653,7 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
     const float* __restrict__ dw_ext, const float* __restrict__ bal_g,
     int32_t* __restrict__ grow, const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs po,
     PeerBufs pdo, __nv_bfloat16* __restrict__ dlr, __nv_bfloat16* __restrict__ dropb,
-    int32_t* __restrict__ drop_tok, int32_t* __restrict__ drop_cnt) {
+    int32_t* __restrict__ drop_tok, int32_t* __restrict__ drop_cnt, int o_pair) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   // peer EP (N1): O rows are read from, and dO rows written to, the experts' owners
   if (pad_kept)
@@ -674,7 +679,8 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
       rows[r] = sl >= 0 ? ct.base[er[r]] + sl : -1;
       wr[r] = w[(size_t)t * k + r];
       if (rows[r] >= 0) {
-        osrc[r] = peer_row(obuf, po, er[r], (size_t)rows[r], dout);
+        osrc[r] = o_pair ? obuf + ((size_t)t * k + r) * dout  // peer EP return rows (local)
+                         : peer_row(obuf, po, er[r], (size_t)rows[r], dout);
         odst[r] = peer_row(dobuf, pdo, er[r], (size_t)rows[r], dout);
       }
     }
@@ -753,10 +759,12 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
   for (int r = 0; r < KM; ++r)
     if (r < k && lane == r) {
       dw[(size_t)t * k + r] = dwr[r];
-      if (grow)  // the gate-dx kernel's gather table (peer EP: owner in the top bits)
-        grow[(size_t)t * k + r] = (pdo.nl && rows[r] >= 0)
-                                      ? rows[r] | ((er[r] / pdo.nl) << MOE_GROW_SHIFT)
-                                      : rows[r];
+      if (grow)  // the gate-dx kernel's gather table (peer EP: owner in the top bits; with
+                 // return rows the dX row is this rank's own (token, choice) row)
+        grow[(size_t)t * k + r] = rows[r] < 0 ? -1
+                                  : o_pair ? (int)((size_t)t * k + r)
+                                  : pdo.nl ? rows[r] | ((er[r] / pdo.nl) << MOE_GROW_SHIFT)
+                                           : rows[r];
     }
   float m = -INFINITY, sp = 0.f, cb = 0.f;
   if (need_p) {
@@ -844,7 +852,7 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
                                                    (__nv_bfloat16*)dlb, maxT, n_pad,           \
                                                    (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow, pad_kept, \
                                                    pad_e0, po, pdo, b.dlr, b.dropb,    \
-                                                   b.drop_tok, b.drop_cnt)
+                                                   b.drop_tok, b.drop_cnt, b.o_pair)
   const int km = k == 1 ? 1 : (k == 2 ? 2 : 8);
   if (vpl <= 2) { if (km == 1) CB(2, 1); else if (km == 2) CB(2, 2); else CB(2, 8); }
   else if (vpl <= 4) { if (km == 1) CB(4, 1); else if (km == 2) CB(4, 2); else CB(4, 8); }

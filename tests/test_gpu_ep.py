@@ -88,6 +88,19 @@ def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0, tra
         from synth import perturb_cached
         fresh = O.topk_sorted(O.gate_logits(to_np(cpu["x"]), to_np(cpu["w_gate"])), k)
         cached = torch.from_numpy(perturb_cached(fresh, n, cached_frac)).cuda()
+    if transport == "peer":
+        # Load every kernel this shape uses before the threaded ranks run: with CUDA lazy
+        # loading, a rank spinning in a barrier kernel while another thread's first launch
+        # loads a module can stall until the barrier's bounded wait gives up (one process,
+        # one GPU; separate processes per GPU are not affected).
+        warm = MoELayer(n, k, d, f, 0, T, dtype, renorm, world_size=1, rank=0, device="cuda",
+                        transport="peer")
+        warm.peer_attach([warm.peer_window()])
+        warm.set_balance_loss(lam)
+        warm.forward(g["x"][:T], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+        warm.backward(dy[:T].contiguous())
+        torch.cuda.synchronize()
+        warm.close()
     layers = [MoELayer(n, k, d, f, 0, T, dtype, renorm, world_size=R, rank=r,
                        nccl_comm=comm.value or 0, device="cuda", transport=transport)
               for r in range(R)]
@@ -124,6 +137,7 @@ def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0, tra
         t.join(timeout=120)
     assert not errs, errs
     ref = MoELayer(n, k, d, f, 0, Tg, dtype, renorm, device="cuda")
+    ref.set_fusion(0)  # single-GPU N2 dx fusion rounds dX once: not bitwise comparable to EP
     ref.set_capacities(caps)
     ref.set_balance_loss(lam)
     if cached is not None:
@@ -266,3 +280,47 @@ def test_peer_virtual_ranks_many_iterations_with_recompiles():
     out, ref = _run_virtual(R, n, k, T, d, f, "bf16", 1, transport="peer", iters=len(seq),
                             caps_seq=seq)
     _check_virtual(out, ref, R, n, "bf16")
+
+
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("R", [2, 4])
+@pytest.mark.parametrize("k,renorm", [(1, 0), (2, 1)])
+def test_peer_return_rows_virtual_ranks(R, k, renorm):
+    """N1 return rows: with d, d_out multiples of 128 the owners' FWD2 / DGRAD_X epilogues
+    store O / dX rows straight into the token owners' windows in (token, choice) order, and
+    the combine / gate-dx kernels read them locally -- bitwise equal to the single-GPU layer
+    and to the owner-read form (MOE_PEER_RET=0)."""
+    import os
+    n, T, d, f = 16, 512, 128, 256
+    out, ref = _run_virtual(R, n, k, T, d, f, "bf16", renorm, transport="peer")
+    _check_virtual(out, ref, R, n, "bf16")
+    for o in out[1:]:
+        assert torch.equal(o[1]["dw_gate"], out[0][1]["dw_gate"])
+    os.environ["MOE_PEER_RET"] = "0"
+    try:
+        out0, _ = _run_virtual(R, n, k, T, d, f, "bf16", renorm, transport="peer")
+    finally:
+        del os.environ["MOE_PEER_RET"]
+    nl = n // R
+    for r, (a, b) in enumerate(zip(out, out0)):
+        assert torch.equal(a[0], b[0])
+        for key in ("dx", "dw_gate"):
+            assert torch.equal(a[1][key], b[1][key]), key
+        for key in ("dw1", "db1", "dw2", "db2"):  # each rank writes its own experts only
+            sl = slice(r * nl, (r + 1) * nl)
+            assert torch.equal(a[1][key][sl], b[1][key][sl]), key
+
+
+@pytest.mark.parametrize("k,renorm", [(1, 0), (2, 1)])
+def test_peer_return_rows_loopback_oracle(k, renorm):
+    """R = 1 peer path with return rows (d = 128) against the oracle."""
+    from paper_2205_01848_b200 import MoELayer
+    n, T, d, f = 16, 1000, 128, 256
+    caps = O.capacities_from_factors([1.0] * n, T, k)
+    pl = MoELayer(n, k, d, f, 0, T, "bf16", renorm, world_size=1, rank=0, device="cuda",
+                  transport="peer")
+    pl.peer_attach([pl.peer_window()])
+    layer, gpu, st, gr, ol = run_pair(n, k, d, f, T, "bf16", caps, renorm, layer=pl)
+    assert st.routing.drops > 0
+    assert_routing_exact(gpu, st, k, check_token_of_slot=True)
+    assert_values(gpu, st, gr, ol, "bf16")
