@@ -60,9 +60,12 @@ def test_runtime_capacity_policy_effect_latency():
     assert drops[0] > 0 and drops[-1] == 0   # dynamic capacities removed the drops
 
 
-def test_graphed_step_matches_eager_and_recaptures():
+@pytest.mark.parametrize("d,f", [(64, 128), (128, 256)])
+def test_graphed_step_matches_eager_and_recaptures(d, f):
+    """(128, 256): every GEMM on the 2-CTA kernel with the N2 combine / dispatch-backward
+    fusions and programmatic dependent launches inside the captured graph."""
     from paper_2205_01848_b200 import GraphedStep
-    layer, g, dy = _setup(dtype="bf16", regime="uniform")
+    layer, g, dy = _setup(dtype="bf16", regime="uniform", d=d, f=f)
     layer.set_capacity_factors([1.25] * layer.n)
     layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
     eager = layer.backward(dy)
