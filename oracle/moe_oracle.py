@@ -375,7 +375,7 @@ def moe_forward(x, params, k: int, capacities, renormalize: int = 1, cached_idx=
 # --------------------------------------------------------------------------- #
 # Backward: exact chain rule of the forward above
 # --------------------------------------------------------------------------- #
-def moe_backward(st: FwdState, dy: np.ndarray, dspec=None, dw_ext=None) -> dict:
+def moe_backward(st: FwdState, dy: np.ndarray, dspec=None, dw_ext=None, relu_mask=None) -> dict:
     """Gradients of sum(dy * y) w.r.t. x, w_gate, w1, b1, w2, b2 (and the logits, dl).
 
     P:225: dropped samples are ignored in back propagation -> dropped pairs get dw = 0 and
@@ -388,7 +388,13 @@ def moe_backward(st: FwdState, dy: np.ndarray, dspec=None, dw_ext=None) -> dict:
     rows (specification loss, Eq. 2; rows of dropped pairs are ignored) and dw_ext
     [T, k] the caller's direct gradient w.r.t. the gate weights w (e.g. L_i of Eq. 2); the
     balance term (Eq. 3) adds dB/dl with T_i held constant (stop-gradient):
-    dB/dp[t,i] = lambda n T_i / T."""
+    dB/dp[t,i] = lambda n T_i / T.
+
+    relu_mask: optional list over experts of boolean [kept_e x f] ReLU' decisions (H > 0 of
+    the kernel under test).  The mask is an integer decision taken by floating point, so for
+    parity both sides take it in the same precision (the kernel's, as the routing decisions
+    come from the kernel's fp32 logits): an A within an ulp of 0 may otherwise flip sign
+    between fp64 and fp32 and move a whole dA element.  None = A > 0 here."""
     dy = np.asarray(dy, np.float64)
     k, n = st.k, st.n
     T = st.x.shape[0]
@@ -420,7 +426,8 @@ def moe_backward(st: FwdState, dy: np.ndarray, dspec=None, dw_ext=None) -> dict:
         W2 = np.asarray(st.params["w2"][e], np.float64)
         dW2[e] = dO[e].T @ st.H[e]
         db2[e] = dO[e].sum(axis=0)
-        dA = (dO[e] @ W2) * (st.A[e] > 0)
+        mask = (st.A[e] > 0) if relu_mask is None else np.asarray(relu_mask[e], bool)
+        dA = (dO[e] @ W2) * mask
         if st.emulate_bf16:
             dA = round_bf16(dA)
         dW1[e] = dA.T @ st.X[e][:kept]

@@ -68,7 +68,14 @@ def run_pair(n, k, d, f, T, dtype, caps, renorm=1, regime="uniform", d_out=None,
     gl = gpu["routing_fwd"]["logits"].astype(np.float64)
     st = O.moe_forward(x64, p64, k, caps, renorm, cached_idx=cidx, logits=gl,
                        emulate_bf16=(dtype == "bf16"))
-    gr = O.moe_backward(st, to_numpy64(dy))
+    # the ReLU' decision in the kernel's precision (its stored H > 0), like routing from its
+    # fp32 logits: both sides take every integer decision alike
+    rf = gpu["routing_fwd"]
+    mask = None
+    if len(rf["base"]) == n + 1 and "h_buf" in rf:
+        mask = [rf["h_buf"][rf["base"][e]: rf["base"][e] + int(st.routing.kept[e])] > 0
+                for e in range(n)]
+    gr = O.moe_backward(st, to_numpy64(dy), relu_mask=mask)
     own_logits = O.gate_logits(x64, p64["w_gate"])
     return layer, gpu, st, gr, own_logits
 
