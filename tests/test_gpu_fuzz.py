@@ -40,3 +40,31 @@ def test_fuzz_vs_oracle(dtype, n, k, d, f, d_out, T, alpha, renorm, regime, fusi
                                        d_out=d_out or None, layer=layer)
     assert_routing_exact(gpu, st, k)
     assert_values(gpu, st, gr, own, dtype)
+
+
+def _ep_cases():
+    rng = np.random.default_rng(1848)
+    out = []
+    for i in range(10):
+        R = int(rng.choice([2, 4]))
+        n = R * int(rng.choice([1, 2, 4, 8]))
+        k = int(min(n, rng.choice([1, 2, 2, 4])))
+        dtype = "f32" if i % 4 == 0 else "bf16"
+        d = int(rng.choice([64, 128, 192]))
+        f = int(rng.choice([64, 128, 256]))
+        T = int(rng.choice([64, 200, 512]))
+        renorm = int(rng.integers(0, 2))
+        transport = str(rng.choice(["peer", "nccl"]))
+        out.append((R, n, k, dtype, d, f, T, renorm, transport))
+    return out
+
+
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("R,n,k,dtype,d,f,T,renorm,transport", _ep_cases())
+def test_fuzz_ep_virtual_ranks(R, n, k, dtype, d, f, T, renorm, transport):
+    """R expert-parallel ranks (threads on one GPU; peer windows or the virtual communicator)
+    against the single-GPU layer on the concatenated batch: routing, y, dx and each owner's
+    expert gradients bitwise equal (dW_g within tolerance: summed in another split)."""
+    from test_gpu_ep import _check_virtual, _run_virtual
+    out, ref = _run_virtual(R, n, k, T, d, f, dtype, renorm, transport=transport)
+    _check_virtual(out, ref, R, n, dtype)
