@@ -37,6 +37,8 @@ struct GateFwdParams {
   int32_t* idx_fix;       // fallback mode: rows of unknown samples (-1) get the fresh top-k
   int dbg;                 // timing experiments (MOE_GATE_DBG), 0 in production
   int tma_logits;          // logits written by TMA from a staged 32 x 16 box (n % 16 == 0)
+  int32_t* hist;           // [T / 128 x n] per-tile expert histogram of idx_out (A3 fused into
+                           // the epilogue; the 128-token M tile is the routing tile), or null
 };
 
 // logits staging of the gate epilogue: one 32-row x 16-column fp32 box (2 KB, 64-byte
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(G_THREADS, 2)
   }
   Bars b = setup_bars<STAGES>(smem + STAGES * STAGE_BYTES, 2 * BN, warp, lane);
   uint8_t* s_stg = smem + STAGES * STAGE_BYTES + 1024;  // [4 warps][2 KB], 1 KB aligned
+  int32_t* s_hist = reinterpret_cast<int32_t*>(s_stg + 4 * GF_STG_BYTES);  // [256]
   const uint32_t tmem_base = *b.tmem;
   const int MT = (p.T + TC_BM - 1) / TC_BM;
   const int nk = K / TC_BK;
@@ -205,6 +208,12 @@ __global__ void __launch_bounds__(G_THREADS, 2)
     int it = 0;
     for (int tile = blockIdx.x; tile < MT; tile += gridDim.x, ++it) {
       const int acc = it & 1;
+      if (p.hist) {  // this tile's histogram starts empty (the previous one has been written)
+        const int i = q * 32 + lane;
+        s_hist[i] = 0;
+        s_hist[i + 128] = 0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
       mbar_wait(&b.tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const int t = tile * TC_BM + q * 32 + lane;
@@ -377,6 +386,19 @@ __global__ void __launch_bounds__(G_THREADS, 2)
           for (int r = 0; r < KM; ++r)
             if (r < k) { wrow[r] = expf(lv[r] - m_run) / ssum; orow[r] = sel_e[r]; }
         }
+        if (p.hist) {
+#pragma unroll
+          for (int r = 0; r < KM; ++r)
+            if (r < k) atomicAdd(&s_hist[sel_e[r]], 1);
+        }
+      }
+      if (p.hist) {  // A3 histogram of this routing tile (integer counts: order-free)
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int i = q * 32 + lane;
+        int32_t* hrow = p.hist + (size_t)tile * n;
+        if (i < n) hrow[i] = s_hist[i];
+        if (i + 128 < n) hrow[i + 128] = s_hist[i + 128];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
       }
     }
   }
@@ -787,7 +809,8 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
   }
   GateFwdParams p{T, n, k, renorm, cached, b.logits, cached ? b.fresh_idx : b.idx, b.w,
                   b.hit_count, b.flags, cached ? b.idx_fix : nullptr,
-                  getenv("MOE_GATE_DBG") ? atoi(getenv("MOE_GATE_DBG")) : 0, tma_logits};
+                  getenv("MOE_GATE_DBG") ? atoi(getenv("MOE_GATE_DBG")) : 0, tma_logits,
+                  (!cached && b.gate_hist) ? b.tile_hist : nullptr};
   const int MT = (T + 127) / 128;
   // two CTAs per SM (4-stage rings): twice the epilogue warps, which bound this kernel
   const int grid = MT < 2 * g_sms ? MT : 2 * g_sms;
@@ -797,7 +820,7 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
                      : (k == 2 ? gate_fwd_tc_kernel<BN, ST, 2>                           \
                                : (k <= 4 ? gate_fwd_tc_kernel<BN, ST, 4>                 \
                                          : gate_fwd_tc_kernel<BN, ST, 8>));              \
-    size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 1024 + 4 * GF_STG_BYTES;             \
+    size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 1024 + 4 * GF_STG_BYTES + 1024;      \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \
     launch_pdl(kf, grid, G_THREADS, sm, s, mx, mw, ml, p, d);                                    \

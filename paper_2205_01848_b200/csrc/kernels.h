@@ -37,6 +37,7 @@ struct RouteBufs {
                           // compacted (dlb layout); null = off
   int32_t* drop_tok;      // [maxT] token of each compacted row
   int32_t* drop_cnt;      // [1] rows in the list (reset by route_scan, counted by combine_bwd)
+  int gate_hist;          // the tcgen05 gate also writes tile_hist (route_hist skipped)
   int o_pair;             // peer EP return rows: O (and dX) of pair (t, r) at row t k + r of the
                           // local return buffer, stored there by the owners' GEMM epilogues
   int32_t* idx_fix;       // cache fallback mode: the gate writes the fresh top-k of unknown

@@ -22,6 +22,11 @@
 
 using namespace moe;
 
+static bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] == '1';
+}
+
 int moe::pdl_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -191,6 +196,7 @@ void bind_buffers(moe_ctx* h) {
   r.dropb = nullptr;  // set per backward (fused dX only)
   r.dlr = nullptr;
   r.o_pair = 0;
+  r.gate_hist = 0;
   r.drop_tok = (int32_t*)(b + L.droptok);
   r.drop_cnt = meta + 783;
 }
@@ -531,6 +537,8 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     // fallback mode: the gate rewrites the rows of unknown samples with their fresh top-k
     rb.idx_fix = fallback ? rb.idx : nullptr;
     const int32_t* gc = fallback ? rb.idx : nullptr;
+    // A3 histogram inside the tcgen05 gate's epilogue when its top-k is the dispatch index
+    rb.gate_hist = h->use_tc && !fallback && !getenv_flag("MOE_NO_GATE_HIST");
     if (h->use_tc)
       KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, gc, rb, s0));
     else
@@ -543,7 +551,9 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
       KL(h, T > 0, "cache_update", s0, launch_cache_observe(h->ctab, h->ctab_num, k, h->cids, T,
                                                             rb.idx, rb.hit_count, rb.flags, s0));
   }
-  KL(h, T > 0, "route_hist", sd, launch_route_hist(rb.idx, T, k, n, rb.tile_hist, sd));
+  if (!rb.gate_hist)
+    KL(h, T > 0, "route_hist", sd, launch_route_hist(rb.idx, T, k, n, rb.tile_hist, sd));
+  rb.gate_hist = 0;
   KL(h, 1, "route_scan", sd, launch_route_scan(rb.tile_hist, ntiles, n, h->ct, rb, sd));
   if (!h->use_ep) {
     KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->cts, rb,
