@@ -11,11 +11,12 @@ from synth import make_dy, make_layer, to_numpy64
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("d", [64, 128])   # 128: 2-CTA GEMMs + fused dispatch backward (k = 1)
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("n,k,renorm", [(8, 2, 1), (16, 1, 0), (8, 2, 0)])
-def test_balance_and_spec_parity(dtype, n, k, renorm):
+def test_balance_and_spec_parity(dtype, n, k, renorm, d):
     from paper_2205_01848_b200 import MoELayer
-    T, d, f, lam = 700, 64, 128, 0.3
+    T, f, lam = 700, 2 * d, 0.3
     caps = O.capacities_from_factors([1.0] * n, T, k)
     cpu = make_layer(n, d, f, d, T, dtype)
     dy = make_dy(T, d, dtype)
@@ -38,7 +39,10 @@ def test_balance_and_spec_parity(dtype, n, k, renorm):
     p64 = {kk: to_numpy64(v) for kk, v in cpu.items() if kk != "x"}
     st = O.moe_forward(to_numpy64(cpu["x"]), p64, k, caps, renorm, logits=_np(rt["logits"]).astype(np.float64),
                        emulate_bf16=(dtype == "bf16"), balance_lambda=lam)
-    gr = O.moe_backward(st, to_numpy64(dy), dspec=to_numpy64(dspec), dw_ext=dw_ext.double().numpy())
+    mask = [_np(rt["h_buf"][rt["base"][e]: rt["base"][e] + int(st.routing.kept[e])]) > 0
+            for e in range(n)]   # ReLU' decisions in the kernel's precision
+    gr = O.moe_backward(st, to_numpy64(dy), dspec=to_numpy64(dspec), dw_ext=dw_ext.double().numpy(),
+                        relu_mask=mask)
     tol = TOL[dtype]
     assert abs(aux - st.extra["aux_loss"]) <= 1e-5 * abs(st.extra["aux_loss"])
     assert np.array_equal(valid, st.extra["spec_valid"])
