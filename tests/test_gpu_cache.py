@@ -17,10 +17,13 @@ def _layer(n, k, d, f, T, dtype, renorm=1):
     return MoELayer(n, k, d, f, 0, T, dtype, renorm, device="cuda")
 
 
-@pytest.mark.parametrize("dtype,k,renorm", [("bf16", 2, 1), ("f32", 1, 0), ("bf16", 1, 0)])
-def test_cache_epochs_match_oracle(dtype, k, renorm):
+@pytest.mark.parametrize("dtype,k,renorm,d", [("bf16", 2, 1, 64), ("f32", 1, 0, 64),
+                                              ("bf16", 1, 0, 64), ("bf16", 1, 0, 128)])
+def test_cache_epochs_match_oracle(dtype, k, renorm, d):
+    """d = 128: 2-CTA GEMMs, the histogram inside the gate epilogue (modes 0 / 3), the fused
+    combine (uncached modes) and dispatch backward."""
     from paper_2205_01848_b200 import AssignmentCache
-    n, d, f, T, N = 16, 64, 128, 256, 768
+    n, f, T, N = 16, 2 * d, 256, 768
     rng = np.random.default_rng(3)
     cpu = make_layer(n, d, f, d, N, dtype)
     g = {kk: v.cuda() for kk, v in cpu.items()}
