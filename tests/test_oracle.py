@@ -519,3 +519,33 @@ def test_loss_variants_finite_differences(renorm):
         xm = x.copy(); xm[ii] -= h
         num = (full(xp, p)[1] - full(xm, p)[1]) / (2 * h)
         assert abs(num - gr["dx"][ii]) <= 1e-4 * max(1.0, np.abs(gr["dx"]).max())
+
+
+def test_relu_mask_argument():
+    """relu_mask (the kernel's ReLU' decisions): the mask A > 0 reproduces the
+    default gradients exactly, and flipping one decision changes exactly that dA element --
+    dx / dW1 / db1 of its expert move by the outer products the chain rule predicts."""
+    x, p, st, dy = _fd_case(4, 2, 1, 1.0, 5)
+    g0 = O.moe_backward(st, dy)
+    g1 = O.moe_backward(st, dy, relu_mask=[a > 0 for a in st.A])
+    for kk in ("dx", "dw_gate", "dw1", "db1", "dw2", "db2", "dl"):
+        assert np.array_equal(g0[kk], g1[kk]), kk
+    e = max(range(len(st.A)), key=lambda j: st.A[j].shape[0])
+    mask = [a > 0 for a in st.A]
+    r, c = 0, int(np.argmax(st.A[e][0] > 0))
+    assert st.A[e][r, c] > 0
+    mask[e] = mask[e].copy()
+    mask[e][r, c] = False
+    g2 = O.moe_backward(st, dy, relu_mask=mask)
+    W2 = np.asarray(p["w2"][e], np.float64)
+    W1 = np.asarray(p["w1"][e], np.float64)
+    dA_rc = float(g0["dO"][e][r] @ W2[:, c])          # the element the flip removes
+    assert math.isclose(g0["db1"][e][c] - g2["db1"][e][c], dA_rc, rel_tol=1e-12, abs_tol=1e-15)
+    want_dW1 = np.zeros_like(g0["dw1"][e])
+    want_dW1[c] = dA_rc * st.X[e][r]
+    assert np.allclose(g0["dw1"][e] - g2["dw1"][e], want_dW1, rtol=1e-12, atol=1e-15)
+    assert np.allclose(g0["dX"][e][r] - g2["dX"][e][r], dA_rc * W1[c], rtol=1e-12, atol=1e-15)
+    others = [j for j in range(len(st.A)) if j != e]
+    for j in others:
+        assert np.array_equal(g0["dw1"][j], g2["dw1"][j])
+    assert np.array_equal(g0["dw2"], g2["dw2"])
