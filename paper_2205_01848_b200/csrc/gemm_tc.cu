@@ -507,7 +507,7 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   const bool two = use_2cta(N, KIND);
   const bool gat = KIND == TC_FWD1 && fz && fz->x;        // A rows gathered from x (N2)
   const bool comb = KIND == TC_FWD2 && fz && fz->y;       // fused combine (N2, k = 1)
-  const bool fdx = KIND == TC_DGRAD_X && fz && fz->dx;    // fused dispatch backward (k = 1)
+  const bool fdx = KIND == TC_DGRAD_X && fz && fz->dx_fused;  // fused dispatch backward (k = 1)
   const PeerBufs* pr = !fz ? nullptr
                        : KIND == TC_FWD2 ? &fz->pret_o : KIND == TC_DGRAD_X ? &fz->pret_dx : nullptr;
   const bool ret = pr && pr->nl != 0;                     // peer EP return rows (N1)

@@ -26,7 +26,9 @@ struct TcFusion {
   void* y = nullptr;              // y [T, d_out]; null = separate combine kernel
   const float* w = nullptr;       // gate weights [T] (k = 1)
   // dispatch backward in the dX GEMM (k = 1): dx[t] = dA[row] W1 + [hi|lo](dl)[row] [W_g;W_g]
-  void* dx = nullptr;             // dx [T, d]; null = dX buffer + gate_dx kernel
+  bool dx_fused = false;          // dispatch backward inside the dX GEMM (extra k-blocks)
+  void* dx = nullptr;             // dx [T, d] written by the epilogue (single GPU), or null
+                                  // (peer EP: the rows go to the token owners' dxret)
   const void* dlr = nullptr;      // [rows, 2 n_pad] bf16 hi | lo of dl in expert-row order
   const void* wg = nullptr;       // W_g [n, d]
   int n = 0, n_pad = 64, accumulate = 0;

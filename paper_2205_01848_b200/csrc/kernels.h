@@ -33,6 +33,7 @@ struct RouteBufs {
   const float* bal_g;     // [n] balance-term coefficients lambda*n*T_i/T_g (backward)
   int32_t* grow;          // [T x k] token-side dO/dX row of each pair or -1 (combine_bwd)
   __nv_bfloat16* dlr;     // [rows x 2 n_pad] hi | lo of dl by expert row (fused dX, k = 1)
+  PeerBufs pdlr;          // peer EP: the owners' dlr regions (nl == 0: dlr is local)
   __nv_bfloat16* dropb;   // fused dX (k = 1): [2 maxT x n_pad] dl pairs of dropped tokens,
                           // compacted (dlb layout); null = off
   int32_t* drop_tok;      // [maxT] token of each compacted row
@@ -68,6 +69,10 @@ cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T,
                             int pad_e0 = 0, const PeerBufs& px = PeerBufs{},
                             const PeerBufs& ptos = PeerBufs{}, const int32_t* pre_dev = nullptr,
                             void* y_zero = nullptr, int dout = 0);
+// fused dispatch backward in peer EP (k = 1): dx[t] = the (t, 0) row the owner's dX GEMM
+// returned (dX + dl W_g), for kept tokens (dropped ones come from the drop-only gate-dx pass)
+cudaError_t launch_dx_from_ret(const void* dxret, const int32_t* slot_of, int T, int d, void* dx,
+                               int accumulate, cudaStream_t s);
 cudaError_t launch_zero_pad(int dtype, void* buf, int cols, const int32_t* kept, int n,
                             const CapTable& ct, cudaStream_t s);
 cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, int k,

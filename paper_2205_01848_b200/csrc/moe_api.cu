@@ -158,7 +158,8 @@ void compute_layout(moe_ctx* h) {
   L.grow = take(T * k * 4);
   L.bpart = take(h->dtype == MOE_BF16 ? ((size_t)h->rows / 256 + h->n_local) * 2 * h->f * 4 : 0);
   // fused dispatch backward (k = 1, one GPU): [hi | lo](dl) by expert row
-  L.dropb = take(h->dtype == MOE_BF16 && k == 1 && !h->use_ep ? 2 * T * (size_t)h->n_pad * 2 : 0);
+  L.dropb = take(h->dtype == MOE_BF16 && k == 1 && (!h->use_ep || h->use_peer)
+                     ? 2 * T * (size_t)h->n_pad * 2 : 0);
   L.droptok = take(k == 1 ? T * 4 : 0);
   L.dlr = take(h->dtype == MOE_BF16 && k == 1 && !h->use_ep ? (size_t)h->rows * 2 * h->n_pad * 2 : 0);
   const bool ep = h->use_ep && !h->use_peer;  // NCCL transport buffers
@@ -195,6 +196,7 @@ void bind_buffers(moe_ctx* h) {
   r.grow = (int32_t*)(b + L.grow);
   r.dropb = nullptr;  // set per backward (fused dX only)
   r.dlr = nullptr;
+  r.pdlr = PeerBufs{};
   r.o_pair = 0;
   r.gate_hist = 0;
   r.drop_tok = (int32_t*)(b + L.droptok);
@@ -304,11 +306,7 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
   h->stream = (cudaStream_t)c.stream;
   const char* fs = getenv("MOE_FORCE_SIMT");
   h->use_tc = (c.dtype == MOE_BF16) && !(fs && fs[0] == '1');
-  {
-    const char* pr = getenv("MOE_PEER_RET");  // 0: combine / gate-dx read the owners' rows
-    h->peer_ret = h->use_peer && h->use_tc && tc_peer_return_supported(h->d, h->dout) &&
-                  !(pr && pr[0] == '0');
-  }
+
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -316,6 +314,11 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
     return MOE_ERR_CUDA;
   }
   h->use_peer = c.transport == MOE_TRANSPORT_PEER ? 1 : 0;
+  {
+    const char* pr = getenv("MOE_PEER_RET");  // 0: combine / gate-dx read the owners' rows
+    h->peer_ret = h->use_peer && h->use_tc && tc_peer_return_supported(h->d, h->dout) &&
+                  !(pr && pr[0] == '0');
+  }
   h->use_ep = (c.nccl_comm || h->use_peer) ? 1 : 0;
   if (h->use_peer) {  // the peer window, sized for the largest capacities allowed later
     int64_t wrows = c.window_rows;
@@ -728,10 +731,15 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                  : nullptr;
   // N2 dispatch backward fused into the dX GEMM (k = 1, one GPU, tcgen05): the combine
   // backward also writes [hi|lo](dl) by expert row, the GEMM adds dl W_g and writes dx rows
-  const bool fdx = h->use_tc && !h->use_ep && k == 1 && (h->fusion & MOE_FUSE_DX) && T > 0 &&
-                   a->dx != nullptr && ((uintptr_t)a->dx % 16) == 0 && tc_dx_fusion_supported(d);
-  rb.dlr = fdx ? (__nv_bfloat16*)(ws + h->L.dlr) : nullptr;
-  rb.dropb = fdx ? (__nv_bfloat16*)(ws + h->L.dropb) : nullptr;
+  const bool fdx_ok = h->use_tc && k == 1 && (h->fusion & MOE_FUSE_DX) && T > 0 &&
+                      a->dx != nullptr && ((uintptr_t)a->dx % 16) == 0 && tc_dx_fusion_supported(d);
+  const bool fdx = fdx_ok && !h->use_ep;
+  // peer EP (N1 return rows): the owners' dX GEMMs add dl W_g and return dx rows
+  const bool fdx_ep = fdx_ok && h->use_peer && h->peer_ret;
+  rb.dlr = fdx ? (__nv_bfloat16*)(ws + h->L.dlr)
+         : fdx_ep ? (__nv_bfloat16*)(h->pwin + h->PL.dlr) : nullptr;
+  rb.pdlr = fdx_ep ? peer_bufs(h, h->PL.dlr) : PeerBufs{};
+  rb.dropb = (fdx || fdx_ep) ? (__nv_bfloat16*)(ws + h->L.dropb) : nullptr;
 
   rb.o_pair = peer && h->peer_ret;
   KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O_tok, rb, T, k, n, dout, h->renorm, h->cts,
@@ -745,6 +753,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   rb.dw_ext = nullptr;
   rb.bal_g = nullptr;
   rb.dlr = nullptr;
+  rb.pdlr = PeerBufs{};
   rb.dropb = nullptr;
   if (peer) {  // N1: dO rows were stored into the owners by the combine backward
     KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DO, s0, (uint32_t*)rb.flags));
@@ -770,9 +779,10 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
       fz.pret_dx = peer_bufs(h, h->PL.dxret);
       fz.tpr = T;
     }
-    if (fdx) {
-      fz.dx = a->dx;
-      fz.dlr = ws + h->L.dlr;
+    if (fdx || fdx_ep) {
+      fz.dx_fused = true;
+      fz.dx = fdx ? a->dx : nullptr;
+      fz.dlr = fdx ? (void*)(ws + h->L.dlr) : (void*)(h->pwin + h->PL.dlr);
       fz.wg = fa.w_gate;
       fz.n = n;
       fz.n_pad = h->n_pad;
@@ -782,7 +792,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                                       h->rows, d, f, dout, kept_local, rb.mtile_prefix, nl,
                                       h->ct, h->max_cap_local, s0, &nk, &h->prof,
                                       (uint32_t*)(ws + h->L.mask), (float*)(ws + h->L.bpart),
-                                      (h->fused_gather || fdx || (peer && h->peer_ret)) ? &fz : nullptr);
+                                      (h->fused_gather || fdx || fdx_ep || (peer && h->peer_ret)) ? &fz : nullptr);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 backward failed");
   } else {
@@ -815,11 +825,15 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
     if (st != MOE_OK) return fail(h, st, err);
   }
   if (a->dx) {  // fused dX GEMM: it wrote the kept tokens, this pass only the dropped ones
+    if (fdx_ep)  // peer EP: the kept tokens' dx rows came back from the owners' dX GEMMs
+      KL(h, T > 0, "dx_from_ret", s0, launch_dx_from_ret(h->pwin + h->PL.dxret, rb.slot_of, T, d,
+                                                         a->dx, acc, s0));
+    const bool drop_only = fdx || fdx_ep;
     if (h->use_tc)
       KL(h, T > 0, "gate_dx", s0, launch_gate_dx_tc(fa.w_gate, dX_tok,
-                                                    fdx ? (void*)(ws + h->L.dropb) : dlb, h->maxT,
-                                                    h->n_pad, rb, T, k, n, d, h->cts, a->dx, acc,
-                                                    s0, pdx, fdx ? 1 : 0));
+                                                    drop_only ? (void*)(ws + h->L.dropb) : dlb,
+                                                    h->maxT, h->n_pad, rb, T, k, n, d, h->cts,
+                                                    a->dx, acc, s0, pdx, drop_only ? 1 : 0));
     else
       KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dX_tok, rb, T, k, n, d, h->cts, a->dx, acc, s0,
                                                  pdx));

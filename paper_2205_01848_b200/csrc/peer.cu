@@ -184,6 +184,9 @@ void peer_layout(PeerLayout& L, int64_t rows, int n, int d, int dout, size_t ele
   L.dxb = take((size_t)rows * d * elem);
   L.oret = take((size_t)pair_rows * dout * elem);
   L.dxret = take((size_t)pair_rows * d * elem);
+  // [hi | lo](dl) pairs of the local experts' rows (fused dispatch backward, k = 1), pushed
+  // by the token owners' combine backward
+  L.dlr = take((size_t)rows * 2 * ((n + 63) / 64 * 64) * elem);
   L.total = o;
 }
 

@@ -38,7 +38,7 @@ enum PeerPhase { PH_CNT = 0, PH_X = 1, PH_O = 2, PH_BAL = 3, PH_DO = 4, PH_DX = 
 
 struct PeerLayout {
   size_t epoch = 0, flags = 256, cnt = 512, bal = 0, dwg = 0, tos = 0, x = 0, o = 0, dob = 0,
-         dxb = 0, oret = 0, dxret = 0, total = 0;
+         dxb = 0, oret = 0, dxret = 0, dlr = 0, total = 0;
   int64_t rows = 0;  // rows of each expert buffer
 };
 

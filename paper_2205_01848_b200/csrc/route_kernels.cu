@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
     __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad, const T* __restrict__ dspec,
     const float* __restrict__ dw_ext, const float* __restrict__ bal_g,
     int32_t* __restrict__ grow, const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs po,
-    PeerBufs pdo, __nv_bfloat16* __restrict__ dlr, __nv_bfloat16* __restrict__ dropb,
+    PeerBufs pdo, __nv_bfloat16* __restrict__ dlr, PeerBufs pdlr, __nv_bfloat16* __restrict__ dropb,
     int32_t* __restrict__ drop_tok, int32_t* __restrict__ drop_cnt, int o_pair) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   // peer EP (N1): O rows are read from, and dO rows written to, the experts' owners
@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
       *reinterpret_cast<__nv_bfloat162*>(dlb + (size_t)t * n_pad + e0) = hi;
       *reinterpret_cast<__nv_bfloat162*>(dlb + ((size_t)maxT + t) * n_pad + e0) = lo;
       if (dlr && rows[0] >= 0) {  // k = 1 fused dispatch backward: the pair by expert row
-        __nv_bfloat16* rr = dlr + (size_t)rows[0] * 2 * n_pad;
+        __nv_bfloat16* rr = peer_row(dlr, pdlr, er[0], (size_t)rows[0], 2 * n_pad);
         *reinterpret_cast<__nv_bfloat162*>(rr + e0) = hi;
         *reinterpret_cast<__nv_bfloat162*>(rr + n_pad + e0) = lo;
       }
@@ -851,7 +851,7 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
                                                    renorm, (T*)dobuf, b.dw, b.dl,              \
                                                    (__nv_bfloat16*)dlb, maxT, n_pad,           \
                                                    (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow, pad_kept, \
-                                                   pad_e0, po, pdo, b.dlr, b.dropb,    \
+                                                   pad_e0, po, pdo, b.dlr, b.pdlr, b.dropb, \
                                                    b.drop_tok, b.drop_cnt, b.o_pair)
   const int km = k == 1 ? 1 : (k == 2 ? 2 : 8);
   if (vpl <= 2) { if (km == 1) CB(2, 1); else if (km == 2) CB(2, 2); else CB(2, 8); }
@@ -872,6 +872,37 @@ cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, Rout
                                         maxT, n_pad, pad_kept, s, pad_e0, po, pdo);
   return combine_bwd_t<float>(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf, dlb, maxT, n_pad,
                               pad_kept, s, pad_e0, po, pdo);
+}
+
+// Peer EP fused dispatch backward (k = 1): copy the returned dx rows of the kept tokens
+// (warp per token, 16-byte vectors; + the old dx when accumulating).
+__global__ void __launch_bounds__(256) dx_from_ret_kernel(
+    const __nv_bfloat16* __restrict__ ret, const int32_t* __restrict__ slot_of, int Tn, int d,
+    __nv_bfloat16* __restrict__ dx, int accumulate) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= Tn || slot_of[t] < 0) return;
+  for (int c = lane * 8; c < d; c += 256) {
+    uint4 v = ld_nc_v4(ret + (size_t)t * d + c);
+    if (accumulate) {
+      float a[8], o[8];
+      unpack(v, a, __nv_bfloat16());
+      unpack(ld_v4(dx + (size_t)t * d + c), o, __nv_bfloat16());
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] += o[j];
+      v = pack(a, __nv_bfloat16());
+    }
+    st_v4(dx + (size_t)t * d + c, v);
+  }
+}
+
+cudaError_t launch_dx_from_ret(const void* dxret, const int32_t* slot_of, int T, int d, void* dx,
+                               int accumulate, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  launch_pdl(dx_from_ret_kernel, (T + 7) / 8, 256, 0, s, (const __nv_bfloat16*)dxret, slot_of, T,
+             d, (__nv_bfloat16*)dx, accumulate);
+  return cudaGetLastError();
 }
 
 // =====================================================================================

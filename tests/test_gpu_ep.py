@@ -61,7 +61,7 @@ def test_ep_loopback_cached(comm):
 
 
 def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0, transport="nccl",
-                 iters=1, caps_seq=None):
+                 iters=1, caps_seq=None, fusion=0):
     """R expert-parallel ranks as threads on one GPU -- over the library's virtual NCCL-style
     communicator, or through the peer-memory transport (N1) with in-process windows -- against
     the single-GPU layer on the concatenated batch.  iters > 1 repeats forward+backward
@@ -112,6 +112,7 @@ def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0, tra
     def work(r):
         try:
             L = layers[r]
+            L.set_fusion(fusion)
             L.set_balance_loss(lam)
             if cached is not None:
                 L.set_cached_assignment(cached[r * T:(r + 1) * T].contiguous())
@@ -137,7 +138,7 @@ def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0, tra
         t.join(timeout=120)
     assert not errs, errs
     ref = MoELayer(n, k, d, f, 0, Tg, dtype, renorm, device="cuda")
-    ref.set_fusion(0)  # single-GPU N2 dx fusion rounds dX once: not bitwise comparable to EP
+    ref.set_fusion(fusion)  # the same N2 flags on both sides (the dx fusion rounds dX once)
     ref.set_capacities(caps)
     ref.set_balance_loss(lam)
     if cached is not None:
@@ -283,19 +284,24 @@ def test_peer_virtual_ranks_many_iterations_with_recompiles():
 
 
 @pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("fusion", [0, 6])
 @pytest.mark.parametrize("R", [2, 4])
 @pytest.mark.parametrize("k,renorm", [(1, 0), (2, 1)])
-def test_peer_return_rows_virtual_ranks(R, k, renorm):
+def test_peer_return_rows_virtual_ranks(R, k, renorm, fusion):
     """N1 return rows: with d, d_out multiples of 128 the owners' FWD2 / DGRAD_X epilogues
     store O / dX rows straight into the token owners' windows in (token, choice) order, and
     the combine / gate-dx kernels read them locally -- bitwise equal to the single-GPU layer
-    and to the owner-read form (MOE_PEER_RET=0)."""
+    and to the owner-read form (MOE_PEER_RET=0).  fusion 6 with k = 1: the owners' dX GEMMs
+    also add dl W_g (pairs pushed by the token owners' combine backward) and return dx rows
+    -- bitwise equal to the single-GPU fused dispatch backward."""
     import os
     n, T, d, f = 16, 512, 128, 256
-    out, ref = _run_virtual(R, n, k, T, d, f, "bf16", renorm, transport="peer")
+    out, ref = _run_virtual(R, n, k, T, d, f, "bf16", renorm, transport="peer", fusion=fusion)
     _check_virtual(out, ref, R, n, "bf16")
     for o in out[1:]:
         assert torch.equal(o[1]["dw_gate"], out[0][1]["dw_gate"])
+    if fusion:
+        return  # the owner-read form has no fused dispatch backward (compared at fusion 0)
     os.environ["MOE_PEER_RET"] = "0"
     try:
         out0, _ = _run_virtual(R, n, k, T, d, f, "bf16", renorm, transport="peer")
