@@ -13,7 +13,10 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_peer_transport_two_processes_ipc():
+@pytest.mark.parametrize("shape", ["", "ret"])
+def test_peer_transport_two_processes_ipc(shape):
+    """shape "ret": d = 128, top-1 -- the owners' GEMM epilogues store O and dx rows into
+    the other PROCESS's window (return rows + fused dispatch backward)."""
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -21,7 +24,8 @@ def test_peer_transport_two_processes_ipc():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "workers", "peer_ipc_worker.py")]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT,
+                       env=dict(os.environ, IPC_SHAPE=shape))
     out = p.stdout + p.stderr
     assert p.returncode == 0, out[-3000:]
     assert out.count(": OK") == 2, out[-3000:]

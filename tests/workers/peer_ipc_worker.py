@@ -20,13 +20,16 @@ def main():
     from paper_2205_01848_b200 import MoELayer
     from paper_2205_01848_b200.dist import peer_connect
     from synth import make_dy, make_layer
-    n, k, T, d, f, dtype = 8, 2, 256, 64, 128, "bf16"
+    # IPC_SHAPE=ret: d = 128, top-1, raw weights -> return rows + fused dispatch backward
+    ret = os.environ.get("IPC_SHAPE", "") == "ret"
+    n, k, T, d, f, dtype = (8, 1, 256, 128, 256, "bf16") if ret else (8, 2, 256, 64, 128, "bf16")
+    renorm = 0 if ret else 1
     Tg = R * T
     cpu = make_layer(n, d, f, d, Tg, dtype)
     g = {kk: v.cuda() for kk, v in cpu.items()}
     dy = make_dy(Tg, d, dtype).cuda()
     caps = O.capacities_from_factors([1.0] * n, Tg, k)
-    L = MoELayer(n, k, d, f, 0, T, dtype, 1, world_size=R, rank=r, device="cuda:0",
+    L = MoELayer(n, k, d, f, 0, T, dtype, renorm, world_size=R, rank=r, device="cuda:0",
                  transport="peer")
     peer_connect(L)
     L.set_capacities(caps)
@@ -34,7 +37,7 @@ def main():
         y = L.forward(g["x"][r * T:(r + 1) * T], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
         gr = L.backward(dy[r * T:(r + 1) * T].contiguous())
     torch.cuda.synchronize()
-    ref = MoELayer(n, k, d, f, 0, Tg, dtype, 1, device="cuda:0")
+    ref = MoELayer(n, k, d, f, 0, Tg, dtype, renorm, device="cuda:0")
     ref.set_capacities(caps)
     y_ref = ref.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
     gr_ref = ref.backward(dy)
