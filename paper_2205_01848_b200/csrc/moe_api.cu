@@ -812,6 +812,26 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   // B4: dx = gather(dX) + dl W_g ;  B5: dW_g = dl^T x
   void* dX_tok = dXb;
   PeerBufs pdx{};
+  // peer EP: the gate-weight gradient partial needs only local data (dl, x); computed before
+  // the exchange barrier, one barrier then covers the returned dX rows and every rank's
+  // dW_g partial
+  float* dwg_f32 = peer ? (float*)(h->pwin + h->PL.dwg) : nccl_ep ? (float*)(ws + h->L.dwg32) : nullptr;
+  auto gate_dw_partial = [&]() -> moe_status_t {
+    if (h->use_tc) {
+      KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw_tc(dlb, h->maxT, h->n_pad, fa.x, T, n, d,
+                                                            (float*)(ws + h->L.partial), a->dw_gate, acc, s0, dwg_f32));
+    } else {
+      int splits = gate_dw_splits(h->maxT, d);
+      KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw(dt, rb.dl, fa.x, T, n, d, (float*)(ws + h->L.partial),
+                                          splits, a->dw_gate, acc, s0, dwg_f32));
+    }
+    if (T == 0 && dwg_f32) CUDA_TRY(h, cudaMemsetAsync(dwg_f32, 0, (size_t)n * d * 4, s0));  // no tokens
+    return MOE_OK;
+  };
+  if (peer && a->dw_gate) {
+    moe_status_t st = gate_dw_partial();
+    if (st != MOE_OK) return st;
+  }
   if (peer) {  // N1: the gate-input gradient reads dX rows from the owners (or, with return
                // rows, this rank's own (token, choice) rows the owners stored)
     KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DX, s0, (uint32_t*)rb.flags));
@@ -839,25 +859,17 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                                                  pdx));
   }
   if (a->dw_gate) {
-    float* f32 = peer ? (float*)(h->pwin + h->PL.dwg)          // N1: pulled by every rank
-                 : nccl_ep ? (float*)(ws + h->L.dwg32) : nullptr;  // EP: all-reduce in fp32
-    if (h->use_tc) {
-      KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw_tc(dlb, h->maxT, h->n_pad, fa.x, T, n, d,
-                                                            (float*)(ws + h->L.partial), a->dw_gate, acc, s0, f32));
-    } else {
-      int splits = gate_dw_splits(h->maxT, d);
-      KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw(dt, rb.dl, fa.x, T, n, d, (float*)(ws + h->L.partial),
-                                          splits, a->dw_gate, acc, s0, f32));
+    if (!peer) {
+      moe_status_t st = gate_dw_partial();
+      if (st != MOE_OK) return st;
     }
-    if (T == 0 && f32) CUDA_TRY(h, cudaMemsetAsync(f32, 0, (size_t)n * d * 4, s0));  // no tokens
-    if (peer) {  // N1: sum of every rank's fp32 partial in rank order
-      KL(h, 1, "peer_barrier", s0, launch_peer_barrier(h->wins, h->R, h->rank, PH_DW, s0, (uint32_t*)rb.flags));
+    if (peer) {  // N1: sum of every rank's fp32 partial in rank order (after the PH_DX barrier)
       KL(h, 1, "gate_dw", s0, launch_peer_sum(h->wins, h->PL.dwg, h->R, (size_t)n * d, dt,
                                               a->dw_gate, acc, s0));
     } else if (h->use_ep) {  // C6
-      moe_status_t st = ep_allreduce_f32(h->ep, f32, (size_t)n * d, s0, &err);
+      moe_status_t st = ep_allreduce_f32(h->ep, dwg_f32, (size_t)n * d, s0, &err);
       if (st != MOE_OK) return fail(h, st, err);
-      KL(h, 1, "gate_dw", s0, launch_f32_to(dt, f32, (size_t)n * d, a->dw_gate, acc, s0));
+      KL(h, 1, "gate_dw", s0, launch_f32_to(dt, dwg_f32, (size_t)n * d, a->dw_gate, acc, s0));
     }
   }
   h->have_fwd = 0;  // H has been consumed

@@ -60,6 +60,8 @@ __global__ void __launch_bounds__(256) peer_plan_kernel(PeerBufs win, int R, int
                                                         int32_t* kept_out, int32_t* mtile_prefix,
                                                         int64_t* drops_out, int32_t* pre_out,
                                                         uint32_t* err_flags) {
+  pdl_wait();  // PDL: predecessor complete + visible; no early trigger: the next
+  // kernel must not take SMs while this one spins on peers (ranks sharing one GPU deadlock)
   __shared__ uint32_t s_ep;
   __shared__ long long s_drops[8];
   __shared__ int32_t s_tiles[MOE_MAX_E];
@@ -131,6 +133,8 @@ __global__ void __launch_bounds__(256) peer_plan_kernel(PeerBufs win, int R, int
 
 __global__ void peer_barrier_kernel(PeerBufs win, int R, int rank, int phase,
                                     uint32_t* err_flags) {
+  pdl_wait();  // PDL: predecessor complete + visible; no early trigger: the next
+  // kernel must not take SMs while this one spins on peers (ranks sharing one GPU deadlock)
   const uint32_t ep = *reinterpret_cast<const volatile uint32_t*>(win.p[rank]);
   barrier_block(win, R, rank, phase, ep, err_flags);
 }
@@ -139,6 +143,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) peer_sum_kernel(PeerBufs win, size_t off, int R,
                                                        size_t count, T* __restrict__ out,
                                                        int accumulate) {
+  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const size_t n4 = count / 4;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
        i += (size_t)gridDim.x * blockDim.x) {
@@ -193,7 +198,7 @@ void peer_layout(PeerLayout& L, int64_t rows, int n, int d, int dout, size_t ele
 cudaError_t launch_peer_plan(const PeerBufs& win, int R, int rank, int n, int n_local,
                              const int32_t* local_counts, const CapTable& ct, RouteBufs b,
                              int32_t* pre_out, cudaStream_t s) {
-  peer_plan_kernel<<<1, 256, 0, s>>>(win, R, rank, n, n_local, local_counts, ct, b.counts,
+  launch_pdl(peer_plan_kernel, 1, 256, 0, s, win, R, rank, n, n_local, local_counts, ct, b.counts,
                                      b.kept, b.mtile_prefix, b.drops, pre_out,
                                      reinterpret_cast<uint32_t*>(b.flags));
   return cudaGetLastError();
@@ -201,7 +206,7 @@ cudaError_t launch_peer_plan(const PeerBufs& win, int R, int rank, int n, int n_
 
 cudaError_t launch_peer_barrier(const PeerBufs& win, int R, int rank, int phase, cudaStream_t s,
                                 uint32_t* err_flags) {
-  peer_barrier_kernel<<<1, 32, 0, s>>>(win, R, rank, phase, err_flags);
+  launch_pdl(peer_barrier_kernel, 1, 32, 0, s, win, R, rank, phase, err_flags);
   return cudaGetLastError();
 }
 
@@ -210,10 +215,10 @@ cudaError_t launch_peer_sum(const PeerBufs& win, size_t off, int R, size_t count
   if (count == 0) return cudaSuccess;
   const int grid = (int)std::min<size_t>((count / 4 + 255) / 256 + 1, 148 * 4);
   if (dtype == 1)
-    peer_sum_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(win, off, R, count,
+    launch_pdl(peer_sum_kernel<__nv_bfloat16>, grid, 256, 0, s, win, off, R, count,
                                                         (__nv_bfloat16*)out, accumulate);
   else
-    peer_sum_kernel<float><<<grid, 256, 0, s>>>(win, off, R, count, (float*)out, accumulate);
+    launch_pdl(peer_sum_kernel<float>, grid, 256, 0, s, win, off, R, count, (float*)out, accumulate);
   return cudaGetLastError();
 }
 
