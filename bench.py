@@ -327,12 +327,20 @@ def run_ours(args):
     clk.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    marks = []  # per-step boundaries (median / p10 / p90 of the step time)
     for _ in range(args.steps):
         step()
+        m = torch.cuda.Event(enable_timing=True)
+        m.record(stream)
+        marks.append(m)
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     ms = ev0.elapsed_time(ev1)
     clocks = clk.stop()
+    per_step = sorted([ev0.elapsed_time(marks[0])] +
+                      [marks[i - 1].elapsed_time(marks[i]) for i in range(1, len(marks))])
+    q = lambda f: per_step[min(len(per_step) - 1, int(f * (len(per_step) - 1) + 0.5))]  # noqa: E731
+    step_stats = {"median": round(q(0.5), 4), "p10": round(q(0.1), 4), "p90": round(q(0.9), 4)}
     barrier()
     launches = layer.launch_count() - l0
     _, dev_flags = layer.check_flags()   # NaN logits / peer-barrier timeout: the run is invalid
@@ -497,6 +505,7 @@ def run_ours(args):
             "roofline": roofline,
             "device_flags": dev_flags,
             "ms_per_step_profiled": round(prof_ms_step, 4),
+            "step_ms": step_stats,
             "hbm_gbs": hbm,
             "kernels": kernels,
             "cpu_baseline": cpu_base,
