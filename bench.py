@@ -501,6 +501,8 @@ def run_ours(args):
                        "fusion": "+".join([nm for nm, on in (("gather", gather), ("combine", fcomb),
                                                              ("dx", fdx)) if on]) or "none",
                        "kept_assignments": A, "drops": stats["drops"],
+                       "drop_rate": round(stats["drops"] / max(1, T * k * (ws if use_ep else 1)), 5),
+                       "sum_capacity_rows": int(sum(layer.capacities)),
                        "padding_flops_avoided": padded_flops},
             "roofline": roofline,
             "device_flags": dev_flags,
