@@ -45,7 +45,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _needs(obj, [src] + headers):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+            cmd = [NVCC, *ARCH, *FLAGS, *os.environ.get("MOE_NVCC_EXTRA", "").split(), "-c", src,
+                   "-o", obj]
             if os.environ.get("MOE_PTXAS_V"):
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)
