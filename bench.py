@@ -270,6 +270,11 @@ def run_ours(args):
     gather = tc1 and bool(fflags & 1) and d % 128 == 0 and f % 128 == 0
     fcomb = tc1 and bool(fflags & 2) and k == 1 and do % 128 == 0 and not args.cached
     fdx = tc1 and bool(fflags & 4) and k == 1 and d % 128 == 0
+    # peer EP (N1): return rows from the GEMM epilogues, and the dispatch backward in the
+    # owners' dX GEMMs (k = 1)
+    pret = (peer and cfg.dtype == "bf16" and getattr(layer, "uses_tcgen05", False)
+            and d % 128 == 0 and do % 128 == 0)
+    fdx_ep = pret and bool(fflags & 4) and k == 1
     layer.set_fusion(fflags)
     tdt = layer.tdtype
     grads = dict(dx=torch.empty(T, d, dtype=tdt, device=dev),
@@ -499,7 +504,8 @@ def run_ours(args):
                                        if use_ep else "1 GPU"),
                        "l2": "inputs > L2 (x 134 MB + weights 1 GB), no flush",
                        "fusion": "+".join([nm for nm, on in (("gather", gather), ("combine", fcomb),
-                                                             ("dx", fdx)) if on]) or "none",
+                                                             ("dx", fdx or fdx_ep),
+                                                             ("return_rows", pret)) if on]) or "none",
                        "kept_assignments": A, "drops": stats["drops"],
                        "drop_rate": round(stats["drops"] / max(1, T * k * (ws if use_ep else 1)), 5),
                        "sum_capacity_rows": int(sum(layer.capacities)),
