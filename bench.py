@@ -219,6 +219,7 @@ def kernel_work(cfg, T, A, s, A_tok=None, gather=False, fcomb=False, fdx=False):
         "gate_dx": ("byte", ((T - A) * (d * s + 4 * n) + 4 * T * k) if fdx
                     else ((A + T) * d * s + 4 * T * n + 8 * T * k)),
         "gate_dw": ("byte", T * d * s + 4 * T * n),
+        "dx_from_ret": ("byte", 2 * A * d * s + 4 * T * k),  # returned dx rows -> dx (peer EP)
     }
 
 
@@ -389,7 +390,7 @@ def run_ours(args):
 
     # ---------------- per-kernel rooflines ----------------
     pk = peaks()
-    work = kernel_work(cfg, T, A, s, A_tok, gather=gather, fcomb=fcomb, fdx=fdx)
+    work = kernel_work(cfg, T, A, s, A_tok, gather=gather, fcomb=fcomb, fdx=fdx or fdx_ep)
     sm_peak_tf = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
     kernels = {}
     for name, (cnt, tot) in ktimes.items():
