@@ -557,9 +557,23 @@ def cpu_oracle_sample(cfg, g, dy, tokens, alpha):
     st = O.moe_forward(x, p, k, caps, cfg.renormalize)
     O.moe_backward(st, dyn)
     dt = time.perf_counter() - t0
-    return {"value": round(Ts / dt, 2), "unit": "tokens/s", "cores": _threads(), "kind": "oracle",
-            "sample": f"{Ts} tokens of {cfg.name} (all {n} experts, alpha {alpha}), fwd+bwd, fp64 NumPy",
-            "seconds": round(dt, 2)}
+    out = {"value": round(Ts / dt, 2), "unit": "tokens/s", "cores": _threads(), "kind": "oracle",
+           "sample": f"{Ts} tokens of {cfg.name} (all {n} experts, alpha {alpha}), fwd+bwd, fp64 NumPy",
+           "seconds": round(dt, 2)}
+    try:  # the same oracle on one core (BLAS limited to one thread), a quarter of the sample
+        from threadpoolctl import threadpool_limits
+        Ts1 = max(64, Ts // 4)
+        caps1 = O.capacities_from_factors([alpha] * n, Ts1, k)
+        with threadpool_limits(limits=1):
+            t0 = time.perf_counter()
+            st = O.moe_forward(x[:Ts1], p, k, caps1, cfg.renormalize)
+            O.moe_backward(st, dyn[:Ts1])
+            dt1 = time.perf_counter() - t0
+        out["single_thread"] = {"value": round(Ts1 / dt1, 2), "cores": 1, "tokens": Ts1,
+                                "seconds": round(dt1, 2)}
+    except Exception as ex:  # threadpoolctl missing: report the all-core number only
+        out["single_thread"] = {"unavailable": str(ex)[:80]}
+    return out
 
 
 def run_reference(args):
