@@ -767,6 +767,8 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
                                            : rows[r];
     }
   float m = -INFINITY, sp = 0.f, cb = 0.f;
+  float ens = 0.f;     // raw mode: exp mass of the experts NOT selected for this token
+  float esel[KM];      // raw mode: exp(l - m) of each selected expert
   if (need_p) {
 #pragma unroll
     for (int j = 0; j < NL; ++j) m = fmaxf(m, fmaxf(lg[j][0], lg[j][1]));
@@ -774,11 +776,23 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
-      const int e = 2 * lane + 64 * j;
-      if (e < n) sp += expf(lg[j][0] - m);
-      if (e + 1 < n) sp += expf(lg[j][1] - m);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = 2 * lane + 64 * j + h;
+        if (e >= n) continue;
+        const float ex = expf(lg[j][h] - m);
+        sp += ex;
+        bool sel = false;
+#pragma unroll
+        for (int r = 0; r < KM; ++r) sel |= (r < k && er[r] == e);
+        if (!sel) ens += ex;
+      }
     }
     sp = __shfl_sync(0xffffffffu, warp_sum(sp), 0);
+    ens = __shfl_sync(0xffffffffu, warp_sum(ens), 0);
+#pragma unroll
+    for (int r = 0; r < KM; ++r)
+      esel[r] = (r < k && er[r] >= 0 && er[r] < n) ? expf(l[er[r]] - m) : 0.f;
     if (bal_g) {  // Eq. 3 balance term: dB/dl = p (g - <p, g>), g_i = lambda n T_i / T_g
 #pragma unroll
       for (int j = 0; j < NL; ++j) {
@@ -801,17 +815,44 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
       const int e = e0 + h;
       float v = 0.f;
       if (e < n) {
+        // The closed forms rewritten without the cancellation of dw_r against sum w dw (a
+        // confident router, w_r -> 1, would otherwise lose every significant digit of dl in
+        // fp32): renorm dl_r = w_r (dw_r - sum_s w_s dw_s) = w_r sum_{s != r} w_s (dw_r - dw_s)
+        // since sum w = 1; raw dl_j = p_j (dp_j - sum_s p_s dw_s) with 1 - p_j expanded as the
+        // exp mass of every other expert.  Same value in exact arithmetic.
         if (renorm) {
 #pragma unroll
-          for (int r = 0; r < KM; ++r)
-            if (er[r] == e) v = wr[r] * (dwr[r] - c);
+          for (int r = 0; r < KM; ++r) {
+            if (r >= k || er[r] != e) continue;
+            float a = 0.f;
+#pragma unroll
+            for (int s2 = 0; s2 < KM; ++s2)
+              if (s2 < k && s2 != r) a = fmaf(wr[s2], dwr[r] - dwr[s2], a);
+            v = wr[r] * a;
+          }
         } else {
           const float p = expf(lg[j][h] - m) / sp;
-          float dp = 0.f;
+          int rs = -1;
 #pragma unroll
           for (int r = 0; r < KM; ++r)
-            if (er[r] == e) dp = dwr[r];
-          v = p * (dp - c);
+            if (r < k && er[r] == e) rs = r;
+          if (rs < 0) {
+            v = -p * c;
+          } else {
+            float osum = ens, other = 0.f;
+            float dws = 0.f;
+#pragma unroll
+            for (int s2 = 0; s2 < KM; ++s2) {
+              if (s2 >= k) continue;
+              if (s2 == rs) {
+                dws = dwr[s2];
+              } else {
+                osum += esel[s2];
+                other = fmaf(wr[s2], dwr[s2], other);
+              }
+            }
+            v = p * (dws * (osum / sp) - other);
+          }
         }
         if (bal_g) v = fmaf(expf(lg[j][h] - m) / sp, bal_g[e] - cb, v);
         dlrow[e] = v;

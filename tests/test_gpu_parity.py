@@ -233,3 +233,34 @@ def test_multitile_stress_bf16(k, renorm):
     layer, gpu, st, gr, ol = run_pair(n, k, d, f, T, "bf16", caps, renorm)
     assert_routing_exact(gpu, st, k)
     assert_values(gpu, st, gr, ol, "bf16")
+
+
+@pytest.mark.parametrize("k,renorm", [(2, 1), (1, 0), (2, 0)])
+def test_confident_router_dl_precision(k, renorm):
+    """A near one-hot router (W_g scaled x25: the top probability is ~1): dl is a tiny
+    difference of the experts' dw, and the cancellation-free closed forms keep it within the
+    fp32 budget of the oracle (the plain w_r (dw_r - sum w dw) loses ~5 digits here)."""
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer, to_numpy64
+    n, d, f, T = 8, 64, 128, 600
+    cpu = make_layer(n, d, f, d, T, "f32")
+    cpu["w_gate"] = cpu["w_gate"] * 25.0
+    dy = make_dy(T, d, "f32")
+    caps = capacity_from_factors([4.0] * n, T, k)
+    layer = MoELayer(n, k, d, f, 0, T, "f32", renorm, device="cuda")
+    layer.set_capacities(caps)
+    g = {kk: v.cuda() for kk, v in cpu.items()}
+    layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+    rt = layer.routing(T)
+    grads = layer.backward(dy.cuda())
+    torch.cuda.synchronize()
+    p64 = {kk: to_numpy64(v) for kk, v in cpu.items() if kk != "x"}
+    st = O.moe_forward(to_numpy64(cpu["x"]), p64, k, caps, renorm,
+                       logits=rt["logits"].cpu().double().numpy())
+    mask = [rt["h_buf"][rt["base"][e]: rt["base"][e] + int(st.routing.kept[e])].cpu().numpy() > 0
+            for e in range(n)]
+    gr = O.moe_backward(st, to_numpy64(dy), relu_mask=mask)
+    assert float(np.max(st.p)) > 0.999999   # the regime this test is about
+    dl = layer.routing(T)["dl"].cpu().double().numpy()
+    assert rel(dl, gr["dl"]) <= 1e-5
+    assert rel(to_numpy64(grads["dw_gate"]), gr["dw_gate"]) <= 1e-5
