@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 def _cases():
     rng = np.random.default_rng(2205)
     out = []
-    for i in range(80):
+    for i in range(160):
         dtype = "bf16" if i % 3 else "f32"
         n = int(rng.choice([3, 8, 16, 40, 64, 130]))
         k = int(min(n, rng.choice([1, 1, 2, 2, 4, 8])))
@@ -45,7 +45,7 @@ def test_fuzz_vs_oracle(dtype, n, k, d, f, d_out, T, alpha, renorm, regime, fusi
 def _ep_cases():
     rng = np.random.default_rng(1848)
     out = []
-    for i in range(20):
+    for i in range(30):
         R = int(rng.choice([2, 4]))
         n = R * int(rng.choice([1, 2, 4, 8]))
         k = int(min(n, rng.choice([1, 2, 2, 4])))
