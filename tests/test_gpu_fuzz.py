@@ -147,3 +147,38 @@ def test_fuzz_features_vs_oracle(dtype, n, k, d, f, T, renorm, cached, lam, spec
     # accumulated bf16 gradients carry one extra rounding per step
     for kk in ("dx", "dw_gate", "dw1", "db1", "dw2", "db2"):
         assert rel(to_numpy64(grads[kk]), want[kk]) <= (tol if dtype == "f32" else 2 * tol), kk
+
+
+def _ep_feature_cases():
+    rng = np.random.default_rng(2021)
+    out = []
+    for i in range(12):
+        R = int(rng.choice([2, 4]))
+        n = R * int(rng.choice([2, 4]))
+        k = int(min(n, rng.choice([1, 2])))
+        dtype = "f32" if i % 4 == 0 else "bf16"
+        d = int(rng.choice([64, 128]))
+        f = 2 * d
+        T = int(rng.choice([128, 256]))
+        renorm = int(rng.integers(0, 2))
+        transport = str(rng.choice(["peer", "nccl"]))
+        cached = float(rng.choice([-1.0, 0.03]))
+        lam = float(rng.choice([0.0, 0.2]))
+        fusion = int(rng.choice([0, 6]))
+        out.append((R, n, k, dtype, d, f, T, renorm, transport, cached, lam, fusion))
+    return out
+
+
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("R,n,k,dtype,d,f,T,renorm,transport,cached,lam,fusion", _ep_feature_cases())
+def test_fuzz_ep_features(R, n, k, dtype, d, f, T, renorm, transport, cached, lam, fusion):
+    """Expert-parallel ranks with cached assignments, the balance term, N2 flags and three
+    iterations with capacity changes (recompiles) in between, bitwise against one GPU."""
+    from oracle import moe_oracle as O
+    from test_gpu_ep import _check_virtual, _run_virtual
+    Tg = R * T
+    seq = [O.capacities_from_factors([a] * n, Tg, k) for a in (1.0, 0.5, 1.5)]
+    out, ref = _run_virtual(R, n, k, T, d, f, dtype, renorm, transport=transport,
+                            cached_frac=(cached if cached >= 0 else None), lam=lam, iters=3,
+                            caps_seq=seq, fusion=fusion)
+    _check_virtual(out, ref, R, n, dtype)
