@@ -315,7 +315,12 @@ MOE_API moe_status_t moe_vcomm_destroy(void* comm);
  * the owners' X buffers, combine reads O rows from them, the combine backward stores dO rows
  * into them and the gate-input gradient reads dX rows from them; the counts, dW_g and the
  * balance sums are exchanged through the windows; one-block barrier kernels order producer
- * and consumer kernels across ranks.  Every rank must call moe_forward / moe_backward the
+ * and consumer kernels across ranks.  Return rows (bf16 with d and d_out multiples of 128;
+ * MOE_PEER_RET=0 disables): the owners' second expert GEMM and dX GEMM store O / dX rows
+ * straight into the TOKEN owner's window at row t*k + r from their epilogues, and combine /
+ * gate-dx read them locally; with MOE_FUSE_DX (k = 1) the combine backward also pushes each
+ * kept pair's dl pair to the owner, whose dX GEMM returns dx rows (dX + dl W_g).  A barrier
+ * whose peer never arrives gives up after 20 s and raises device flag bit 3.  Every rank must call moe_forward / moe_backward the
  * same number of times (the barrier epochs advance in lockstep).  Routing, outputs and
  * gradients equal the NCCL path and the single-GPU path on the concatenated batch
  * (reading 12); dW_g is summed in rank order (identical on every rank). */
