@@ -259,8 +259,17 @@ def run_ours(args):
                      transport="peer" if peer else "nccl")
     if peer:  # open every rank's peer window (CUDA IPC handles over the process group)
         if ws > 1:
-            from paper_2205_01848_b200.dist import peer_connect
-            peer_connect(layer)
+            from paper_2205_01848_b200.dist import nccl_comm_ptr, peer_connect
+            if not peer_connect(layer, strict=False):
+                # some rank could not map its peers' windows (no CUDA IPC / P2P on this box):
+                # every rank switches to the NCCL transport together (stated in the config)
+                print("bench: peer windows unavailable on some rank; using the NCCL transport",
+                      file=sys.stderr)
+                del layer
+                peer = False
+                comm = nccl_comm_ptr(device=dev)
+                layer = MoELayer(n, k, d, f, do, T, cfg.dtype, cfg.renormalize, world_size=ws,
+                                 rank=rank, nccl_comm=comm, device=dev, transport="nccl")
         else:
             layer.peer_attach([layer.peer_window()])
     layer.set_capacity_factors([alpha] * n, T * (ws if use_ep else 1))

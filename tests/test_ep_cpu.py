@@ -102,3 +102,53 @@ def test_ep_plan_gloo_world2(R, n, k):
             if kl_a[r, e]:
                 assert pre_a[r, e] + kl_a[r, e] <= cap[e]
                 assert pre_a[r, e] == kl_a[:r, e].sum()       # no gap before rank r's block
+
+
+class _FakeLayer:
+    """Stands in for MoELayer's IPC window calls: rank `bad` cannot open its peers' windows."""
+
+    def __init__(self, rank, bad):
+        self.rank, self.bad, self.got = rank, bad, None
+
+    def peer_export(self):
+        return bytes([self.rank]) * 64
+
+    def peer_import(self, handles):
+        if self.rank == self.bad:
+            raise RuntimeError("cudaIpcOpenMemHandle failed")
+        self.got = [h[0] for h in handles]
+
+
+def _connect_worker(rank, R, port, bad, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=R)
+    from paper_2205_01848_b200.dist import peer_connect
+    L = _FakeLayer(rank, bad)
+    ok = peer_connect(L, strict=False)
+    try:
+        peer_connect(_FakeLayer(rank, bad), strict=True)
+        strict_raised = False
+    except RuntimeError:
+        strict_raised = True
+    q.put((rank, ok, strict_raised, L.got))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("bad", [-1, 1])
+def test_peer_connect_ranks_agree(bad):
+    """Every rank learns whether EVERY rank opened the windows (bench.py then switches all
+    ranks to the NCCL transport together instead of hanging or diverging)."""
+    R = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_connect_worker, args=(r, R, port, bad, q)) for r in range(R)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(R))
+    for p in ps:
+        p.join(timeout=60)
+    for rank, ok, strict_raised, got in res:
+        assert ok == (bad < 0) and strict_raised == (bad >= 0)
+        if rank != bad:
+            assert got == list(range(R))
