@@ -69,7 +69,7 @@ def _check_routing(cfg, rt, caps):
     return lg, idx, ort
 
 
-def _group_oracle(cfg, g, toks, lg, idx, slot_of, h_rows=None, dy=None):
+def _group_oracle(cfg, g, toks, lg, idx, slot_of, h_rows=None, dy=None, cached=False):
     """The oracle on the tokens `toks` alone (ascending), with capacities that keep exactly
     their kept pairs: callers pass groups in which every pair is kept, or every pair
     dropped, or a single token."""
@@ -84,7 +84,8 @@ def _group_oracle(cfg, g, toks, lg, idx, slot_of, h_rows=None, dy=None):
     for key in ("w1", "b1", "w2", "b2"):
         params[key] = _Experts(g[key], used)
     st = O.moe_forward(to_numpy64(g["x"][toks]), params, k, caps, cfg.renormalize,
-                       logits=lg[toks], emulate_bf16=(cfg.dtype == "bf16"))
+                       logits=lg[toks], emulate_bf16=(cfg.dtype == "bf16"),
+                       cached_idx=np.ascontiguousarray(idx[toks]) if cached else None)
     gr = None
     if dy is not None:   # ReLU' decisions from the kernel's H rows, in the oracle's slot order
         rows = [[] for _ in range(n)]
@@ -167,3 +168,54 @@ def test_c4_full_size_forward_vs_oracle():
     torch.cuda.synchronize()
     assert layer.check_flags()[1] == 0
     assert all(bool(torch.isfinite(v.float()).all()) for v in grads.values())
+
+
+@pytest.mark.timeout(600)
+def test_c5_full_size_cached_vs_oracle():
+    """c5 (c3 shape with sample-assignment caching, §4.2) in the bench's launch
+    configuration, with 3 % of the cached rows stale: dispatch follows the cached indices,
+    the fresh top-k and the hit count follow the kernel's logits, the whole batch's grouping
+    is the oracle's, and sampled tokens' y and dx match the oracle in cached mode."""
+    from synth import perturb_cached
+    cfg, g, layer, caps = _setup("c5")
+    n, k, T = cfg.n_experts, cfg.top_k, cfg.tokens
+    dy = make_dy(T, cfg.d_out, cfg.dtype, device="cuda")
+    # the cached table is an input: the oracle's own top-k (fp64 logits), 3 % rows replaced
+    fresh0 = O.topk_sorted(O.gate_logits(to_numpy64(g["x"]), to_numpy64(g["w_gate"])), k)
+    cidx = np.ascontiguousarray(perturb_cached(fresh0, n, 0.03), dtype=np.int32)
+    layer.set_cached_assignment(torch.from_numpy(cidx).cuda())
+    y = layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+    rt = layer.routing(T)
+    stats = layer.stats()
+    h_buf, base = rt["h_buf"], rt["base"]
+    grads = layer.backward(dy)
+    torch.cuda.synchronize()
+    assert layer.check_flags()[1] == 0
+    lg = rt["logits"].cpu().double().numpy()
+    fresh = O.topk_sorted(lg, k)
+    assert np.array_equal(rt["fresh_idx"].cpu().numpy(), fresh)
+    assert np.array_equal(rt["idx"].cpu().numpy(), cidx)
+    ort = O.route(cidx, caps, n)
+    assert np.array_equal(rt["slot_of"].cpu().numpy(), ort.slot_of)
+    hits = int((np.sort(fresh, axis=1) == np.sort(cidx, axis=1)).all(axis=1).sum())
+    assert stats["hit_count"] == hits and 0 < hits < T
+    rb = layer.routing(T)
+    dl, dw = rb["dl"].cpu().double().numpy(), rb["dw"].cpu().double().numpy()
+    w = rt["w"].cpu().double().numpy()
+    tol = TOL[cfg.dtype]
+    rng = np.random.default_rng(5)
+    stale = np.where((fresh != cidx).any(axis=1) & (ort.slot_of >= 0).all(axis=1))[0]
+    samples = _samples(ort, T, k) + sorted(int(t) for t in rng.choice(stale, 4, replace=False))
+    samples = sorted(set(samples))
+    h_rows = {(t, r): h_buf[base[int(cidx[t, r])] + int(ort.slot_of[t, r])].float().cpu().numpy()
+              for t in samples for r in range(k) if ort.slot_of[t, r] >= 0}
+    kept = [t for t in samples if (ort.slot_of[t] >= 0).all()]
+    dropped = [t for t in samples if (ort.slot_of[t] < 0).all()]
+    for grp in (kept, dropped):
+        st, gr = _group_oracle(cfg, g, grp, lg, cidx, ort.slot_of, h_rows, dy, cached=True)
+        for j, t in enumerate(grp):
+            assert rel(w[t], st.w[j]) <= 1e-5, t
+            assert rel(to_numpy64(y[t]), st.y[j]) <= tol, t
+            assert rel(dw[t], gr["dw"][j]) <= tol, t
+            assert rel(dl[t], gr["dl"][j]) <= tol, t
+            assert rel(to_numpy64(grads["dx"][t]), gr["dx"][j]) <= tol, t
