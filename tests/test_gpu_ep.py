@@ -138,7 +138,10 @@ def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0, tra
         t.join(timeout=120)
     assert not errs, errs
     ref = MoELayer(n, k, d, f, 0, Tg, dtype, renorm, device="cuda")
-    ref.set_fusion(fusion)  # the same N2 flags on both sides (the dx fusion rounds dX once)
+    # the N2 flags the ranks actually apply (the dx fusion rounds dX + dl W_g once): the peer
+    # transport fuses the dispatch backward into the owners' dX GEMMs, the NCCL-style
+    # transport does not (its dX rows travel back unfused)
+    ref.set_fusion(fusion if transport == "peer" else fusion & ~4)
     ref.set_capacities(caps)
     ref.set_balance_loss(lam)
     if cached is not None:

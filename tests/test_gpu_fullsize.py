@@ -219,3 +219,18 @@ def test_c5_full_size_cached_vs_oracle():
             assert rel(dw[t], gr["dw"][j]) <= tol, t
             assert rel(dl[t], gr["dl"][j]) <= tol, t
             assert rel(to_numpy64(grads["dx"][t]), gr["dx"][j]) <= tol, t
+
+
+@pytest.mark.timeout(600, method="thread")
+@pytest.mark.parametrize("R,transport", [(2, "peer"), (4, "peer"), (2, "nccl")])
+def test_c3_per_rank_expert_parallel_bitwise(R, transport):
+    """The bench's N > 1 configuration at its per-rank size (c3 per rank: 65,536 tokens per
+    rank, n / R experts per rank; peer transport with return rows and the fused dispatch
+    backward, or the NCCL-style transport bench.py falls back to), as R virtual ranks on one
+    GPU: routing, y, dx and each owner's expert gradients bitwise equal to the single-GPU
+    layer on the concatenated batch."""
+    from test_gpu_ep import _check_virtual, _run_virtual
+    cfg = get_config("c3")
+    out, ref = _run_virtual(R, cfg.n_experts, cfg.top_k, cfg.tokens, cfg.d_model, cfg.d_ff,
+                            cfg.dtype, cfg.renormalize, transport=transport, fusion=6)
+    _check_virtual(out, ref, R, cfg.n_experts, cfg.dtype)
