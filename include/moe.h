@@ -35,6 +35,17 @@
  *    handle, internal events/side streams.  x and the parameters must stay unchanged
  *    until moe_backward has been enqueued (the backward re-reads them).
  *  - One handle per thread; handles are not reentrant.
+ *
+ * Environment switches (read once per process; unset = the product configuration, which
+ * every test and the bench use unless they say otherwise -- the others exist for A/B timing
+ * and diagnosis, DESIGN.md lists what each measured):
+ *   MOE_PDL=0          launch without programmatic dependent launch
+ *   MOE_FORCE_SIMT=1   bf16 layers on the CUDA-core (SIMT) GEMMs instead of tcgen05
+ *   MOE_PEER_RET=0     peer transport: owners' rows read remotely instead of return rows
+ *   MOE_TC_1CTA=mask   GEMM kinds (bit per kind) on the 1-CTA instead of the 2-CTA kernel
+ *   MOE_TC_SCHED=1     contiguous tile chunk per CTA pair instead of round-robin
+ *   MOE_TC_PF=n        GEMM producer prefetches B k-blocks to L2 for the next wave
+ *   MOE_TC_DBG, MOE_GATE_DBG   timing-only experiments that SKIP work (wrong results)
  */
 #ifndef DYNAMOE_B200_MOE_H
 #define DYNAMOE_B200_MOE_H
