@@ -218,10 +218,16 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int t0 = 0; t0 < ntiles; t0 += 256) {
-    int i = t0 + threadIdx.x;
-    int v = (i < ntiles) ? hist[(size_t)i * n + e] : 0;
-    int incl = v;
+  constexpr int PER = 4;  // tiles per thread: every load of a chunk is in flight at once
+  for (int t0 = 0; t0 < ntiles; t0 += 256 * PER) {
+    const int i0 = t0 + threadIdx.x * PER;
+    int v[PER], sum = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      v[j] = (i0 + j < ntiles) ? hist[(size_t)(i0 + j) * n + e] : 0;
+      sum += v[j];
+    }
+    int incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -234,7 +240,12 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
       if (q < wid) wpre += warp_tot[q];
       tot += warp_tot[q];
     }
-    if (i < ntiles) tile_off[(size_t)i * n + e] = carry + wpre + incl - v;
+    int run = carry + wpre + incl - sum;  // exclusive prefix of this thread's first tile
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (i0 + j < ntiles) tile_off[(size_t)(i0 + j) * n + e] = run;
+      run += v[j];
+    }
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
@@ -252,11 +263,18 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
     const int lane = threadIdx.x;
     long long dr = 0;
     int carry = 0;
-    for (int q0 = 0; q0 < n; q0 += 32) {
+    int cq[MOE_MAX_E / 32];  // every expert's count requested before the first use
+#pragma unroll
+    for (int j = 0; j < MOE_MAX_E / 32; ++j)
+      cq[j] = j * 32 + lane < n ? *((volatile int32_t*)counts + j * 32 + lane) : 0;
+#pragma unroll
+    for (int j = 0; j < MOE_MAX_E / 32; ++j) {
+      const int q0 = j * 32;
+      if (q0 >= n) break;
       const int q = q0 + lane;
       int kq = 0;
       if (q < n) {
-        const int c = *((volatile int32_t*)counts + q);
+        const int c = cq[j];
         kq = min(c, ct.cap[q]);
         kept[q] = kq;
         dr += (long long)(c - kq);
