@@ -1110,21 +1110,44 @@ __global__ void __launch_bounds__(256) gate_dw_kernel(const float* __restrict__ 
   }
 }
 
+// out[i] = sum_q partial[q][i] (+ out[i]).  32 elements per block; warp g sums the splits
+// q = g, g + 8, ... with all of its loads in flight (a serial chain of `splits` dependent
+// L2 round trips was the kernel's whole cost), then warp 0 adds the 8 group sums in fixed
+// order: deterministic.
 template <typename T>
-__global__ void reduce_partials_kernel(const float* __restrict__ partial, int splits,
-                                       size_t count, T* __restrict__ out, int accumulate) {
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ partial,
+                                                              int splits, size_t count,
+                                                              T* __restrict__ out, int accumulate) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
-  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count) return;
+  __shared__ float sg[8][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const size_t i = (size_t)blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int q = 0; q < splits; ++q) s += partial[(size_t)q * count + i];
-  if (accumulate) s += to_f(out[i]);
-  out[i] = from_f<T>(s);
+  if (i < count) {
+    for (int q0 = g; q0 < splits; q0 += 64) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int q = q0 + 8 * j;
+        v[j] = q < splits ? __ldg(partial + (size_t)q * count + i) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[j];
+    }
+  }
+  sg[g][lane] = s;
+  __syncthreads();
+  if (g != 0 || i >= count) return;
+  float t = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) t += sg[q][lane];
+  if (accumulate) t += to_f(out[i]);
+  out[i] = from_f<T>(t);
 }
 
 cudaError_t launch_reduce_partials(int dtype, const float* partial, int splits, size_t count,
                                    void* out, int accumulate, cudaStream_t s) {
-  int rb = (int)((count + 255) / 256);
+  int rb = (int)((count + 31) / 32);
   if (dtype == 1)
     launch_pdl(reduce_partials_kernel<__nv_bfloat16>, rb, 256, 0, s, partial, splits, count,
                                                              (__nv_bfloat16*)out, accumulate);
