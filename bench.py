@@ -6,7 +6,8 @@ dispatch, expert FFN grouped GEMMs, combine, and every backward incl. weight gra
 one batch of synthetic tokens.  Workload: BASELINE configs[2] (c3) per GPU -- 64 experts,
 top-1, d_model 1024, d_ff 4096, 65,536 tokens per GPU, bf16, capacity factor 1.0 -- with
 experts sharded over the N ranks (weak scaling).  Inputs (x 134 MB, expert weights 1 GB)
-exceed the 126 MB L2, so no explicit flush is needed between steps.
+exceed the 126 MB L2, so no explicit flush is needed between steps; configs whose inputs
+fit the L2 (c1, c2) write 2x the L2 before every timed step and time the steps alone.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
 """
@@ -335,24 +336,42 @@ def run_ours(args):
     # ---------------- timed region (device events on the launching stream) ----------------
     # The headline runs with the library's per-kernel events OFF; a second pass of the same
     # K steps with them on gives the per-kernel table (roofline) below.
+    # L2: inputs (x, dy, weights) larger than the L2 stream through it every step; smaller
+    # ones (c1, c2) would stay resident, so every timed step then starts after a write of
+    # 2x the L2 (outside the step's events) and the time is the sum of the step intervals
+    l2_bytes = getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 << 20)
+    in_bytes = sum(int(t.numel() * t.element_size())
+                   for t in (g["x"], dy, g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"]))
+    flush_buf = (torch.empty(2 * l2_bytes, dtype=torch.uint8, device=dev)
+                 if in_bytes < 2 * l2_bytes else None)
+
+    def timed_steps(nsteps):
+        """[(start, end)] events of nsteps steps: back to back, or each after an L2 flush."""
+        evs = []
+        prev = torch.cuda.Event(enable_timing=True)
+        prev.record(stream)
+        for _ in range(nsteps):
+            if flush_buf is not None:
+                flush_buf.zero_()
+                prev = torch.cuda.Event(enable_timing=True)
+                prev.record(stream)
+            step()
+            m = torch.cuda.Event(enable_timing=True)
+            m.record(stream)
+            evs.append((prev, m))
+            prev = m
+        return evs
+
     l0 = layer.launch_count()
     clk = ClockSampler(local, dev)
     barrier()
     clk.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    marks = []  # per-step boundaries (median / p10 / p90 of the step time)
-    for _ in range(args.steps):
-        step()
-        m = torch.cuda.Event(enable_timing=True)
-        m.record(stream)
-        marks.append(m)
-    ev1.record(stream)
+    marks = timed_steps(args.steps)  # per-step intervals (median / p10 / p90, SURVEY §8(d))
     torch.cuda.synchronize(dev)
-    ms = ev0.elapsed_time(ev1)
     clocks = clk.stop()
-    per_step = sorted([ev0.elapsed_time(marks[0])] +
-                      [marks[i - 1].elapsed_time(marks[i]) for i in range(1, len(marks))])
+    per_step = sorted(a_.elapsed_time(b_) for a_, b_ in marks)
+    ms = (sum(per_step) if flush_buf is not None
+          else marks[0][0].elapsed_time(marks[-1][1]))
     q = lambda f: per_step[min(len(per_step) - 1, int(f * (len(per_step) - 1) + 0.5))]  # noqa: E731
     step_stats = {"median": round(q(0.5), 4), "p10": round(q(0.1), 4), "p90": round(q(0.9), 4)}
     barrier()
@@ -370,13 +389,9 @@ def run_ours(args):
     layer.profile(True)
     layer.profile_read(reset=True)
     barrier()
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    for _ in range(args.steps):
-        step()
-    p1.record(stream)
+    pm = timed_steps(args.steps)
     torch.cuda.synchronize(dev)
-    prof_ms_step = max_over_ranks(p0.elapsed_time(p1)) / args.steps
+    prof_ms_step = max_over_ranks(sum(a_.elapsed_time(b_) for a_, b_ in pm)) / args.steps
     barrier()
     ktimes = layer.profile_read(reset=True)
     layer.profile(False)
@@ -514,7 +529,11 @@ def run_ours(args):
                        "parallelism": (f"ep{ws} (experts sharded, tokens data-parallel, "
                                        + ("peer memory, device-initiated)" if peer else "NCCL)")
                                        if use_ep else "1 GPU"),
-                       "l2": "inputs > L2 (x 134 MB + weights 1 GB), no flush",
+                       "l2": (f"inputs {in_bytes / 1e6:.0f} MB < 2x L2: each timed step after "
+                              f"a {2 * l2_bytes / 1e6:.0f} MB write (flush), time = sum of steps"
+                              if flush_buf is not None else
+                              f"inputs {in_bytes / 1e6:.0f} MB > L2 {l2_bytes / 1e6:.0f} MB, "
+                              "no flush"),
                        "fusion": "+".join([nm for nm, on in (("gather", gather), ("combine", fcomb),
                                                              ("dx", fdx or fdx_ep),
                                                              ("return_rows", pret)) if on]) or "none",
