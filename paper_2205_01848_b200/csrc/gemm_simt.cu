@@ -22,44 +22,54 @@ __global__ void __launch_bounds__(256) gemm_simt_mgroup_kernel(
   const int Me = kept[e];
   const int m0 = blockIdx.y * SB_M, n0 = blockIdx.x * SB_N;
   if (m0 >= Me) return;
-  __shared__ float As[SB_K][SB_M + 4];
-  __shared__ float Bs[SB_K][SB_N + 4];
+  __shared__ __align__(16) float As[SB_K][SB_M + 4];
+  __shared__ __align__(16) float Bs[SB_K][SB_N + 4];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const T* Ae = A + (size_t)ct.base[e] * lda;
   const T* Be = B + (size_t)e * b_estride;
   float acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += SB_K) {
-    {  // A tile: rows m0.., cols k0.. (row-major, contiguous along k)
-      int m = tid >> 2, kq = (tid & 3) * 4;
+  // the next k-tile is loaded into registers while the current one is multiplied out of
+  // shared memory (global latency overlapped; same k order per output element)
+  float ra[4], rb[4];
+  const int am = tid >> 2, akq = (tid & 3) * 4;                           // A: row, k quad
+  const int bn = BK_MAJOR ? tid >> 2 : (tid & 15) * 4, bk = BK_MAJOR ? (tid & 3) * 4 : tid >> 4;
+  auto load = [&](int k0) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        int kk = kq + q;
-        As[kk][m] = (m0 + m < Me && k0 + kk < K) ? to_f(Ae[(size_t)(m0 + m) * lda + k0 + kk]) : 0.f;
-      }
+    for (int q = 0; q < 4; ++q) {
+      const int kk = akq + q;
+      ra[q] = (m0 + am < Me && k0 + kk < K) ? to_f(Ae[(size_t)(m0 + am) * lda + k0 + kk]) : 0.f;
     }
     if (BK_MAJOR) {  // B_e stored [N x K]
-      int nn = tid >> 2, kq = (tid & 3) * 4;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        int kk = kq + q;
-        Bs[kk][nn] = (n0 + nn < N && k0 + kk < K) ? to_f(Be[(size_t)(n0 + nn) * K + k0 + kk]) : 0.f;
+        const int kk = bk + q;
+        rb[q] = (n0 + bn < N && k0 + kk < K) ? to_f(Be[(size_t)(n0 + bn) * K + k0 + kk]) : 0.f;
       }
     } else {  // B_e stored [K x N]
-      int kk = tid >> 4, nq = (tid & 15) * 4;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        int nn = nq + q;
-        Bs[kk][nn] = (n0 + nn < N && k0 + kk < K) ? to_f(Be[(size_t)(k0 + kk) * N + n0 + nn]) : 0.f;
+        const int nn = bn + q;
+        rb[q] = (n0 + nn < N && k0 + bk < K) ? to_f(Be[(size_t)(k0 + bk) * N + n0 + nn]) : 0.f;
       }
     }
+  };
+  load(0);
+  for (int k0 = 0; k0 < K; k0 += SB_K) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      As[akq + q][am] = ra[q];
+      if (BK_MAJOR) Bs[bk + q][bn] = rb[q];
+      else Bs[bk][bn + q] = rb[q];
+    }
     __syncthreads();
+    if (k0 + SB_K < K) load(k0 + SB_K);
 #pragma unroll
     for (int kk = 0; kk < SB_K; ++kk) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+      // one 16-byte shared load per operand (row stride 68 floats keeps them aligned);
+      // same k order per output element as scalar loads: bitwise identical results
+      const float4 av = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 bv = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float a[4] = {av.x, av.y, av.z, av.w}, b[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -99,30 +109,36 @@ __global__ void __launch_bounds__(256) gemm_simt_kgroup_kernel(
   const int e = blockIdx.z;
   const int Ke = kept[e];
   const int m0 = blockIdx.y * SB_M, n0 = blockIdx.x * SB_N;
-  __shared__ float As[SB_K][SB_M + 4];
-  __shared__ float Bs[SB_K][SB_N + 4];
+  __shared__ __align__(16) float As[SB_K][SB_M + 4];
+  __shared__ __align__(16) float Bs[SB_K][SB_N + 4];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const T* Ae = Abuf + (size_t)ct.base[e] * lda;
   const T* Be = Bbuf + (size_t)ct.base[e] * ldb;
   float acc[4][4] = {};
-  for (int k0 = 0; k0 < Ke; k0 += SB_K) {
-    {
-      int kk = tid >> 4, q4 = (tid & 15) * 4;
+  float ra[4], rb[4];  // next k-tile in registers during the current tile's FMAs
+  const int lk = tid >> 4, lq = (tid & 15) * 4;
+  auto load = [&](int k0) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        int mm = q4 + q;
-        As[kk][mm] = (k0 + kk < Ke && m0 + mm < M) ? to_f(Ae[(size_t)(k0 + kk) * lda + m0 + mm]) : 0.f;
-        Bs[kk][mm] = (k0 + kk < Ke && n0 + mm < N) ? to_f(Be[(size_t)(k0 + kk) * ldb + n0 + mm]) : 0.f;
-      }
+    for (int q = 0; q < 4; ++q) {
+      const int mm = lq + q;
+      ra[q] = (k0 + lk < Ke && m0 + mm < M) ? to_f(Ae[(size_t)(k0 + lk) * lda + m0 + mm]) : 0.f;
+      rb[q] = (k0 + lk < Ke && n0 + mm < N) ? to_f(Be[(size_t)(k0 + lk) * ldb + n0 + mm]) : 0.f;
+    }
+  };
+  load(0);
+  for (int k0 = 0; k0 < Ke; k0 += SB_K) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      As[lk][lq + q] = ra[q];
+      Bs[lk][lq + q] = rb[q];
     }
     __syncthreads();
+    if (k0 + SB_K < Ke) load(k0 + SB_K);
 #pragma unroll
     for (int kk = 0; kk < SB_K; ++kk) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+      const float4 av = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 bv = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float a[4] = {av.x, av.y, av.z, av.w}, b[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
