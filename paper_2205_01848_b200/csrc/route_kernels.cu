@@ -1160,7 +1160,7 @@ cudaError_t launch_reduce_partials(int dtype, const float* partial, int splits, 
 int gate_dw_splits(int T, int d) {
   int ctiles = (d + 63) / 64;
   int want = (2 * 148 + ctiles - 1) / ctiles;
-  int maxs = (T + 255) / 256;
+  int maxs = (T + 63) / 64;  // >= 64 tokens per split: small T still fills the GPU
   return max(1, min(want, maxs));
 }
 
