@@ -336,7 +336,7 @@ __device__ __forceinline__ void zero_pads_block(T* __restrict__ buf, int cols,
   }
 }
 
-template <typename T>
+template <typename T, int RU, int KM>
 __global__ void __launch_bounds__(256) dispatch_kernel(
     const int32_t* __restrict__ idx, const T* __restrict__ x, int Tn, int k, int n, int d,
     long long token_base, CapTable ct, const int32_t* __restrict__ tile_off,
@@ -397,47 +397,57 @@ __global__ void __launch_bounds__(256) dispatch_kernel(
     }
   }
   __syncthreads();
-  // row copies: warp per token
+  // row copies: warp per token, RU tokens per warp at a time (RU > 1 for small batches,
+  // whose few blocks would otherwise wait one row latency per token); KM bounds k
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int VE = Vec<T>::N;
   const int nvec = d / VE;
-  for (int lt2 = wid; lt2 < MOE_ROUTE_TILE; lt2 += 8) {
-    const int tt = t0 + lt2;
-    if (tt >= Tn) break;
-    T* dsts[MOE_MAX_K];  // fully unrolled (registers, no local-memory array)
-    bool any = false;
+  for (int b0 = wid * RU; b0 < MOE_ROUTE_TILE; b0 += 8 * RU) {
+    if (t0 + b0 >= Tn) break;
+    T* dsts[RU][KM];  // fully unrolled (registers, no local-memory array)
+    bool cp[RU];
 #pragma unroll
-    for (int r = 0; r < MOE_MAX_K; ++r) {
-      dsts[r] = nullptr;
-      if (r < k) {
-        const int rw = srow[lt2 * k + r];
-        if (rw >= 0) {
-          any = true;
-          if (xbuf) dsts[r] = peer_row(xbuf, px, sexp[lt2 * k + r], (size_t)rw, d);
+    for (int j = 0; j < RU; ++j) {
+      const int lt2 = b0 + j, tt = t0 + lt2;
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < KM; ++r) {
+        dsts[j][r] = nullptr;
+        if (r < k && tt < Tn) {
+          const int rw = srow[lt2 * k + r];
+          if (rw >= 0) {
+            any = true;
+            if (xbuf) dsts[j][r] = peer_row(xbuf, px, sexp[lt2 * k + r], (size_t)rw, d);
+          }
         }
       }
+      if (!any && yz && tt < Tn) {  // all pairs dropped: y[t] = 0
+        for (int v = lane; v < dout / VE; v += 32)
+          st_v4(yz + (size_t)tt * dout + (size_t)v * VE, make_uint4(0, 0, 0, 0));
+      }
+      cp[j] = any && xbuf != nullptr;
     }
-    if (!any && yz) {  // all pairs dropped: y[t] = 0
-      for (int v = lane; v < dout / VE; v += 32)
-        st_v4(yz + (size_t)tt * dout + (size_t)v * VE, make_uint4(0, 0, 0, 0));
-    }
-    if (!any || !xbuf) continue;
-    const T* src = x + (size_t)tt * d;
     for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
-      uint4 buf[4];
+      uint4 buf[RU][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int v = v0 + u * 32 + lane;
-        if (v < nvec) buf[u] = ld_nc_v4(src + (size_t)v * VE);
+      for (int j = 0; j < RU; ++j) {
+        const T* src = x + (size_t)(t0 + b0 + j) * d;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int v = v0 + u * 32 + lane;
+          if (cp[j] && v < nvec) buf[j][u] = ld_nc_v4(src + (size_t)v * VE);
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int v = v0 + u * 32 + lane;
-        if (v < nvec)
+      for (int j = 0; j < RU; ++j)
 #pragma unroll
-          for (int q = 0; q < MOE_MAX_K; ++q)
-            if (dsts[q]) st_v4(dsts[q] + (size_t)v * VE, buf[u]);
-      }
+        for (int u = 0; u < 4; ++u) {
+          int v = v0 + u * 32 + lane;
+          if (cp[j] && v < nvec)
+#pragma unroll
+            for (int q = 0; q < KM; ++q)
+              if (dsts[j][q]) st_v4(dsts[j][q] + (size_t)v * VE, buf[j][u]);
+        }
     }
   }
   // (no fence here: the exchange barrier kernel that follows on this stream releases, at
@@ -451,17 +461,18 @@ cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T,
                             const int32_t* pre_dev, void* y_zero, int dout) {
   if (T == 0 && !(pad_kept && px.nl)) return cudaSuccess;  // peer EP: own pads still zeroed
   int ntiles = std::max(1, (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE);
-  if (dtype == 1)
-    launch_pdl(dispatch_kernel<__nv_bfloat16>, ntiles, 256, 0, s, 
-        idx, (const __nv_bfloat16*)x, T, k, n, d, token_base, ct, b.tile_off, b.slot_of,
-        b.token_of_slot, (__nv_bfloat16*)xbuf, pad_kept, pad_e0, px, ptos, pre_dev,
-        (__nv_bfloat16*)y_zero, dout);
-  else
-    launch_pdl(dispatch_kernel<float>, ntiles, 256, 0, s, idx, (const float*)x, T, k, n, d,
-                                                  token_base, ct, b.tile_off, b.slot_of,
-                                                  b.token_of_slot, (float*)xbuf, pad_kept,
-                                                  pad_e0, px, ptos, pre_dev, (float*)y_zero,
-                                                  dout);
+  // top-1 with fewer routing tiles than two per SM: four tokens per warp in flight
+  const bool small = k == 1 && ntiles < 2 * 148;  // B200: 148 SMs
+#define DISP(TT, RU_, KM_)                                                                   \
+  launch_pdl(dispatch_kernel<TT, RU_, KM_>, ntiles, 256, 0, s, idx, (const TT*)x, T, k, n, d, \
+             token_base, ct, b.tile_off, b.slot_of, b.token_of_slot, (TT*)xbuf, pad_kept,    \
+             pad_e0, px, ptos, pre_dev, (TT*)y_zero, dout)
+  if (dtype == 1) {
+    if (small) DISP(__nv_bfloat16, 4, 1); else DISP(__nv_bfloat16, 1, MOE_MAX_K);
+  } else {
+    if (small) DISP(float, 4, 1); else DISP(float, 1, MOE_MAX_K);
+  }
+#undef DISP
   return cudaGetLastError();
 }
 
