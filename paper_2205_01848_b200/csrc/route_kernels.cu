@@ -38,17 +38,36 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(
 #pragma unroll
   for (int j = 0; j < NJ; ++j) acc[j] = 0.f;
 
-  for (int k0 = 0; k0 < d; k0 += GATE_DK) {
-    for (int i = tid; i < GATE_TOK * GATE_DK; i += 256) {
-      int r = i / GATE_DK, c = i % GATE_DK;
-      int t = t0 + r;
-      xs[r * (GATE_DK + 1) + c] = (t < Tn) ? to_f(x[(size_t)t * d + k0 + c]) : 0.f;
+  // the next d-slice of x and W_g is loaded into registers while the current one is
+  // multiplied out of shared memory (same c order per logit: bitwise identical results)
+  static_assert(GATE_TOK * GATE_DK == 4 * 256, "x slice = 4 elements per thread");
+  float rx[4], rw[NJ];  // n * GATE_DK <= 8 NJ * 32 = NJ * 256 elements of W_g
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = tid + 256 * q, r = i / GATE_DK, c = i % GATE_DK, t = t0 + r;
+      rx[q] = (t < Tn) ? to_f(x[(size_t)t * d + k0 + c]) : 0.f;
     }
-    for (int i = tid; i < n * GATE_DK; i += 256) {
-      int r = i / GATE_DK, c = i % GATE_DK;
-      ws[r * (GATE_DK + 1) + c] = to_f(wg[(size_t)r * d + k0 + c]);
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) {
+      const int i = tid + 256 * q;
+      if (i < n * GATE_DK) rw[q] = to_f(wg[(size_t)(i / GATE_DK) * d + k0 + i % GATE_DK]);
+    }
+  };
+  load(0);
+  for (int k0 = 0; k0 < d; k0 += GATE_DK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = tid + 256 * q;
+      xs[(i / GATE_DK) * (GATE_DK + 1) + i % GATE_DK] = rx[q];
+    }
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) {
+      const int i = tid + 256 * q;
+      if (i < n * GATE_DK) ws[(i / GATE_DK) * (GATE_DK + 1) + i % GATE_DK] = rw[q];
     }
     __syncthreads();
+    if (k0 + GATE_DK < d) load(k0 + GATE_DK);
 #pragma unroll 4
     for (int c = 0; c < GATE_DK; ++c) {
       float xv = xs[tok * (GATE_DK + 1) + c];
