@@ -1266,7 +1266,15 @@ __global__ void colsum_kernel(const T* __restrict__ buf, int cols,
   const int m = kept[e];
   const T* p = buf + (size_t)ct.base[e] * cols + j;
   float s = 0.f;
-  for (int r = 0; r < m; ++r) s += to_f(p[(size_t)r * cols]);
+  int r = 0;
+  for (; r + 8 <= m; r += 8) {  // eight row loads in flight, added in row order
+    float q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = to_f(p[(size_t)(r + i) * cols]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += q[i];
+  }
+  for (; r < m; ++r) s += to_f(p[(size_t)r * cols]);
   if (accumulate) s += to_f(out[(size_t)e * cols + j]);
   out[(size_t)e * cols + j] = from_f<T>(s);
 }
