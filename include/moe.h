@@ -131,7 +131,10 @@ MOE_API moe_status_t moe_capacity_from_factors(int32_t n, int64_t tokens_global,
    after this call (the new table travels as kernel arguments: stream-ordered, no sync).
    Returns MOE_ERR_WORKSPACE_TOO_SMALL when the set workspace is too small for the new
    layout; the capacities ARE recorded, so the caller queries moe_workspace_size,
-   allocates and calls moe_set_workspace.  Weights are never touched. */
+   allocates and calls moe_set_workspace.  With the peer transport, capacities whose
+   local expert rows exceed the library-owned peer window (cfg.window_rows) are refused
+   with MOE_ERR_CONFIG and NOT recorded (the previous capacities stay in force).
+   Weights are never touched. */
 MOE_API moe_status_t moe_set_capacities(moe_handle_t h, const int32_t* cap);
 MOE_API moe_status_t moe_get_capacities(moe_handle_t h, int32_t* cap_out /* host [n] */);
 
@@ -186,7 +189,9 @@ MOE_API moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a);
 
 /* Backward of sum(dy * y) for the last forward (which it consumes: H is overwritten by dA).
    Gradients overwrite their outputs (accumulate = 0) or add to them (accumulate = 1).
-   Any gradient pointer may be NULL to skip writing it, except that the routing / expert
+   Expert parallelism: dw1 / db1 / dw2 / db2 are the full [n, ...] tensors; this rank writes
+   its own experts' slices, and with accumulate = 0 the other experts' slices are zeroed
+   (stream-ordered memsets), so the whole tensor is defined.  Any gradient pointer may be NULL to skip writing it, except that the routing / expert
    chain is always computed.  All pointers device, layer dtype. */
 typedef struct {
   const void* dy;

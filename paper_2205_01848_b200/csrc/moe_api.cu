@@ -405,8 +405,8 @@ moe_status_t moe_set_capacities(moe_handle_t h, const int32_t* cap) {
   std::vector<int32_t> nc(h->n);
   for (int e = 0; e < h->n; ++e) nc[e] = (int32_t)std::min<int64_t>(cap[e], tg);
   if (h->use_peer && max_owner_rows(h, nc) > h->PL.rows)
-    return fail(h, MOE_ERR_WORKSPACE_TOO_SMALL, "peer window too small for these capacities "
-                                                "(raise cfg.window_rows)");
+    return fail(h, MOE_ERR_CONFIG, "peer window too small for these capacities "
+                                   "(raise cfg.window_rows); capacities unchanged");
   h->cap = nc;
   relayout(h);
   h->have_fwd = 0;  // saved activations no longer match the layout
@@ -768,6 +768,18 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   char* db1 = a->db1 ? (char*)a->db1 + (size_t)h->e_lo * f * h->s : nullptr;
   char* dw2 = a->dw2 ? (char*)a->dw2 + (size_t)h->e_lo * dout * f * h->s : nullptr;
   char* db2 = a->db2 ? (char*)a->db2 + (size_t)h->e_lo * dout * h->s : nullptr;
+  if (h->R > 1 && !acc) {  // EP: the other ranks' expert slices of the full tensors read zero
+    const size_t per[4] = {(size_t)f * d * h->s, (size_t)f * h->s, (size_t)dout * f * h->s,
+                           (size_t)dout * h->s};
+    void* full[4] = {a->dw1, a->db1, a->dw2, a->db2};
+    for (int q = 0; q < 4; ++q) {
+      if (!full[q]) continue;
+      char* base = (char*)full[q];
+      if (h->e_lo > 0) CUDA_TRY(h, cudaMemsetAsync(base, 0, per[q] * h->e_lo, s0));
+      const size_t hi = (size_t)(h->e_lo + nl);
+      if (hi < (size_t)n) CUDA_TRY(h, cudaMemsetAsync(base + per[q] * hi, 0, per[q] * (n - hi), s0));
+    }
+  }
   if (h->use_tc) {
     int64_t nk = 0;
     TcFusion fz;  // N2: dW1 = dA^T X gathers the x rows like the forward did

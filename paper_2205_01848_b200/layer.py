@@ -62,6 +62,11 @@ class MoELayer:
             L.check(self.lib.moe_init(C.byref(cfg), C.byref(h)), None, "moe_init")
         self.h = h
         self.layout_generation = 0   # bumped by every recompile (capacity change)
+        # bumped by every call that changes arguments a captured CUDA graph has baked in
+        # (capacities, cached indices, assignment cache, fusion, loss variants)
+        self.generation = 0
+        self._saved = None
+        self._fwd_id = 0             # forward counter: a backward must follow its own forward
         self.ws = None
         self._cached_ref = None
         self._alloc_workspace()
@@ -127,13 +132,17 @@ class MoELayer:
     def set_capacities(self, caps):
         """Dynamic capacity factors (S4.1): new per-expert capacities, stream-ordered."""
         arr = (C.c_int32 * self.n)(*[int(c) for c in caps])
-        self.layout_generation += 1
         st = self.lib.moe_set_capacities(self.h, arr)
-        if st == L.MOE_ERR_WORKSPACE_TOO_SMALL:
+        if st == L.MOE_ERR_WORKSPACE_TOO_SMALL:   # recorded; the layout needs a bigger block
             self._alloc_workspace()
-            return
-        L.check(st, self.h, "moe_set_capacities")
-        self._sync_stream()
+        else:
+            L.check(st, self.h, "moe_set_capacities")
+            self._sync_stream()
+        want = [min(int(c), max(1, self.max_tokens * self.world_size)) for c in caps]
+        if self.capacities != want:
+            raise RuntimeError(f"moe_set_capacities did not take effect: {self.capacities}")
+        self.layout_generation += 1
+        self.generation += 1
 
     def set_capacity_factors(self, alphas, tokens_global=None):
         tg = tokens_global if tokens_global is not None else self.max_tokens * self.world_size
@@ -144,8 +153,9 @@ class MoELayer:
         if idx is not None:
             if idx.dtype != torch.int32 or not idx.is_cuda or not idx.is_contiguous():
                 raise ValueError("cached indices must be a contiguous int32 CUDA tensor")
-        self._cached_ref = idx
         L.check(self.lib.moe_set_cached_assignment(self.h, _ptr(idx)), self.h)
+        self._cached_ref = idx
+        self.generation += 1
 
     def set_assignment_cache(self, table, sample_ids, mode: int):
         """Per-sample assignment cache (N4): table int32 [num_samples, k] (device, -1 =
@@ -162,6 +172,7 @@ class MoELayer:
         else:
             self._ctab_ref = None
             L.check(self.lib.moe_set_assignment_cache(self.h, None, 0, None, 0), self.h)
+        self.generation += 1
 
     # -- N2 fusions ---------------------------------------------------------------------
     FUSE_GATHER, FUSE_COMBINE, FUSE_DX = 1, 2, 4
@@ -171,12 +182,14 @@ class MoELayer:
         buffer), FUSE_COMBINE (k = 1: y written by the second GEMM's epilogue) and FUSE_DX
         (k = 1: dx = dX + dl W_g written by the dX GEMM).  Default COMBINE | DX."""
         L.check(self.lib.moe_set_fusion(self.h, int(flags)), self.h)
+        self.generation += 1
 
     # -- loss variants (N3) -----------------------------------------------------------
     def set_balance_loss(self, lam: float):
         """Eq. 3 balance term weight (0 = off); the backward then includes dB/dl."""
         L.check(self.lib.moe_set_balance_loss(self.h, float(lam)), self.h)
         self._lam = float(lam)
+        self.generation += 1
 
     def aux_loss(self) -> float:
         """B of the last forward (synchronises)."""
@@ -198,12 +211,14 @@ class MoELayer:
         else:
             self.spec = self.spec_valid = None
             L.check(self.lib.moe_set_spec_outputs(self.h, None, None), self.h)
+        self.generation += 1
 
     def set_spec_grads(self, dspec=None, dw_ext=None):
         """Gradients w.r.t. the spec rows ([T*k, d_out], layer dtype) and the gate weights
         ([T, k] fp32) consumed by the following backwards (None = none)."""
         self._spec_grads = (dspec, dw_ext)
         L.check(self.lib.moe_set_spec_grads(self.h, _ptr(dspec), _ptr(dw_ext)), self.h)
+        self.generation += 1
 
     # -- hot path -------------------------------------------------------------------
     def _check(self, t, shape, name):
@@ -227,14 +242,24 @@ class MoELayer:
         a = L.FwdArgs(T, _ptr(x), _ptr(w_gate), _ptr(w1), _ptr(b1), _ptr(w2), _ptr(b2), _ptr(y))
         L.check(self.lib.moe_forward(self.h, C.byref(a)), self.h, "moe_forward")
         self._saved = (x, w_gate, w1, b1, w2, b2)   # keep alive until backward (moe.h)
+        self._fwd_id += 1
         return y
 
     def backward(self, dy, grads=None, accumulate=False, need=("dx", "dw_gate", "dw1", "db1",
-                                                               "dw2", "db2")):
+                                                               "dw2", "db2"), fwd_id=None):
+        """Gradients of the LAST forward (the library keeps one saved forward).  fwd_id: the
+        value of `self._fwd_id` right after the forward these gradients belong to; a
+        mismatch (another forward ran in between) raises instead of mixing batches."""
+        if fwd_id is not None and fwd_id != self._fwd_id:
+            raise RuntimeError("MoELayer.backward: another forward ran since the forward this "
+                               "backward belongs to (the layer saves only the last one)")
+        if self._saved is None:
+            raise RuntimeError("MoELayer.backward: no saved forward (backward called twice?)")
         x, w_gate, w1, b1, w2, b2 = self._saved
         T = x.shape[0]
         self._check(dy, (T, self.d_out), "dy")
         if grads is None:
+            # (EP: the library zeroes the other ranks' expert slices itself, moe.h)
             alloc = torch.zeros if accumulate else torch.empty
             shapes = dict(dx=x.shape, dw_gate=w_gate.shape, dw1=w1.shape, db1=b1.shape,
                           dw2=w2.shape, db2=b2.shape)
@@ -365,11 +390,13 @@ class MoEFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, layer, x, w_gate, w1, b1, w2, b2):
         ctx.layer = layer
-        return layer.forward(x, w_gate, w1, b1, w2, b2)
+        y = layer.forward(x, w_gate, w1, b1, w2, b2)
+        ctx.fwd_id = layer._fwd_id
+        return y
 
     @staticmethod
     def backward(ctx, dy):
-        g = ctx.layer.backward(dy.contiguous())
+        g = ctx.layer.backward(dy.contiguous(), fwd_id=ctx.fwd_id)
         return None, g["dx"], g["dw_gate"], g["dw1"], g["db1"], g["dw2"], g["db2"]
 
 

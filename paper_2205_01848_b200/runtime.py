@@ -147,8 +147,11 @@ def capacity_trigger(policy):
 class GraphedStep:
     """forward + backward of a layer captured into one CUDA graph over static tensors.
 
-    A recompile (capacities changed) invalidates the captured kernel arguments; call
-    `recapture()` (done automatically when `layer.layout_generation` changed)."""
+    A recompile (capacities changed), like any other setter that changes kernel arguments
+    (cached indices, assignment cache, fusion flags, loss variants), invalidates the captured
+    arguments; `replay()` re-captures when `layer.generation` changed.  The tensors the
+    captured arguments point at (cached indices, cache table, spec gradients) are kept
+    alive by the capture itself, so a replay never reads memory Python has released."""
 
     def __init__(self, layer, x, params, dy, grads, y=None):
         self.layer = layer
@@ -175,10 +178,13 @@ class GraphedStep:
         with torch.cuda.graph(g):
             self._body()
         self.graph = g
-        self.gen = self.layer.layout_generation
+        self.gen = self.layer.generation
+        L = self.layer
+        self._pinned_args = (getattr(L, "_cached_ref", None), getattr(L, "_ctab_ref", None),
+                             getattr(L, "_spec_grads", None), getattr(L, "spec", None))
 
     def replay(self):
-        if self.gen != self.layer.layout_generation:
+        if self.gen != self.layer.generation:
             self.recapture()
         self.graph.replay()
         return self.y

@@ -5,7 +5,7 @@ import pytest
 import torch
 
 from oracle import moe_oracle as O
-from parity_util import TOL, _np, rel
+from parity_util import TOL, _np, checked_relu_mask, kernel_relu_mask, rel
 from synth import make_dy, make_layer, to_numpy64
 
 pytestmark = pytest.mark.gpu
@@ -39,8 +39,7 @@ def test_balance_and_spec_parity(dtype, n, k, renorm, d):
     p64 = {kk: to_numpy64(v) for kk, v in cpu.items() if kk != "x"}
     st = O.moe_forward(to_numpy64(cpu["x"]), p64, k, caps, renorm, logits=_np(rt["logits"]).astype(np.float64),
                        emulate_bf16=(dtype == "bf16"), balance_lambda=lam)
-    mask = [_np(rt["h_buf"][rt["base"][e]: rt["base"][e] + int(st.routing.kept[e])]) > 0
-            for e in range(n)]   # ReLU' decisions in the kernel's precision
+    mask = checked_relu_mask(st, kernel_relu_mask(rt, st), "losses")
     gr = O.moe_backward(st, to_numpy64(dy), dspec=to_numpy64(dspec), dw_ext=dw_ext.double().numpy(),
                         relu_mask=mask)
     tol = TOL[dtype]

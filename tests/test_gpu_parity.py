@@ -11,7 +11,8 @@ import torch
 from oracle import moe_oracle as O
 from synth import perturb_cached
 
-from parity_util import assert_routing_exact, assert_values, rel, run_pair
+from parity_util import (assert_routing_exact, assert_values, checked_relu_mask, kernel_relu_mask,
+                         rel, run_pair)
 
 pytestmark = pytest.mark.gpu
 
@@ -257,8 +258,7 @@ def test_confident_router_dl_precision(k, renorm):
     p64 = {kk: to_numpy64(v) for kk, v in cpu.items() if kk != "x"}
     st = O.moe_forward(to_numpy64(cpu["x"]), p64, k, caps, renorm,
                        logits=rt["logits"].cpu().double().numpy())
-    mask = [rt["h_buf"][rt["base"][e]: rt["base"][e] + int(st.routing.kept[e])].cpu().numpy() > 0
-            for e in range(n)]
+    mask = checked_relu_mask(st, kernel_relu_mask(rt, st), "confident router")
     gr = O.moe_backward(st, to_numpy64(dy), relu_mask=mask)
     assert float(np.max(st.p)) > 0.999999   # the regime this test is about
     dl = layer.routing(T)["dl"].cpu().double().numpy()

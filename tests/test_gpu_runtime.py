@@ -87,3 +87,49 @@ def test_graphed_step_matches_eager_and_recaptures(d, f):
     layer.backward(dy)
     torch.cuda.synchronize()
     assert torch.equal(y2, y2_e) and not torch.equal(y2, y_e)
+
+
+def test_graphed_step_recaptures_on_cached_assignment_and_fusion():
+    """Setters other than capacities (cached indices, fusion flags) also change captured
+    kernel arguments: the replay re-captures and matches eager; the captured cached-index
+    tensor stays alive after the caller drops it."""
+    import numpy as np
+    from paper_2205_01848_b200 import GraphedStep
+    from synth import perturb_cached
+    n, k, T = 16, 1, 1024
+    layer, g, dy = _setup(n, k, T, dtype="bf16", regime="uniform", d=128, f=256)
+    layer.set_capacity_factors([1.25] * n)
+    grads = {kk: torch.empty_like(v) for kk, v in
+             dict(dx=g["x"], dw_gate=g["w_gate"], dw1=g["w1"], db1=g["b1"], dw2=g["w2"],
+                  db2=g["b2"]).items()}
+    gs = GraphedStep(layer, g["x"], g, dy, grads)
+    y0 = gs.replay().clone()
+    fresh = layer.routing(T)["fresh_idx"].cpu().numpy()
+    cidx = torch.from_numpy(np.ascontiguousarray(perturb_cached(fresh, n, 0.5),
+                                                 dtype=np.int32)).cuda()
+    layer.set_cached_assignment(cidx)
+    del cidx                                  # the graph's capture keeps it alive
+    y1 = gs.replay().clone()
+    y1_e = layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"]).clone()
+    layer.backward(dy)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y1_e) and not torch.equal(y1, y0)
+    layer.set_cached_assignment(None)
+    layer.set_fusion(0)
+    y2 = gs.replay().clone()
+    torch.cuda.synchronize()
+    assert torch.equal(y2, y0)                # combine fusion is bitwise equal to unfused
+
+
+def test_backward_of_a_stale_forward_raises():
+    """One saved forward per layer: a backward after another forward (e.g. an eval pass)
+    must not silently use the wrong batch (autograd path)."""
+    from paper_2205_01848_b200 import DynaMoE
+    torch.manual_seed(0)
+    m = DynaMoE(8, 2, 64, 128, 0, 256, "f32", device="cuda")
+    x = torch.randn(256, 64, device="cuda", requires_grad=True)
+    y = m(x)
+    with torch.no_grad():
+        m(torch.randn(256, 64, device="cuda"))
+    with pytest.raises(RuntimeError, match="another forward"):
+        y.sum().backward()
