@@ -51,6 +51,10 @@ def parse():
                     help="dynamic: the capacity policy (moe_policy_*) adapts C_e for "
                          "--policy-warmup steps before the timed region (P:221-236)")
     ap.add_argument("--policy-warmup", type=int, default=50)
+    ap.add_argument("--emulate-padded", action="store_true",
+                    help="TIMING ONLY: expert GEMMs over all C_e rows (MOE_DBG_PAD_GEMM=1), "
+                         "what a capacity-padded implementation (the paper's FlexFlow "
+                         "operators, P:234, P:370) spends; outputs are not valid")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=8192)
@@ -67,6 +71,8 @@ def parse():
                          "epilogue; dx = dispatch backward inside the dX GEMM; default = both; "
                          "all = also gather x rows in the expert GEMMs (TMA gather4)")
     a = ap.parse_args()
+    if a.emulate_padded:
+        os.environ["MOE_DBG_PAD_GEMM"] = "1"
     if a.config is None:
         a.config = "c3" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "c4"
     return a
@@ -300,7 +306,7 @@ def run_ours(args):
     fflags = {"none": 0, "combine": 2, "dx": 4, "default": 6, "all": 7}[args.fusion]
     tc1 = not use_ep and cfg.dtype == "bf16" and getattr(layer, "uses_tcgen05", False)
     gather = tc1 and bool(fflags & 1) and d % 128 == 0 and f % 128 == 0
-    fcomb = tc1 and bool(fflags & 2) and k == 1 and do % 128 == 0 and not args.cached
+    fcomb = tc1 and bool(fflags & 2) and k == 1 and do % 128 == 0
     fdx = tc1 and bool(fflags & 4) and k == 1 and d % 128 == 0
     # peer EP (N1): return rows from the GEMM epilogues, and the dispatch backward in the
     # owners' dX GEMMs (k = 1)
@@ -342,7 +348,8 @@ def run_ours(args):
             if new is not None:
                 layer.set_capacities(new)
                 recompiles += 1
-
+        torch.cuda.synchronize(dev)
+        time.sleep(2.0)  # the warm-up steps heat the GPU: time from the same rested state
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
         step()
@@ -573,7 +580,8 @@ def run_ours(args):
         owner = torch.div(rt_["idx"].long(), nl_, rounding_mode="floor")
         off = int(((rt_["slot_of"] >= 0) & (owner != rank)).sum().item())
         bar = ktimes.get("peer_barrier", (0, 0.0))
-        exchange = {"transport": "peer memory (CUDA IPC windows, device-initiated stores)"
+        via = getattr(layer, "peer_via", "in-process windows")
+        exchange = {"transport": f"peer memory ({via}, device-initiated loads/stores)"
                                  if peer else "NCCL grouped send/recv",
                     "off_rank_rows_per_exchange": off,
                     "nvlink_bytes_per_exchange": off * d * s,
@@ -595,7 +603,9 @@ def run_ours(args):
                                    + (f"dynamic capacity (policy, {args.policy_warmup} steps)"
                                       if policy is not None else f"alpha {alpha}")
                                    + (f", {args.regime} routing" if args.regime != "uniform" else "")
-                                   + (", cached assignments" if args.cached else ""),
+                                   + (", cached assignments" if args.cached else "")
+                                   + (", EMULATED capacity-padded GEMMs (timing only)"
+                                      if args.emulate_padded else ""),
                        "tokens_per_gpu": T, "n_experts": n, "top_k": k, "d_model": d, "d_ff": f,
                        "capacity_factor": alpha if policy is None else "dynamic",
                        "regime": args.regime, "recompiles": recompiles,
@@ -631,6 +641,7 @@ def run_ours(args):
             "clocks": clocks,
         }
         print(json.dumps(out), flush=True)
+    layer.close()   # an NCCL symmetric window is deregistered while the communicator lives
     if dist is not None:
         dist.destroy_process_group()
 

@@ -344,6 +344,18 @@ MOE_API moe_status_t moe_peer_window(moe_handle_t h, void** window, size_t* byte
 MOE_API moe_status_t moe_peer_export(moe_handle_t h, void* ipc_handle /* host, 64 bytes */);
 MOE_API moe_status_t moe_peer_attach(moe_handle_t h, void* const* windows /* host [R] */);
 MOE_API moe_status_t moe_peer_import(moe_handle_t h, const void* handles /* host [R][64] */);
+/* The same attachment on an NCCL communicator instead of IPC handles (NCCL >= 2.28
+   symmetric memory; collective: every rank of the group calls it, in the same order as
+   its other collectives on that communicator).  The window is re-allocated with
+   ncclMemAlloc, zeroed, registered with ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC),
+   and every rank's mapping is taken from the NCCL device API (ncclGetPeerPointer) of the
+   load/store-accessible (LSA, NVLink) team.  nccl_comm: the ncclComm_t of the expert-
+   parallel group (size world_size, this rank = cfg.rank), e.g. torch's ProcessGroupNCCL
+   communicator; it must outlive the handle (moe_destroy deregisters the window on it).
+   Errors: MOE_ERR_NCCL if the library lacks the API or not every rank is in the LSA team
+   (the handle then keeps its own window: fall back to moe_peer_import), MOE_ERR_STATE if
+   already attached, MOE_ERR_INVALID_ARG if the communicator's size / rank differ. */
+MOE_API moe_status_t moe_peer_connect_nccl(moe_handle_t h, void* nccl_comm);
 
 /* N2 fusions of the single-GPU tcgen05 path, a bitmask of moe_fusion_t;
    default MOE_FUSE_COMBINE | MOE_FUSE_DX (GATHER is opt-in: on B200 the TMA gather4 stream
@@ -355,10 +367,12 @@ MOE_API moe_status_t moe_peer_import(moe_handle_t h, const void* handles /* host
      no X buffer is materialised.  Applies when world_size == 1 (no EP), dtype bf16, d and f
      multiples of 128 and x 16-byte aligned; else the X buffer path runs.  x must stay
      unchanged until moe_backward has been enqueued (already required above).
-   MOE_FUSE_COMBINE (k == 1, world_size == 1, bf16, no cached indices, no AggregateSpec
-     outputs, d_out a multiple of 128): the second expert GEMM's epilogue writes y[t] = w[t] O[row]
+   MOE_FUSE_COMBINE (k == 1, world_size == 1, bf16, no AggregateSpec outputs, d_out a
+     multiple of 128): the second expert GEMM's epilogue writes y[t] = w[t] O[row]
      (Alg. 1 l.8) next to O and the dispatch zeroes the y rows of dropped tokens, so no
-     separate combine pass re-reads O.  Takes effect at the next moe_forward.
+     separate combine pass re-reads O.  With cached indices the gate runs concurrently with
+     the routing / dispatch / first GEMM and the second GEMM waits for it (its weights).
+     Takes effect at the next moe_forward.
    MOE_FUSE_DX (k == 1, world_size == 1, bf16, d a multiple of 128, dx requested): the
      dispatch backward (dx[t] = dX[row] + dl[t] W_g) runs inside the dX = dA W1 GEMM --
      extra k-blocks accumulate [hi|lo](dl) [W_g; W_g] into the same fp32 accumulator and the

@@ -117,6 +117,7 @@ EXPORTS = {
     "moe_peer_export": ([C.c_void_p, C.c_void_p], C.c_int),
     "moe_peer_attach": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
     "moe_peer_import": ([C.c_void_p, C.c_void_p], C.c_int),
+    "moe_peer_connect_nccl": ([C.c_void_p, C.c_void_p], C.c_int),
 }
 
 _lib = None

@@ -23,6 +23,21 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 
+def nccl_include():
+    """Headers of the NCCL torch loads (nccl.h + the NCCL >= 2.28 device API, nccl_device.h):
+    the nvidia-nccl wheel in this environment; only the peer-window path (nccl_lsa.cu) uses
+    them, and the library itself is resolved at run time (dlopen)."""
+    try:
+        import nvidia
+        for base in nvidia.__path__:
+            inc = os.path.join(base, "nccl", "include")
+            if os.path.exists(os.path.join(inc, "nccl_device.h")):
+                return inc
+    except ImportError:
+        pass
+    raise RuntimeError("nccl_device.h (NCCL >= 2.28 headers, nvidia-nccl wheel) not found")
+
+
 def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
@@ -47,6 +62,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if force or _needs(obj, [src] + headers):
             cmd = [NVCC, *ARCH, *FLAGS, *os.environ.get("MOE_NVCC_EXTRA", "").split(), "-c", src,
                    "-o", obj]
+            if os.path.basename(src) == "nccl_lsa.cu":
+                cmd[1:1] = ["-I", nccl_include()]
             if os.environ.get("MOE_PTXAS_V"):
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)

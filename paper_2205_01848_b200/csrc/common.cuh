@@ -104,6 +104,26 @@ __device__ __forceinline__ void st_v4(void* p, const uint4& v) {
   *reinterpret_cast<uint4*>(p) = v;
 }
 
+// Zero rows [kept_e, roundup(kept_e, MOE_PAD_ROWS)) of expert regions e = first, first +
+// stride, ... (local region j starts at row ct.base[e0 + j]) with all threads of the calling
+// block: the token-contraction (weight-gradient) GEMMs read whole 64-row K-blocks.
+template <typename T>
+__device__ __forceinline__ void zero_pads_block(T* __restrict__ buf, int cols,
+                                                const int32_t* __restrict__ kept,
+                                                const CapTable& ct, int nreg, int e0, int first,
+                                                int stride) {
+  constexpr int VE = Vec<T>::N;
+  const int nvec = cols / VE;
+  for (int j = first; j < nreg; j += stride) {
+    const int kp = kept[j];
+    const int r0 = ct.base[e0 + j] + kp;
+    const int r1 = ct.base[e0 + j] + ((kp + MOE_PAD_ROWS - 1) / MOE_PAD_ROWS) * MOE_PAD_ROWS;
+    const size_t total = (size_t)max(r1 - r0, 0) * nvec;
+    for (size_t i = threadIdx.x; i < total; i += blockDim.x)
+      st_v4(buf + (size_t)r0 * cols + i * VE, make_uint4(0, 0, 0, 0));
+  }
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

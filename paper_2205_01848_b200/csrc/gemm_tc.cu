@@ -607,10 +607,15 @@ moe_status_t tc_ffn_forward(TcPlan* plan, void* X, const void* w1, const void* b
                             int d, int f, int dout, const int32_t* kept,
                             const int32_t* mtile_prefix, int n_local, const CapTable& ct,
                             int max_cap, cudaStream_t s, int64_t* nlaunch, Prof* prof,
-                            uint32_t* mask, const TcFusion* fz) {
+                            uint32_t* mask, const TcFusion* fz,
+                            cudaError_t (*between)(void*), void* between_ctx) {
   (void)plan; (void)max_cap;
   if (!ensure_encode()) return MOE_ERR_CUDA;
-  if (rows == 0 || n_local == 0) { *nlaunch = 0; return MOE_OK; }
+  if (rows == 0 || n_local == 0) {
+    *nlaunch = 0;
+    if (between && between(between_ctx) != cudaSuccess) return MOE_ERR_CUDA;
+    return MOE_OK;
+  }
   moe_status_t st;
   {
     ProfScope ps(prof, "ffn_gemm1", s);
@@ -618,6 +623,7 @@ moe_status_t tc_ffn_forward(TcPlan* plan, void* X, const void* w1, const void* b
                          nullptr, fz);
   }
   if (st != MOE_OK) return st;
+  if (between && between(between_ctx) != cudaSuccess) return MOE_ERR_CUDA;
   {
     ProfScope ps(prof, "ffn_gemm2", s);
     st = mgroup<TC_FWD2>(H, rows, f, w2, dout, n_local, b2, O, dout, kept, mtile_prefix, ct, s,

@@ -48,7 +48,10 @@ moe_status_t tc_ffn_forward(TcPlan* p, void* X, const void* w1, const void* b1,
                             int d, int f, int dout, const int32_t* kept,
                             const int32_t* mtile_prefix, int n_local, const CapTable& ct,
                             int max_cap, cudaStream_t s, int64_t* nlaunch, Prof* prof,
-                            uint32_t* mask, const TcFusion* fz = nullptr);
+                            uint32_t* mask, const TcFusion* fz = nullptr,
+                            cudaError_t (*between)(void*) = nullptr, void* between_ctx = nullptr);
+// (between: enqueued after the FWD1 launch and before FWD2, e.g. the cached-mode join with the
+//  gate stream so FWD2's fused combine sees the gate weights)
 // Backward: dW2 = dO^T H, db2 = sum dO; dA = (dO W2) * 1[H>0] (into H);
 // dW1 = dA^T X, db1 = sum dA; dX = dA W1.
 moe_status_t tc_ffn_backward(TcPlan* p, void* X, void* H, void* dO, void* dX, const void* w1,

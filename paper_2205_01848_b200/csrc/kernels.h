@@ -78,6 +78,11 @@ cudaError_t launch_zero_pad(int dtype, void* buf, int cols, const int32_t* kept,
 cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, int k,
                                int d_out, const CapTable& ct, void* y, cudaStream_t s,
                                const PeerBufs& po = PeerBufs{});
+cudaError_t launch_combine_bwd_bulk(const void* dy, const void* obuf, RouteBufs b, int T, int k,
+                                    int n, int dout, int renorm, const CapTable& ct,
+                                    void* dobuf, void* dlb, int maxT, int n_pad,
+                                    const int32_t* pad_kept, cudaStream_t s, int pad_e0,
+                                    const PeerBufs& po, const PeerBufs& pdo);
 cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, RouteBufs b,
                                int T, int k, int n, int d_out, int renorm,
                                const CapTable& ct, void* dobuf, void* dlb, int maxT, int n_pad,

@@ -18,6 +18,7 @@
 #include "prof.h"
 #include "ep.h"
 #include "peer.h"
+#include "nccl_lsa.h"
 #include <map>
 
 using namespace moe;
@@ -48,7 +49,7 @@ struct moe_ctx {
   int n_local = 0, e_lo = 0, n_pad = 64;
   size_t s = 4;  // bytes per element
   cudaStream_t stream = nullptr, side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_gate = nullptr;
   std::vector<int32_t> cap;   // global capacities C_e (all n)
   CapTable ct{};              // GEMM side: cap (all n) + base of LOCAL expert regions
   CapTable cts{};             // token side (dispatch/combine/gate_dx): base/pre per global e
@@ -94,7 +95,8 @@ struct moe_ctx {
   // peer-memory transport (N1)
   int use_peer = 0, peer_attached = 0;
   PeerLayout PL{};
-  char* pwin = nullptr;              // own window (cudaMalloc)
+  char* pwin = nullptr;              // own window (cudaMalloc, or NCCL symmetric memory)
+  LsaWindow lsa{};                   // set when the window is an NCCL symmetric window
   PeerBufs wins{};                   // all ranks' windows in this process
   bool opened[MOE_MAX_R] = {};       // windows opened from IPC handles (closed at destroy)
   std::string err;
@@ -309,7 +311,8 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
 
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_gate, cudaEventDisableTiming) != cudaSuccess) {
     delete h;
     return MOE_ERR_CUDA;
   }
@@ -340,6 +343,7 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
       if (h->pwin) cudaFree(h->pwin);
       cudaEventDestroy(h->ev_fork);
       cudaEventDestroy(h->ev_join);
+      cudaEventDestroy(h->ev_gate);
       cudaStreamDestroy(h->side);
       delete h;
       return MOE_ERR_CUDA;
@@ -374,12 +378,15 @@ moe_status_t moe_destroy(moe_handle_t h) {
   if (h->ep) ep_destroy(h->ep);
   for (int j = 0; j < MOE_MAX_R; ++j)
     if (h->opened[j]) cudaIpcCloseMemHandle(h->wins.p[j]);
-  if (h->pwin) {
+  if (h->lsa.buf) {
+    lsa_window_destroy(&h->lsa);  // (synchronises the device first)
+  } else if (h->pwin) {
     cudaDeviceSynchronize();
     cudaFree(h->pwin);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ev_gate) cudaEventDestroy(h->ev_gate);
   if (h->side) cudaStreamDestroy(h->side);
   tc_plan_free(&h->tc);
   h->prof.destroy();
@@ -497,12 +504,12 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   h->last_cached = cached || fallback;
   // N2 (single GPU, tcgen05 path).  GATHER: the expert GEMMs gather x rows by
   // token_of_slot (no X buffer; the dispatch writes only the routing tables).  COMBINE: with
-  // k = 1 and the gate weights known before the experts (not cached), FWD2's epilogue also
-  // writes y (no combine pass re-reading O).
+  // k = 1, FWD2's epilogue also writes y (no combine pass re-reading O); in cached mode FWD2
+  // then waits for the gate (which ran concurrently with the routing, dispatch and FWD1).
   const bool tc1 = h->use_tc && !h->use_ep && T > 0;
   const bool gather = tc1 && (h->fusion & MOE_FUSE_GATHER) && ((uintptr_t)a->x % 16) == 0 &&
                       tc_gather_supported(d, f);
-  const bool fcomb = tc1 && (h->fusion & MOE_FUSE_COMBINE) && k == 1 && !cached &&
+  const bool fcomb = tc1 && (h->fusion & MOE_FUSE_COMBINE) && k == 1 &&
                      h->spec == nullptr && ((uintptr_t)a->y % 16) == 0 &&
                      tc_combine_supported(dout);
   h->fused_gather = gather;
@@ -601,6 +608,19 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     // pad rows of the received regions (single GPU: fused into the dispatch kernel)
     KL(h, 1, "zero_pad", sd, launch_zero_pad(dt, X, d, rb.kept, h->n_local, h->ct, sd));
   }
+  // Cached (S4.2): the gate is enqueued now -- after the routing / dispatch chain on the side
+  // stream, before the expert GEMMs -- so it runs concurrently with the routing and dispatch
+  // (enqueued after FWD1 it could only start once the persistent GEMM frees the SMs).
+  if (cached) {
+    if (h->use_tc)
+      KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, cidx, rb, s0));
+    else
+      KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, cidx, rb, s0));
+    if (tab)  // cache_step (S:254); the side stream only reads idx, never the table
+      KL(h, T > 0, "cache_update", s0, launch_cache_update(h->ctab, h->ctab_num, k, h->cids, T,
+                                                           rb.fresh_idx, s0));
+    CUDA_TRY(h, cudaEventRecord(h->ev_gate, s0));
+  }
   // expert FFN: H = relu(X W1^T + b1); O = H W2^T + b2 over kept_e rows per local expert
   const int nl = h->n_local;
   const char* w1 = (const char*)a->w1 + (size_t)h->e_lo * f * d * h->s;
@@ -610,10 +630,17 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   const int32_t* kept_local = rb.kept;
   if (h->use_tc) {
     int64_t nk = 0;
+    // cached + fused combine: FWD2's epilogue reads the gate weights -> join with the gate
+    struct Join { cudaStream_t sd; cudaEvent_t ev; } join{sd, h->ev_gate};
+    auto wait_gate = [](void* c) -> cudaError_t {
+      Join* j = static_cast<Join*>(c);
+      return cudaStreamWaitEvent(j->sd, j->ev, 0);
+    };
     moe_status_t st = tc_ffn_forward(&h->tc, X, w1, b1, w2, b2, H, O, h->rows, d, f, dout,
                                      kept_local, rb.mtile_prefix, nl, h->ct, h->max_cap_local,
                                      sd, &nk, &h->prof, (uint32_t*)(ws + h->L.mask),
-                                     (gather || fcomb || h->peer_ret) ? &fz : nullptr);
+                                     (gather || fcomb || h->peer_ret) ? &fz : nullptr,
+                                     (cached && fcomb) ? +wait_gate : nullptr, &join);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 forward failed");
   } else {
@@ -636,14 +663,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     moe_status_t st = ep_from_experts(h->ep, h->plan, O, O_tok, h->ct, dout, (int)h->s, sd, &err);  // C3
     if (st != MOE_OK) return fail(h, st, err);
   }
-  if (cached) {
-    if (h->use_tc)
-      KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, cidx, rb, s0));
-    else
-      KL(h, T > 0, "gate_topk", s0, launch_gate_topk(dt, a->x, a->w_gate, T, n, d, k, h->renorm, cidx, rb, s0));
-    if (tab)  // cache_step (S:254); the side stream only reads idx, never the table
-      KL(h, T > 0, "cache_update", s0, launch_cache_update(h->ctab, h->ctab_num, k, h->cids, T,
-                                                           rb.fresh_idx, s0));
+  if (cached) {  // join: everything after needs both the gate and the expert outputs
     CUDA_TRY(h, cudaEventRecord(h->ev_join, sd));
     CUDA_TRY(h, cudaStreamWaitEvent(s0, h->ev_join, 0));
   }
@@ -917,6 +937,25 @@ moe_status_t moe_peer_attach(moe_handle_t h, void* const* windows) {
   h->wins.nl = h->n_local;
   h->peer_attached = 1;
   return MOE_OK;
+}
+
+moe_status_t moe_peer_connect_nccl(moe_handle_t h, void* nccl_comm) {
+  if (!h || !nccl_comm) return MOE_ERR_INVALID_ARG;
+  if (!h->use_peer) return fail(h, MOE_ERR_STATE, "not a peer-transport handle");
+  if (h->peer_attached || h->lsa.buf)
+    return fail(h, MOE_ERR_STATE, "peer windows already attached");
+  void* ptrs[MOE_MAX_R] = {};
+  LsaWindow w;
+  std::string err;
+  moe_status_t st = lsa_window_create(nccl_comm, h->R, h->rank, h->PL.total, &w, ptrs, &err);
+  if (st != MOE_OK) return fail(h, st, err);
+  // the NCCL window replaces the cudaMalloc one (same layout, zeroed)
+  cudaDeviceSynchronize();
+  cudaFree(h->pwin);
+  h->pwin = (char*)w.buf;
+  h->lsa = w;
+  if (h->ws) bind_buffers(h);  // token_of_slot lives in the window
+  return moe_peer_attach(h, ptrs);
 }
 
 moe_status_t moe_peer_import(moe_handle_t h, const void* handles) {

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
     const int32_t* __restrict__ hist, int ntiles, int n, CapTable ct,
     int32_t* __restrict__ tile_off, int32_t* __restrict__ counts, int32_t* __restrict__ kept,
     int32_t* __restrict__ mtile_prefix, int64_t* __restrict__ drops,
-    uint32_t* __restrict__ ticket, int32_t* __restrict__ drop_cnt) {
+    uint32_t* __restrict__ ticket, int32_t* __restrict__ drop_cnt, int pad_gemm) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   const int e = blockIdx.x;
   __shared__ int32_t warp_tot[8];
@@ -295,8 +295,11 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
       if (q < n) {
         const int c = cq[j];
         kq = min(c, ct.cap[q]);
-        kept[q] = kq;
         dr += (long long)(c - kq);
+        // timing experiment only (MOE_DBG_PAD_GEMM=1): the expert GEMMs run over all C_e
+        // rows, as a capacity-padded implementation would -- results are NOT valid
+        if (pad_gemm) kq = ct.cap[q];
+        kept[q] = kq;
       }
       const int v = (kq + 127) / 128;
       int incl = v;
@@ -321,8 +324,12 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
 
 cudaError_t launch_route_scan(const int32_t* hist, int ntiles, int n, const CapTable& ct,
                               RouteBufs b, cudaStream_t s) {
+  static const int pad_gemm = [] {
+    const char* v = getenv("MOE_DBG_PAD_GEMM");
+    return v && v[0] == '1' ? 1 : 0;
+  }();
   launch_pdl(route_scan_kernel, n, 256, 0, s, hist, ntiles, n, ct, b.tile_off, b.counts, b.kept,
-                                      b.mtile_prefix, b.drops, b.ticket, b.drop_cnt);
+                                      b.mtile_prefix, b.drops, b.ticket, b.drop_cnt, pad_gemm);
   return cudaGetLastError();
 }
 
@@ -338,23 +345,6 @@ cudaError_t launch_route_scan(const int32_t* hist, int ntiles, int n, const CapT
 // whole 64-row K-blocks).  Fused into the dispatch / combine-backward kernels on one GPU.
 // Local region j starts at row ct.base[e0 + j]; regions are 128-row aligned and kept <= cap,
 // so roundup(kept, 64) never leaves the region.
-template <typename T>
-__device__ __forceinline__ void zero_pads_block(T* __restrict__ buf, int cols,
-                                                const int32_t* __restrict__ kept,
-                                                const CapTable& ct, int nreg, int e0, int first,
-                                                int stride) {
-  constexpr int VE = Vec<T>::N;
-  const int nvec = cols / VE;
-  for (int j = first; j < nreg; j += stride) {
-    const int kp = kept[j];
-    const int r0 = ct.base[e0 + j] + kp;
-    const int r1 = ct.base[e0 + j] + ((kp + MOE_PAD_ROWS - 1) / MOE_PAD_ROWS) * MOE_PAD_ROWS;
-    const size_t total = (size_t)max(r1 - r0, 0) * nvec;
-    for (size_t i = threadIdx.x; i < total; i += blockDim.x)
-      st_v4(buf + (size_t)r0 * cols + i * VE, make_uint4(0, 0, 0, 0));
-  }
-}
-
 template <typename T, int RU, int KM>
 __global__ void __launch_bounds__(256) dispatch_kernel(
     const int32_t* __restrict__ idx, const T* __restrict__ x, int Tn, int k, int n, int d,
@@ -956,6 +946,12 @@ cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, Rout
                                const int32_t* pad_kept, cudaStream_t s, int pad_e0,
                                const PeerBufs& po, const PeerBufs& pdo) {
   if (T == 0 && !(pad_kept && pdo.nl)) return cudaSuccess;  // peer EP: own pads still zeroed
+  if (dtype == 1) {  // bulk-copy staged form when it applies (bitwise equal, see its header)
+    const cudaError_t e = launch_combine_bwd_bulk(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf,
+                                                  dlb, maxT, n_pad, pad_kept, s, pad_e0, po, pdo);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();  // clear a sticky "not supported" from the attribute call, if any
+  }
   if (dtype == 1)
     return combine_bwd_t<__nv_bfloat16>(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf, dlb,
                                         maxT, n_pad, pad_kept, s, pad_e0, po, pdo);

@@ -117,10 +117,18 @@ class MoELayer:
         arr = (C.c_void_p * len(windows))(*windows)
         L.check(self.lib.moe_peer_attach(self.h, arr), self.h, "moe_peer_attach")
 
+    def peer_connect_nccl(self, nccl_comm: int):
+        """Cross-process ranks over an NCCL communicator (collective): the window becomes
+        NCCL symmetric memory and the peers' mappings come from the NCCL device API."""
+        L.check(self.lib.moe_peer_connect_nccl(self.h, C.c_void_p(nccl_comm)), self.h,
+                "moe_peer_connect_nccl")
+        self.peer_via = "nccl-symmetric-window"
+
     def peer_import(self, handles):
         """Cross-process ranks: all ranks' IPC handles (list of 64-byte strings)."""
         buf = C.create_string_buffer(b"".join(handles), 64 * len(handles))
         L.check(self.lib.moe_peer_import(self.h, buf), self.h, "moe_peer_import")
+        self.peer_via = "cuda-ipc"
 
     # -- recompile-enabled optimisations ----------------------------------------------
     @property

@@ -337,3 +337,29 @@ def test_peer_return_rows_loopback_oracle(k, renorm):
     assert st.routing.drops > 0
     assert_routing_exact(gpu, st, k, check_token_of_slot=True)
     assert_values(gpu, st, gr, ol, "bf16")
+
+
+@pytest.mark.parametrize("dtype,n,k,renorm", [("bf16", 16, 1, 0), ("f32", 8, 2, 1)])
+def test_peer_windows_on_nccl_symmetric_memory(comm, dtype, n, k, renorm):
+    """N1 on NCCL's symmetric memory: the peer window is re-allocated with ncclMemAlloc,
+    registered on torch's communicator (ncclCommWindowRegister, SYMMETRIC) and mapped through
+    the NCCL device API (ncclGetPeerPointer, LSA team); the layer then matches the oracle and
+    the single-GPU path bit for bit (1-rank loopback: one GPU here)."""
+    from paper_2205_01848_b200 import MoELayer
+    T, d, f = 777, 128, 256
+    caps = O.capacities_from_factors([1.0] * n, T, k)
+    pl = MoELayer(n, k, d, f, 0, T, dtype, renorm, world_size=1, rank=0, device="cuda",
+                  transport="peer")
+    pl.peer_connect_nccl(comm)
+    assert pl.peer_via == "nccl-symmetric-window"
+    try:
+        layer, gpu, st, gr, ol = run_pair(n, k, d, f, T, dtype, caps, renorm, layer=pl)
+        assert st.routing.drops > 0
+        assert_routing_exact(gpu, st, k, check_token_of_slot=True)
+        assert_values(gpu, st, gr, ol, dtype)
+        _, ref, _, _, _ = run_pair(n, k, d, f, T, dtype, caps, renorm)
+        for key in ("y", "dx", "dw1", "db1", "dw2", "db2", "dw_gate"):
+            assert np.array_equal(gpu[key], ref[key]), key
+        assert layer.check_flags()[1] == 0
+    finally:
+        pl.close()   # deregisters the window while the communicator is alive

@@ -98,8 +98,9 @@ def test_fused_bitwise_equals_unfused(n, k, d, f, T, renorm, regime, alpha):
 
 
 def test_fused_cached_mode_bitwise():
-    """Cached indices: the gate runs concurrently with the experts, so only the gather is
-    fused (the combine waits for the gate weights); results equal the unfused path."""
+    """Cached indices: the gate runs concurrently with the routing / dispatch / first GEMM on
+    the other stream and the second GEMM (fused combine) waits for its weights; results
+    equal the unfused path bitwise (y poisoned first: every row must be written)."""
     from paper_2205_01848_b200 import MoELayer, capacity_from_factors
     from synth import make_dy, make_layer
     n, k, d, f, T = 8, 1, 256, 256, 999
@@ -111,7 +112,7 @@ def test_fused_cached_mode_bitwise():
     layer.set_capacities(capacity_from_factors([1.0] * n, T, k))
     layer.set_cached_assignment(cidx)
     y0, g0 = _run(layer, g, dy, 0)
-    y1, g1 = _run(layer, g, dy, 3)
+    y1, g1 = _run(layer, g, dy, 3, y_fill=float("nan"))
     _bitwise(y1, y0, "y")
     for key in g0:
         _bitwise(g1[key], g0[key], key)
@@ -159,3 +160,33 @@ def test_fused_bitwise_at_bench_size():
         ref = float(w[t]) * o
         err = (y1[t].float() - ref).abs().max() / ref.abs().max()
         assert err < 2e-2, (t, float(err))
+
+
+@pytest.mark.parametrize("n,k,d,T,renorm,regime,lam,fusion", [
+    (64, 1, 1024, 4096, 0, "uniform", 0.0, 6),     # c3-shaped, fused dX (drop list, dlr)
+    (16, 2, 256, 1001, 1, "skewed", 0.0, 0),       # k = 2, heavy drops, ragged T
+    (8, 1, 128, 777, 0, "uniform", 0.3, 0),        # balance term, raw weights
+    (6, 2, 64, 300, 0, "uniform", 0.0, 0),         # n % 4 != 0: logits read from global
+])
+def test_combine_bwd_bulk_bitwise_equals_register_form(n, k, d, T, renorm, regime, lam, fusion,
+                                                       monkeypatch):
+    """The bulk-copy staged combine backward (combine_bwd_bulk.cu, opt-in MOE_CB_BULK=1)
+    computes the same arithmetic in the same order as the register-staged default kernel:
+    every output bitwise equal (dy, O rows and logits are only staged differently)."""
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer
+    g = {kk: v.cuda() for kk, v in make_layer(n, d, 2 * d, d, T, "bf16", regime).items()}
+    dy = make_dy(T, d, "bf16").cuda()
+    layer = MoELayer(n, k, d, 2 * d, 0, T, "bf16", renorm, device="cuda")
+    layer.set_capacities(capacity_from_factors([1.0] * n, T, k))
+    layer.set_balance_loss(lam)
+    outs = []
+    for bulk in ("0", "1"):
+        monkeypatch.setenv("MOE_CB_BULK", bulk)
+        y, gr = _run(layer, g, dy, fusion, y_fill=float("nan"))
+        r = layer.routing(T)
+        outs.append((gr, r["dl"].clone(), r["dw"].clone()))
+    (g1, dl1, dw1), (g2, dl2, dw2) = outs
+    assert torch.equal(dl1, dl2) and torch.equal(dw1, dw2)
+    for key in g1:
+        _bitwise(g2[key], g1[key], key)
