@@ -65,10 +65,12 @@ def parse():
     ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
                     help="expert-parallel exchange: peer = device-initiated through peer "
                          "memory over NVLink (N1, default); nccl = grouped send/recv")
-    ap.add_argument("--fusion", choices=["none", "combine", "dx", "default", "all"],
+    ap.add_argument("--fusion", choices=["none", "combine", "dx", "otok", "legacy", "default",
+                                         "all"],
                     default="default",
                     help="N2 fusions (k = 1): combine = y written by the second expert GEMM's "
-                         "epilogue; dx = dispatch backward inside the dX GEMM; default = both; "
+                         "epilogue; dx = dispatch backward inside the dX GEMM; default = combine+dx+otok; "
+                         "otok = O stored in (token, choice) order; legacy = combine+dx; "
                          "all = also gather x rows in the expert GEMMs (TMA gather4)")
     a = ap.parse_args()
     if a.emulate_padded:
@@ -303,11 +305,13 @@ def run_ours(args):
             layer.peer_attach([layer.peer_window()])
     layer.set_capacity_factors([alpha] * n, T * (ws if use_ep else 1))
     # N2 fusions (moe_set_fusion): gather x rows in the expert GEMMs, combine in FWD2 (k = 1)
-    fflags = {"none": 0, "combine": 2, "dx": 4, "default": 6, "all": 7}[args.fusion]
+    fflags = {"none": 0, "combine": 2, "dx": 4, "otok": 8, "legacy": 6, "default": 14,
+              "all": 15}[args.fusion]
     tc1 = not use_ep and cfg.dtype == "bf16" and getattr(layer, "uses_tcgen05", False)
     gather = tc1 and bool(fflags & 1) and d % 128 == 0 and f % 128 == 0
     fcomb = tc1 and bool(fflags & 2) and k == 1 and do % 128 == 0
     fdx = tc1 and bool(fflags & 4) and k == 1 and d % 128 == 0
+    otok = tc1 and bool(fflags & 8) and do % 128 == 0
     # peer EP (N1): return rows from the GEMM epilogues, and the dispatch backward in the
     # owners' dX GEMMs (k = 1)
     pret = (peer and cfg.dtype == "bf16" and getattr(layer, "uses_tcgen05", False)
@@ -328,8 +332,15 @@ def run_ours(args):
         cached_idx = layer.routing(T)["idx"].clone()
         layer.set_cached_assignment(cached_idx)
 
+    # TIMING EXPERIMENT ONLY (MOE_BENCH_L2CLEAN=1, profiled pass): a 2x-L2 read between the
+    # forward and the backward writes back and evicts the forward's dirty L2 lines, so the
+    # backward's first kernel is timed without the previous kernel's deferred write-back
+    l2clean = None
+
     def step():
         layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"], y=y)
+        if l2clean is not None:
+            l2clean.sum()
         layer.backward(dy, grads=grads)
 
     # dynamic capacity factors (S4.1): the library's policy (reading 14) adapts
@@ -434,8 +445,11 @@ def run_ours(args):
     time.sleep(2.0)
     layer.profile(True)
     layer.profile_read(reset=True)
+    if os.environ.get("MOE_BENCH_L2CLEAN") == "1":
+        l2clean = torch.ones(l2_bytes // 2, dtype=torch.float32, device=dev)
     barrier()
     pm = timed_steps(args.steps)
+    l2clean = None
     torch.cuda.synchronize(dev)
     prof_ms_step = max_over_ranks(sum(a_.elapsed_time(b_) for a_, b_ in pm)) / args.steps
     barrier()
@@ -620,6 +634,7 @@ def run_ours(args):
                               "no flush"),
                        "fusion": "+".join([nm for nm, on in (("gather", gather), ("combine", fcomb),
                                                              ("dx", fdx or fdx_ep),
+                                                             ("otok", otok),
                                                              ("return_rows", pret)) if on]) or "none",
                        "kept_assignments": A, "drops": stats["drops"],
                        "drop_rate": round(stats["drops"] / max(1, T * k * (ws if use_ep else 1)), 5),

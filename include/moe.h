@@ -358,7 +358,7 @@ MOE_API moe_status_t moe_peer_import(moe_handle_t h, const void* handles /* host
 MOE_API moe_status_t moe_peer_connect_nccl(moe_handle_t h, void* nccl_comm);
 
 /* N2 fusions of the single-GPU tcgen05 path, a bitmask of moe_fusion_t;
-   default MOE_FUSE_COMBINE | MOE_FUSE_DX (GATHER is opt-in: on B200 the TMA gather4 stream
+   default MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK (GATHER is opt-in: on B200 the TMA gather4 stream
    is slower than the dispatch copy it replaces).  GATHER and COMBINE give
    bitwise identical results (same products, same accumulation order); DX see below.
    MOE_FUSE_GATHER: the expert GEMMs that read x rows (H = relu(X W1^T + b1) and
@@ -379,8 +379,15 @@ MOE_API moe_status_t moe_peer_connect_nccl(moe_handle_t h, void* nccl_comm);
      epilogue writes dx rows directly (no dX buffer, no separate pass); tokens whose pair was
      dropped get dx = dl W_g from a small kernel.  NOT bitwise equal to the unfused path (dX
      is no longer rounded to bf16 before the sum -- one rounding instead of two); within the
-     bf16 tolerance of the oracle. */
-typedef enum { MOE_FUSE_GATHER = 1, MOE_FUSE_COMBINE = 2, MOE_FUSE_DX = 4 } moe_fusion_t;
+     bf16 tolerance of the oracle.
+   MOE_FUSE_OTOK (world_size == 1, bf16, d_out a multiple of 128): the second expert GEMM's
+     epilogue stores O in (token, choice) order -- row t k + r of the O buffer -- instead of
+     expert-region order, so the combine and the combine backward read a token's O rows
+     without first resolving its routing slots (the row loads issue together with the
+     routing-table loads).  Bitwise equal to the expert-order layout; moe_get_routing's o_buf
+     is then [T k x d_out] in token order. */
+typedef enum { MOE_FUSE_GATHER = 1, MOE_FUSE_COMBINE = 2, MOE_FUSE_DX = 4,
+               MOE_FUSE_OTOK = 8 } moe_fusion_t;
 MOE_API moe_status_t moe_set_fusion(moe_handle_t h, int32_t flags);
 
 /* Number of kernels the library launched since the handle was created (for bench

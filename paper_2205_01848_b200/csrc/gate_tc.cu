@@ -39,6 +39,9 @@ struct GateFwdParams {
   int tma_logits;          // logits written by TMA from a staged 32 x 16 box (n % 16 == 0)
   int32_t* hist;           // [T / 128 x n] per-tile expert histogram of idx_out (A3 fused into
                            // the epilogue; the 128-token M tile is the routing tile), or null
+  float4* stats;           // [T] softmax statistics for the combine backward, or null:
+                           // (max logit m, sum_e exp(l_e - m), sum over the experts NOT in the
+                           // dispatch set of exp(l_e - m), 0)
 };
 
 // logits staging of the gate epilogue: one 32-row x 16-column fp32 box (2 KB, 64-byte
@@ -237,7 +240,6 @@ __global__ void __launch_bounds__(G_THREADS, 2)
           if (r < k) cidx[r] = p.cached[(size_t)t * k + r];
       }
       float m_run = -INFINITY;
-      float s_run = 0.f;  // raw mode: online softmax denominator sum_e exp(l_e - m_run)
       bool nan_seen = false;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       float* lrow = p.logits + (size_t)t * n;
@@ -304,37 +306,63 @@ __global__ void __launch_bounds__(G_THREADS, 2)
             if (cidx[r] == e) cval[r] = v;
           }
         }
-        // row max and (raw mode) the softmax denominator from registers, rescaled per chunk
-        float cm = -INFINITY;
+        // row max from registers
 #pragma unroll
         for (int j = 0; j < 32; ++j)
-          if (c * 32 + j < n) cm = fmaxf(cm, __uint_as_float(r32[j]));
-        if (cm > m_run) {
-          if (!p.renorm) s_run *= expf(m_run - cm);
-          m_run = cm;
-        }
-        if (!p.renorm) {
+          if (c * 32 + j < n) m_run = fmaxf(m_run, __uint_as_float(r32[j]));
+      }
+      // the dispatch set: the cached indices when valid, else the fresh top-k
+      float lv[KM];
+      int use[KM];
+      bool ok = true, unknown = false;
+      if (p.cached) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c * 32 + j < n) s_run += expf(__uint_as_float(r32[j]) - m_run);
+        for (int r = 0; r < KM; ++r) {
+          if (r >= k) break;
+          ok &= (cidx[r] >= 0 && cidx[r] < n);
+          unknown |= cidx[r] == -1;
+#pragma unroll
+          for (int q2 = 0; q2 < r; ++q2) ok &= (cidx[q2] != cidx[r]);
         }
+      }
+#pragma unroll
+      for (int r = 0; r < KM; ++r) {
+        use[r] = (p.cached && ok) ? cidx[r] : sel_e[r];
+        lv[r] = (p.cached && ok) ? cval[r] : sel_v[r];
+      }
+      // Softmax denominator (raw mode) and the backward's statistics: a second pass over the
+      // accumulator (warp-collective TMEM loads, every lane) splits sum_e exp(l_e - m) into the
+      // experts outside the dispatch set (ens, ascending e) and the selected ones (esel), so the
+      // combine backward gets 1 - p_sel = ens / s without cancellation.
+      float ens = 0.f, s_run = 0.f;
+      float esel[KM];
+#pragma unroll
+      for (int r = 0; r < KM; ++r) esel[r] = (r < k) ? expf(lv[r] - m_run) : 0.f;
+      if (!p.renorm || p.stats) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          if (c * 32 >= n) break;  // warp-uniform
+          uint32_t r32[32];
+          tmem_ld32(taddr + c * 32, r32);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int e = c * 32 + j;
+            bool sel = false;
+#pragma unroll
+            for (int r = 0; r < KM; ++r) sel |= (r < k && use[r] == e);
+            if (e < n && !sel) ens += expf(__uint_as_float(r32[j]) - m_run);
+          }
+        }
+        s_run = ens;
+#pragma unroll
+        for (int r = 0; r < KM; ++r) s_run += esel[r];
       }
       tc_fence_before();
       mbar_arrive(&b.tempty[acc]);
       if (valid) {
         if (nan_seen) atomicOr(p.flags, 1);
-        float lv[KM];
-        int use[KM];
+        if (p.stats) p.stats[t] = make_float4(m_run, s_run, ens, 0.f);
         if (p.cached) {
-          bool ok = true, unknown = false;
-#pragma unroll
-          for (int r = 0; r < KM; ++r) {
-            if (r >= k) break;
-            ok &= (cidx[r] >= 0 && cidx[r] < n);
-            unknown |= cidx[r] == -1;
-#pragma unroll
-            for (int q2 = 0; q2 < r; ++q2) ok &= (cidx[q2] != cidx[r]);
-          }
           // an unknown sample (fallback mode) is routed by its fresh top-k, a miss
           if (!ok && !(unknown && p.idx_fix)) atomicOr(p.flags, 2);
           if (!ok && p.idx_fix) {
@@ -352,19 +380,7 @@ __global__ void __launch_bounds__(G_THREADS, 2)
             same &= found;
           }
           if (same && ok) atomicAdd(p.hit, 1);
-#pragma unroll
-          for (int r = 0; r < KM; ++r) {
-            use[r] = ok ? cidx[r] : sel_e[r];
-            lv[r] = ok ? cval[r] : sel_v[r];
-          }
-        } else {
-#pragma unroll
-          for (int r = 0; r < KM; ++r) {
-            use[r] = sel_e[r];
-            lv[r] = sel_v[r];
-          }
         }
-        (void)use;
         int32_t* orow = p.idx_out + (size_t)t * k;
         float* wrow = p.w_out + (size_t)t * k;
         // raw mode: p_i = exp(l_i - max) / sum_e exp(l_e - max), the row re-read from L1/L2
@@ -381,10 +397,9 @@ __global__ void __launch_bounds__(G_THREADS, 2)
           for (int r = 0; r < KM; ++r)
             if (r < k) { wrow[r] = ev[r] / ssum; orow[r] = sel_e[r]; }
         } else {
-          const float ssum = s_run;
 #pragma unroll
           for (int r = 0; r < KM; ++r)
-            if (r < k) { wrow[r] = expf(lv[r] - m_run) / ssum; orow[r] = sel_e[r]; }
+            if (r < k) { wrow[r] = esel[r] / s_run; orow[r] = sel_e[r]; }
         }
         if (p.hist) {
 #pragma unroll
@@ -810,7 +825,7 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
   GateFwdParams p{T, n, k, renorm, cached, b.logits, cached ? b.fresh_idx : b.idx, b.w,
                   b.hit_count, b.flags, cached ? b.idx_fix : nullptr,
                   getenv("MOE_GATE_DBG") ? atoi(getenv("MOE_GATE_DBG")) : 0, tma_logits,
-                  (!cached && b.gate_hist) ? b.tile_hist : nullptr};
+                  (!cached && b.gate_hist) ? b.tile_hist : nullptr, (float4*)b.sstat};
   const int MT = (T + 127) / 128;
   // two CTAs per SM (4-stage rings): twice the epilogue warps, which bound this kernel
   const int grid = MT < 2 * g_sms ? MT : 2 * g_sms;

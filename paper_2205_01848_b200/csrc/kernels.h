@@ -39,10 +39,13 @@ struct RouteBufs {
   int32_t* drop_tok;      // [maxT] token of each compacted row
   int32_t* drop_cnt;      // [1] rows in the list (reset by route_scan, counted by combine_bwd)
   int gate_hist;          // the tcgen05 gate also writes tile_hist (route_hist skipped)
-  int o_pair;             // peer EP return rows: O (and dX) of pair (t, r) at row t k + r of the
-                          // local return buffer, stored there by the owners' GEMM epilogues
+  int o_pair;             // O of pair (t, r) at row t k + r: peer EP return rows (stored by the
+                          // owners' GEMM epilogues) or the single-GPU token-ordered O (OTOK)
+  int dx_pair;            // peer EP return rows: dX of pair (t, r) at row t k + r as well
   int32_t* idx_fix;       // cache fallback mode: the gate writes the fresh top-k of unknown
                           // samples (cached row with -1) into these dispatch-index rows
+  float* sstat;           // [T x 4] softmax statistics (m, sum exp, exp mass outside the dispatch
+                          // set, 0) written by the tcgen05 gate for the combine backward, or null
 };
 
 // Per-sample assignment cache (N4; SPEC cache_step / cached_route): idx[t] = table[ids[t]]
@@ -78,11 +81,6 @@ cudaError_t launch_zero_pad(int dtype, void* buf, int cols, const int32_t* kept,
 cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, int k,
                                int d_out, const CapTable& ct, void* y, cudaStream_t s,
                                const PeerBufs& po = PeerBufs{});
-cudaError_t launch_combine_bwd_bulk(const void* dy, const void* obuf, RouteBufs b, int T, int k,
-                                    int n, int dout, int renorm, const CapTable& ct,
-                                    void* dobuf, void* dlb, int maxT, int n_pad,
-                                    const int32_t* pad_kept, cudaStream_t s, int pad_e0,
-                                    const PeerBufs& po, const PeerBufs& pdo);
 cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, RouteBufs b,
                                int T, int k, int n, int d_out, int renorm,
                                const CapTable& ct, void* dobuf, void* dlb, int maxT, int n_pad,

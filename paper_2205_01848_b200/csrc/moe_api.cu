@@ -40,7 +40,7 @@ int moe::pdl_enabled() {
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
       xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, grow, ep_all, sendbuf, oret, dwg32,
-      pre_dev, dlr, dropb, droptok, total;
+      pre_dev, dlr, dropb, droptok, sstat, total;
 };
 
 struct moe_ctx {
@@ -71,9 +71,10 @@ struct moe_ctx {
   moe_fwd_args_t fa{};
   int64_t launches = 0;
   int use_tc = 0;             // tcgen05 path for bf16 (env MOE_FORCE_SIMT=1 disables)
-  int fusion = MOE_FUSE_COMBINE | MOE_FUSE_DX;  // N2 fusions (moe_set_fusion; GATHER opt-in)
+  int fusion = MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK;  // N2 (moe_set_fusion; GATHER opt-in)
   int fused_gather = 0;       // the last forward gathered x rows in the GEMMs (no X buffer)
   int peer_ret = 0;           // peer EP: O / dX rows returned by the GEMM epilogues (N1)
+  int otok = 0;               // the last forward stored O in (token, choice) order (MOE_FUSE_OTOK)
   TcPlan tc{};
   Prof prof;
   float balance_lambda = 0.f; // Eq. 3 balance term weight (0 = off)
@@ -147,7 +148,9 @@ void compute_layout(moe_ctx* h) {
   L.token_of_slot = take(h->use_peer ? 0 : std::max<size_t>((size_t)h->rows, T * k) * 4);
   L.xbuf = take(prow * h->d * h->s);
   L.hbuf = take((size_t)h->rows * h->f * h->s);
-  L.obuf = take(prow * h->dout * h->s);
+  // single GPU, tcgen05: O may be stored in (token, choice) order instead (MOE_FUSE_OTOK)
+  const size_t orow = (!h->use_ep && h->use_tc) ? std::max(prow, T * k) : prow;
+  L.obuf = take(orow * h->dout * h->s);
   L.dobuf = take(prow * h->dout * h->s);
   L.dxbuf = take(prow * h->d * h->s);
   const size_t splits = std::max(gate_dw_splits(h->maxT, h->d), gate_dw_tc_splits(h->maxT, h->n, h->d));
@@ -170,6 +173,7 @@ void compute_layout(moe_ctx* h) {
   L.sendbuf = take(ep ? T * k * (size_t)std::max(h->d, h->dout) * h->s : 0);
   L.oret = take(ep ? T * k * (size_t)h->dout * h->s : 0);
   L.dwg32 = take(ep ? n * (size_t)h->d * 4 : 0);
+  L.sstat = take(h->use_tc ? T * 16 : 0);
   L.total = o;
 }
 
@@ -200,8 +204,10 @@ void bind_buffers(moe_ctx* h) {
   r.dlr = nullptr;
   r.pdlr = PeerBufs{};
   r.o_pair = 0;
+  r.dx_pair = 0;
   r.gate_hist = 0;
   r.drop_tok = (int32_t*)(b + L.droptok);
+  r.sstat = nullptr;  // set per forward (tcgen05 gate, when the backward needs p)
   r.drop_cnt = meta + 783;
 }
 
@@ -512,7 +518,12 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   const bool fcomb = tc1 && (h->fusion & MOE_FUSE_COMBINE) && k == 1 &&
                      h->spec == nullptr && ((uintptr_t)a->y % 16) == 0 &&
                      tc_combine_supported(dout);
+  // O rows in (token, choice) order: FWD2's epilogue stores row t k + r (the peer EP return-row
+  // store with this rank as the only owner), so the combine and its backward read O by token
+  // with no routing-table lookup in front of the row loads
+  const bool otok = tc1 && (h->fusion & MOE_FUSE_OTOK) && tc_combine_supported(dout);
   h->fused_gather = gather;
+  h->otok = otok;
   TcFusion fz;
   fz.T = T;
   fz.tos = rb.token_of_slot;
@@ -525,8 +536,16 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   if (h->peer_ret) {  // N1: FWD2's epilogue stores O rows into the token owners' windows
     fz.pret_o = peer_bufs(h, h->PL.oret);
     fz.tpr = T;
+  } else if (otok) {
+    fz.pret_o.p[0] = (char*)O;
+    fz.pret_o.nl = 1;
+    fz.tpr = T;
   }
   CUDA_TRY(h, cudaMemsetAsync(rb.hit_count, 0, 4, s0));
+  // softmax statistics from the tcgen05 gate for the combine backward (raw weights or the
+  // Eq. 3 balance term need the full p); kept with the forward's state
+  rb.sstat = (h->use_tc && (!h->renorm || h->balance_lambda != 0.f))
+                 ? (float*)(ws + h->L.sstat) : nullptr;
   if (tab)  // idx[t] = table[sample_ids[t]] (before the fork: the side stream reads it)
     KL(h, T > 0, "cache_gather", s0, launch_cache_gather(h->ctab, h->ctab_num, k, h->cids, T,
                                                          rb.idx, rb.flags, s0));
@@ -639,7 +658,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     moe_status_t st = tc_ffn_forward(&h->tc, X, w1, b1, w2, b2, H, O, h->rows, d, f, dout,
                                      kept_local, rb.mtile_prefix, nl, h->ct, h->max_cap_local,
                                      sd, &nk, &h->prof, (uint32_t*)(ws + h->L.mask),
-                                     (gather || fcomb || h->peer_ret) ? &fz : nullptr,
+                                     (gather || fcomb || h->peer_ret || otok) ? &fz : nullptr,
                                      (cached && fcomb) ? +wait_gate : nullptr, &join);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 forward failed");
@@ -688,7 +707,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   }
   rb.spec = h->spec;
   rb.spec_valid = h->spec_valid;
-  rb.o_pair = h->peer_ret;
+  rb.o_pair = h->peer_ret || otok;
   if (!fcomb)
     KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O_tok, rb, T, k, dout, h->cts, a->y, s0, po));
   rb.spec = nullptr;
@@ -761,7 +780,8 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   rb.pdlr = fdx_ep ? peer_bufs(h, h->PL.dlr) : PeerBufs{};
   rb.dropb = (fdx || fdx_ep) ? (__nv_bfloat16*)(ws + h->L.dropb) : nullptr;
 
-  rb.o_pair = peer && h->peer_ret;
+  rb.o_pair = (peer && h->peer_ret) || h->otok;
+  rb.dx_pair = peer && h->peer_ret;
   KL(h, T > 0, "combine_bwd", s0, launch_combine_bwd(dt, a->dy, O_tok, rb, T, k, n, dout, h->renorm, h->cts,
                                                      dO_tok, dlb, h->maxT, h->n_pad,
                                                      nccl_ep ? nullptr : rb.kept, s0,
@@ -769,6 +789,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                                                      peer && !h->peer_ret ? peer_bufs(h, h->PL.o) : PeerBufs{},
                                                      peer ? peer_bufs(h, h->PL.dob) : PeerBufs{}));
   rb.o_pair = 0;
+  rb.dx_pair = 0;
   rb.dspec = nullptr;
   rb.dw_ext = nullptr;
   rb.bal_g = nullptr;
@@ -1179,7 +1200,7 @@ moe_status_t moe_vcomm_destroy(void* comm) { return vcomm_destroy(comm); }
 
 moe_status_t moe_set_fusion(moe_handle_t h, int32_t flags) {
   if (!h) return MOE_ERR_INVALID_ARG;
-  if (flags & ~(MOE_FUSE_GATHER | MOE_FUSE_COMBINE | MOE_FUSE_DX))
+  if (flags & ~(MOE_FUSE_GATHER | MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK))
     return fail(h, MOE_ERR_INVALID_ARG, "unknown fusion flag");
   h->fusion = flags;
   return MOE_OK;

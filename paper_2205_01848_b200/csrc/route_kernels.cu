@@ -531,20 +531,24 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
   constexpr int VE = Vec<T>::N;
   const int nvec = dout / VE;
   const T* src[KM];  // O row of each kept pair (peer EP: read from the owner over NVLink)
+  const T* lsrc[KM]; // the row each load reads: with o_pair known before the routing tables
   float wr[KM];
 #pragma unroll
   for (int r = 0; r < KM; ++r) {
     src[r] = nullptr;
+    lsrc[r] = (o_pair && r < k) ? obuf + ((size_t)t * k + r) * dout : nullptr;
     wr[r] = 0.f;
     if (r < k) {
       const int sl = slot_of[(size_t)t * k + r];
       if (sl >= 0) {
         const int e = idx[(size_t)t * k + r];
-        // o_pair (peer EP return rows): the owner's GEMM stored O at this (token, choice) row
+        // o_pair (O in (token, choice) order, or peer EP return rows): the GEMM stored O at
+        // this (token, choice) row
         src[r] = o_pair ? obuf + ((size_t)t * k + r) * dout
                         : peer_row(obuf, po, e, (size_t)(ct.base[e] + sl), dout);
         wr[r] = w[(size_t)t * k + r];
       }
+      if (!o_pair) lsrc[r] = src[r];
     }
   }
   T* yrow = y + (size_t)t * dout;
@@ -555,7 +559,7 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int v = vb + j * 32 + lane;
-      if (src[r] && v < nvec) u[r][j] = ld_nc_v4(src[r] + (size_t)v * VE);
+      if (lsrc[r] && v < nvec) u[r][j] = ld_nc_v4(lsrc[r] + (size_t)v * VE);
     }
   if (spec) {  // AggregateSpec (App. A): the chosen experts' rows, zeros if dropped
 #pragma unroll
@@ -681,28 +685,72 @@ cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, 
 // raw dl_j = p_j (dp_j - sum_r w_r dw_r) with dp_j = dw_r at j = i_r.  Warp per token; the
 // logits, dy and O rows are all requested before the first use.
 // =====================================================================================
-template <typename T, int VPL, int KM>
-__global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
+#ifndef MOE_CB_MINB
+#define MOE_CB_MINB 4  // resident 256-thread blocks per SM (register budget 64)
+#endif
+// NL = expert pairs per lane (n <= 64 NL); FULL = the loss-variant / EP features (spec
+// gradients, balance term, peer buffers, pad zeroing) compiled in, else they are off (the
+// single-GPU product path: fewer registers and instructions, same arithmetic)
+template <typename T, int VPL, int KM, int NL, bool FULL>
+__global__ void __launch_bounds__(256, MOE_CB_MINB) combine_bwd_kernel(
     const T* __restrict__ dy, const T* __restrict__ obuf, const float* __restrict__ w,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of,
     const float* __restrict__ logits, CapTable ct, int Tn, int k, int n, int dout, int renorm,
     T* __restrict__ dobuf, float* __restrict__ dw, float* __restrict__ dl,
-    __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad, const T* __restrict__ dspec,
-    const float* __restrict__ dw_ext, const float* __restrict__ bal_g,
+    __nv_bfloat16* __restrict__ dlb, int maxT, int n_pad, const float4* __restrict__ sstat,
+    const T* __restrict__ dspec_,
+    const float* __restrict__ dw_ext_, const float* __restrict__ bal_g_,
     int32_t* __restrict__ grow, const int32_t* __restrict__ pad_kept, int pad_e0, PeerBufs po,
     PeerBufs pdo, __nv_bfloat16* __restrict__ dlr, PeerBufs pdlr, __nv_bfloat16* __restrict__ dropb,
-    int32_t* __restrict__ drop_tok, int32_t* __restrict__ drop_cnt, int o_pair) {
+    int32_t* __restrict__ drop_tok, int32_t* __restrict__ drop_cnt, int o_pair, int dx_pair) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
+  const T* dspec = FULL ? dspec_ : nullptr;
+  const float* dw_ext = FULL ? dw_ext_ : nullptr;
+  const float* bal_g = FULL ? bal_g_ : nullptr;
   // peer EP (N1): O rows are read from, and dO rows written to, the experts' owners
   if (pad_kept)
-    zero_pads_block(dobuf, dout, pad_kept, ct, pdo.nl ? pdo.nl : n, pad_e0, blockIdx.x, gridDim.x);
+    zero_pads_block(dobuf, dout, pad_kept, ct, (FULL && pdo.nl) ? pdo.nl : n, pad_e0, blockIdx.x,
+                    gridDim.x);
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= Tn) return;
   constexpr int VE = Vec<T>::N;
-  constexpr int NL = MOE_MAX_E / 64;  // expert pairs per lane (n <= 256)
   const bool need_p = !renorm || bal_g != nullptr;  // full softmax row needed
   const int nvec = dout / VE;
+  const T* dyrow = dy + (size_t)t * dout;
+  // Everything that does not depend on the routing tables is requested first, so the
+  // slot / index loads overlap the row loads instead of preceding them: the statistics and
+  // logits row, and (lean path) the first block of the dy row and -- O in (token, choice)
+  // order -- of the O rows.
+  uint4 g[VPL];
+  uint4 u[KM][VPL];
+  if (!FULL) {
+#pragma unroll
+    for (int jv = 0; jv < VPL; ++jv) {
+      const int v = jv * 32 + lane;
+      if (v < nvec) g[jv] = ld_nc_v4(dyrow + (size_t)v * VE);
+    }
+    if (o_pair) {
+#pragma unroll
+      for (int r = 0; r < KM; ++r)
+#pragma unroll
+        for (int jv = 0; jv < VPL; ++jv) {
+          const int v = jv * 32 + lane;
+          if (r < k && v < nvec) u[r][jv] = ld_nc_v4(obuf + ((size_t)t * k + r) * dout + (size_t)v * VE);
+        }
+    }
+  }
+  float4 st4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (need_p && sstat != nullptr) st4 = sstat[t];
+  // this lane's experts: pairs e = 2*lane + 64*j (+1)
+  float lg[NL][2];
+  const float* l = logits + (size_t)t * n;
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const int e = 2 * lane + 64 * j;
+    lg[j][0] = (need_p && e < n) ? l[e] : -INFINITY;
+    lg[j][1] = (need_p && e + 1 < n) ? l[e + 1] : -INFINITY;
+  }
   int rows[KM], er[KM];
   float wr[KM], part[KM];
   const T* osrc[KM];
@@ -716,10 +764,16 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
       er[r] = idx[(size_t)t * k + r];
       rows[r] = sl >= 0 ? ct.base[er[r]] + sl : -1;
       wr[r] = w[(size_t)t * k + r];
+      // o_pair (O in (token, choice) order: MOE_FUSE_OTOK, or peer EP return rows): the row
+      // address needs no routing table, so its load is issued unconditionally, concurrently
+      // with the slot / index loads (a dropped pair's row is unwritten and never used)
+      if (o_pair) osrc[r] = obuf + ((size_t)t * k + r) * dout;
       if (rows[r] >= 0) {
-        osrc[r] = o_pair ? obuf + ((size_t)t * k + r) * dout  // peer EP return rows (local)
-                         : peer_row(obuf, po, er[r], (size_t)rows[r], dout);
-        odst[r] = peer_row(dobuf, pdo, er[r], (size_t)rows[r], dout);
+        if (!o_pair)
+          osrc[r] = FULL ? peer_row(obuf, po, er[r], (size_t)rows[r], dout)
+                         : obuf + (size_t)rows[r] * dout;
+        odst[r] = FULL ? peer_row(dobuf, pdo, er[r], (size_t)rows[r], dout)
+                       : dobuf + (size_t)rows[r] * dout;
       }
     }
   }
@@ -733,30 +787,20 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
     }
     dpos = __shfl_sync(0xffffffffu, dpos, 0);
   }
-  // this lane's experts: pairs e = 2*lane + 64*j (+1)
-  float lg[NL][2];
-  const float* l = logits + (size_t)t * n;
-#pragma unroll
-  for (int j = 0; j < NL; ++j) {
-    const int e = 2 * lane + 64 * j;
-    lg[j][0] = (need_p && e < n) ? l[e] : -INFINITY;
-    lg[j][1] = (need_p && e + 1 < n) ? l[e + 1] : -INFINITY;
-  }
-  const T* dyrow = dy + (size_t)t * dout;
   for (int vb = 0; vb < nvec; vb += VPL * 32) {  // one pass for d_out*s <= 512*VPL bytes
-  uint4 g[VPL];
-  uint4 u[KM][VPL];
+  const bool early = !FULL && vb == 0;  // the lean path's first block is already in flight
 #pragma unroll
   for (int jv = 0; jv < VPL; ++jv) {
     const int v = vb + jv * 32 + lane;
-    if (v < nvec) g[jv] = ld_nc_v4(dyrow + (size_t)v * VE);
+    if (!early && v < nvec) g[jv] = ld_nc_v4(dyrow + (size_t)v * VE);
   }
 #pragma unroll
   for (int r = 0; r < KM; ++r)
 #pragma unroll
     for (int jv = 0; jv < VPL; ++jv) {
       const int v = vb + jv * 32 + lane;
-      if (rows[r] >= 0 && v < nvec) u[r][jv] = ld_nc_v4(osrc[r] + (size_t)v * VE);
+      if (!(early && o_pair) && osrc[r] != nullptr && v < nvec)
+        u[r][jv] = ld_nc_v4(osrc[r] + (size_t)v * VE);
     }
 #pragma unroll
   for (int jv = 0; jv < VPL; ++jv) {
@@ -800,14 +844,20 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
       if (grow)  // the gate-dx kernel's gather table (peer EP: owner in the top bits; with
                  // return rows the dX row is this rank's own (token, choice) row)
         grow[(size_t)t * k + r] = rows[r] < 0 ? -1
-                                  : o_pair ? (int)((size_t)t * k + r)
-                                  : pdo.nl ? rows[r] | ((er[r] / pdo.nl) << MOE_GROW_SHIFT)
+                                  : dx_pair ? (int)((size_t)t * k + r)
+                                  : (FULL && pdo.nl) ? rows[r] | ((er[r] / pdo.nl) << MOE_GROW_SHIFT)
                                            : rows[r];
     }
   float m = -INFINITY, sp = 0.f, cb = 0.f;
   float ens = 0.f;     // raw mode: exp mass of the experts NOT selected for this token
   float esel[KM];      // raw mode: exp(l - m) of each selected expert
-  if (need_p) {
+  if (need_p && sstat != nullptr) {
+    // the tcgen05 gate's statistics of this row (max, sum, mass outside the dispatch set):
+    // no warp reductions here, and ens was summed without cancellation
+    m = st4.x;
+    sp = st4.y;
+    ens = st4.z;
+  } else if (need_p) {
 #pragma unroll
     for (int j = 0; j < NL; ++j) m = fmaxf(m, fmaxf(lg[j][0], lg[j][1]));
 #pragma unroll
@@ -828,6 +878,8 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
     }
     sp = __shfl_sync(0xffffffffu, warp_sum(sp), 0);
     ens = __shfl_sync(0xffffffffu, warp_sum(ens), 0);
+  }
+  if (need_p) {
 #pragma unroll
     for (int r = 0; r < KM; ++r)
       esel[r] = (r < k && er[r] >= 0 && er[r] < n) ? expf(l[er[r]] - m) : 0.f;
@@ -904,7 +956,8 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
       *reinterpret_cast<__nv_bfloat162*>(dlb + (size_t)t * n_pad + e0) = hi;
       *reinterpret_cast<__nv_bfloat162*>(dlb + ((size_t)maxT + t) * n_pad + e0) = lo;
       if (dlr && rows[0] >= 0) {  // k = 1 fused dispatch backward: the pair by expert row
-        __nv_bfloat16* rr = peer_row(dlr, pdlr, er[0], (size_t)rows[0], 2 * n_pad);
+        __nv_bfloat16* rr = FULL ? peer_row(dlr, pdlr, er[0], (size_t)rows[0], 2 * n_pad)
+                                 : dlr + (size_t)rows[0] * 2 * n_pad;
         *reinterpret_cast<__nv_bfloat162*>(rr + e0) = hi;
         *reinterpret_cast<__nv_bfloat162*>(rr + n_pad + e0) = lo;
       }
@@ -924,18 +977,35 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
                                  const PeerBufs& pdo) {
   dim3 grid(std::max(1, (T_ + 7) / 8));
   const int vpl = (d_out / Vec<T>::N + 31) / 32;  // > 8: the kernel loops over 4 KB blocks
-#define CB(V, K)                                                                               \
-  launch_pdl(combine_bwd_kernel<T, V, K>, grid, 256, 0, s, (const T*)dy, (const T*)obuf, b.w, b.idx,   \
-                                                   b.slot_of, b.logits, ct, T_, k, n, d_out,   \
-                                                   renorm, (T*)dobuf, b.dw, b.dl,              \
-                                                   (__nv_bfloat16*)dlb, maxT, n_pad,           \
-                                                   (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow, pad_kept, \
-                                                   pad_e0, po, pdo, b.dlr, b.pdlr, b.dropb, \
-                                                   b.drop_tok, b.drop_cnt, b.o_pair)
+#define CB(V, K, NLL, F)                                                                       \
+  launch_pdl(combine_bwd_kernel<T, V, K, NLL, F>, grid, 256, 0, s, (const T*)dy, (const T*)obuf, \
+             b.w, b.idx, b.slot_of, b.logits, ct, T_, k, n, d_out, renorm, (T*)dobuf, b.dw,    \
+             b.dl, (__nv_bfloat16*)dlb, maxT, n_pad, (const float4*)b.sstat,                   \
+             (const T*)b.dspec, b.dw_ext, b.bal_g, b.grow, pad_kept, pad_e0, po, pdo, b.dlr,   \
+             b.pdlr, b.dropb, b.drop_tok, b.drop_cnt, b.o_pair, b.dx_pair)
   const int km = k == 1 ? 1 : (k == 2 ? 2 : 8);
-  if (vpl <= 2) { if (km == 1) CB(2, 1); else if (km == 2) CB(2, 2); else CB(2, 8); }
-  else if (vpl <= 4) { if (km == 1) CB(4, 1); else if (km == 2) CB(4, 2); else CB(4, 8); }
-  else { if (km == 1) CB(8, 1); else if (km == 2) CB(8, 2); else CB(8, 8); }
+  // single-GPU product path (bf16, k <= 2, no loss variants, no peer buffers): the lean
+  // instantiation, <= 4 vectors per lane per pass (the same per-lane order of the dot
+  // products as one wider pass), NL = ceil(n / 64)
+  const bool lean = sizeof(T) == 2 && km <= 2 && !b.dspec && !b.dw_ext && !b.bal_g &&
+                    !po.nl && !pdo.nl && !b.pdlr.nl;
+  if (lean) {
+    const int nl = n <= 64 ? 1 : (n <= 128 ? 2 : 4);
+#define CBL(V, K)                                                            \
+    {                                                                        \
+      if (nl == 1) CB(V, K, 1, false);                                       \
+      else if (nl == 2) CB(V, K, 2, false);                                  \
+      else CB(V, K, 4, false);                                               \
+    }
+    if (km == 2) CBL(2, 2)  // (2 vectors per lane per pass: no spills at k = 2)
+    else if (vpl <= 2) CBL(2, 1)
+    else CBL(4, 1)
+#undef CBL
+    return cudaGetLastError();
+  }
+  if (vpl <= 2) { if (km == 1) CB(2, 1, 4, true); else if (km == 2) CB(2, 2, 4, true); else CB(2, 8, 4, true); }
+  else if (vpl <= 4) { if (km == 1) CB(4, 1, 4, true); else if (km == 2) CB(4, 2, 4, true); else CB(4, 8, 4, true); }
+  else { if (km == 1) CB(8, 1, 4, true); else if (km == 2) CB(8, 2, 4, true); else CB(8, 8, 4, true); }
 #undef CB
   return cudaGetLastError();
 }
@@ -946,12 +1016,6 @@ cudaError_t launch_combine_bwd(int dtype, const void* dy, const void* obuf, Rout
                                const int32_t* pad_kept, cudaStream_t s, int pad_e0,
                                const PeerBufs& po, const PeerBufs& pdo) {
   if (T == 0 && !(pad_kept && pdo.nl)) return cudaSuccess;  // peer EP: own pads still zeroed
-  if (dtype == 1) {  // bulk-copy staged form when it applies (bitwise equal, see its header)
-    const cudaError_t e = launch_combine_bwd_bulk(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf,
-                                                  dlb, maxT, n_pad, pad_kept, s, pad_e0, po, pdo);
-    if (e != cudaErrorNotSupported) return e;
-    cudaGetLastError();  // clear a sticky "not supported" from the attribute call, if any
-  }
   if (dtype == 1)
     return combine_bwd_t<__nv_bfloat16>(dy, obuf, b, T, k, n, d_out, renorm, ct, dobuf, dlb,
                                         maxT, n_pad, pad_kept, s, pad_e0, po, pdo);

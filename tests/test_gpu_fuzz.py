@@ -26,7 +26,7 @@ def _cases():
         alpha = float(rng.choice([0.25, 0.5, 1.0, 1.25, 2.0, 7.0]))
         renorm = int(rng.integers(0, 2))
         regime = str(rng.choice(["uniform", "skewed", "ties"]))
-        fusion = int(rng.choice([0, 2, 4, 6, 7]))
+        fusion = int(rng.choice([0, 2, 4, 14, 15]))
         out.append((dtype, n, k, d, f, d_out, T, alpha, renorm, regime, fusion))
     return out
 
@@ -85,7 +85,7 @@ def _feature_cases():
         cached = float(rng.choice([-1.0, 0.0, 0.03, 0.5]))   # -1: caching off
         lam = float(rng.choice([0.0, 0.0, 0.3]))
         spec = bool(rng.integers(0, 2))
-        fusion = int(rng.choice([0, 6, 7]))
+        fusion = int(rng.choice([0, 14, 15]))
         a1, a2 = (float(v) for v in rng.choice([0.5, 1.0, 1.5, 3.0], 2))
         out.append((dtype, n, k, d, f, T, renorm, cached, lam, spec, fusion, a1, a2))
     return out

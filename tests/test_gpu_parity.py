@@ -182,6 +182,8 @@ def test_determinism(dtype):
     ("f32", 2, 64, 64, 1, 0),
     ("bf16", 1, 128, 256, 0, 6),   # fused dispatch backward (+ drop-only pass) accumulating
     ("bf16", 2, 128, 256, 1, 0),   # 2-CTA GEMMs, db1 from DGRAD_A, unfused gate-dx
+    ("bf16", 1, 128, 256, 0, 14),  # default flags: + O in token order
+    ("bf16", 2, 128, 256, 1, 8),   # k = 2, O in token order (separate combine)
 ])
 def test_accumulate_gradients(dtype, k, d, f, renorm, fusion):
     n, T = 8, 520
