@@ -492,14 +492,28 @@ def run_ours(args):
             else:
                 ach = amt / (avg_ms / 1e3) / 1e12
                 tc = layer.tdtype == torch.bfloat16 and getattr(layer, "uses_tcgen05", False)
+                tf = layer.tdtype == torch.float32 and getattr(layer, "uses_tf32", False)
                 # the burst peak applies while the clock holds its maximum through the timed
                 # region (a short region from a rested GPU); the sustained one otherwise
-                peak = (pk["bf16"] if at_max_clock else pk["bf16_sus"]) if tc else sm_peak_tf
-                ent.update(bound="tensor" if tc else "alu", achieved=round(ach, 2), peak=round(peak, 1),
-                           unit="TFLOP/s", frac=round(ach / peak, 4), algorithmic=amt)
+                bpk = pk["bf16"] if at_max_clock else pk["bf16_sus"]
+                if tc:
+                    peak = bpk
+                elif tf:
+                    # fp32 GEMMs as split-tf32 on the tensor cores: the tf32 dense peak is the
+                    # measured bf16 peak x the guide's nominal ratio (1.1 / 2.25 PF), and every
+                    # fp32 product costs 4 tf32 MMAs -> effective fp32 peak = tf32 peak / 4
+                    peak = bpk * (1.1 / 2.25) / 4
+                else:
+                    peak = sm_peak_tf
+                ent.update(bound="tensor" if (tc or tf) else "alu", achieved=round(ach, 2),
+                           peak=round(peak, 1), unit="TFLOP/s", frac=round(ach / peak, 4),
+                           algorithmic=amt)
                 if tc:
                     ent.update(frac_burst=round(ach / pk["bf16"], 4),
                                frac_sustained=round(ach / pk["bf16_sus"], 4))
+                if tf:
+                    ent.update(peak_note="tf32 peak (measured bf16 x 1.1/2.25) / 4 MMAs per fp32 "
+                                         "product (split-tf32)")
         kernels[name] = ent
     tot_k = sum(v[1] for v in ktimes.values()) or 1.0
     for name, (cnt, tot) in ktimes.items():

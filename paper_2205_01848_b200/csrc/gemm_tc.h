@@ -62,4 +62,18 @@ moe_status_t tc_ffn_backward(TcPlan* p, void* X, void* H, void* dO, void* dX, co
                              int64_t* nlaunch, Prof* prof, uint32_t* mask, float* bias_part,
                              const TcFusion* fz = nullptr);
 
+// fp32 path (c1 / c2): the same expert GEMMs on tcgen05 kind::tf32 with 3xTF32 operand
+// splitting (gemm_tf32.cu): fp32 buffers, bias / db fused as in the bf16 1-CTA kernels.
+bool tf32_supported(int d, int f, int dout);   // d, f, d_out multiples of 32
+moe_status_t tf32_ffn_forward(void* X, const void* w1, const void* b1, const void* w2,
+                              const void* b2, void* H, void* O, int64_t rows, int d, int f,
+                              int dout, const int32_t* kept, const int32_t* mtile_prefix,
+                              int n_local, const CapTable& ct, cudaStream_t s, int64_t* nlaunch,
+                              Prof* prof);
+moe_status_t tf32_ffn_backward(void* X, void* H, void* dO, void* dX, const void* w1,
+                               const void* w2, void* dw1, void* db1, void* dw2, void* db2,
+                               int accumulate, int64_t rows, int d, int f, int dout,
+                               const int32_t* kept, const int32_t* mtile_prefix, int n_local,
+                               const CapTable& ct, cudaStream_t s, int64_t* nlaunch, Prof* prof);
+
 }  // namespace moe

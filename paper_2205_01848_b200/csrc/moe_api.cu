@@ -71,6 +71,7 @@ struct moe_ctx {
   moe_fwd_args_t fa{};
   int64_t launches = 0;
   int use_tc = 0;             // tcgen05 path for bf16 (env MOE_FORCE_SIMT=1 disables)
+  int use_tf32 = 0;           // fp32: expert GEMMs on tcgen05 kind::tf32 (3xTF32), else SIMT
   int fusion = MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK;  // N2 (moe_set_fusion; GATHER opt-in)
   int fused_gather = 0;       // the last forward gathered x rows in the GEMMs (no X buffer)
   int peer_ret = 0;           // peer EP: O / dX rows returned by the GEMM epilogues (N1)
@@ -314,6 +315,7 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
   h->stream = (cudaStream_t)c.stream;
   const char* fs = getenv("MOE_FORCE_SIMT");
   h->use_tc = (c.dtype == MOE_BF16) && !(fs && fs[0] == '1');
+  h->use_tf32 = (c.dtype == MOE_F32) && !(fs && fs[0] == '1') && tf32_supported(h->d, h->f, dout);
 
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -662,6 +664,12 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
                                      (cached && fcomb) ? +wait_gate : nullptr, &join);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 forward failed");
+  } else if (h->use_tf32) {
+    int64_t nk = 0;
+    moe_status_t st = tf32_ffn_forward(X, w1, b1, w2, b2, H, O, h->rows, d, f, dout, kept_local,
+                                       rb.mtile_prefix, nl, h->ct, sd, &nk, &h->prof);
+    h->launches += nk;
+    if (st != MOE_OK) return fail(h, st, "tcgen05 tf32 forward failed");
   } else {
     KL(h, 1, "ffn_gemm1", sd, launch_gemm_simt_mgroup(dt, X, d, w1, 1, (int64_t)f * d, b1, H, f, f, d, kept_local,
                                      nl, h->ct, h->max_cap_local, EPI_BIAS_RELU, sd));
@@ -848,6 +856,13 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                                       (h->fused_gather || fdx || fdx_ep || (peer && h->peer_ret)) ? &fz : nullptr);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 backward failed");
+  } else if (h->use_tf32) {
+    int64_t nk = 0;
+    moe_status_t st = tf32_ffn_backward(X, H, dO, dXb, w1, w2, dw1, db1, dw2, db2, acc, h->rows,
+                                        d, f, dout, kept_local, rb.mtile_prefix, nl, h->ct, s0,
+                                        &nk, &h->prof);
+    h->launches += nk;
+    if (st != MOE_OK) return fail(h, st, "tcgen05 tf32 backward failed");
   } else {
     // B3a: dW2_e = dO_e^T H_e ; db2 = sum dO   (before H is overwritten by dA)
     if (dw2) KL(h, 1, "wgrad_w2", s0, launch_gemm_simt_kgroup(dt, dO, dout, H, f, dw2, dout, f, kept_local, nl, h->ct, acc, s0));

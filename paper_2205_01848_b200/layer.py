@@ -52,6 +52,9 @@ class MoELayer:
         import os
         # bf16 layers run the expert FFN and gate contractions on tcgen05 tensor cores
         self.uses_tcgen05 = dtype == "bf16" and os.environ.get("MOE_FORCE_SIMT", "0") != "1"
+        # fp32: expert GEMMs on tcgen05 kind::tf32 with split operands (gemm_tf32.cu)
+        self.uses_tf32 = (dtype == "f32" and os.environ.get("MOE_FORCE_SIMT", "0") != "1"
+                          and d_model % 32 == 0 and d_ff % 32 == 0 and (d_out or d_model) % 32 == 0)
         cfg = L.MoEConfig(n_experts, top_k, d_model, d_ff, d_out, max_tokens, L.DTYPES[dtype],
                           int(renormalize), world_size, rank, C.c_void_p(nccl_comm),
                           C.c_void_p(self._stream()), L.TRANSPORTS[transport], 0,
