@@ -688,10 +688,12 @@ cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, 
 #ifndef MOE_CB_MINB
 #define MOE_CB_MINB 4  // resident 256-thread blocks per SM (register budget 64)
 #endif
-// NL = expert pairs per lane (n <= 64 NL); FULL = the loss-variant / EP features (spec
-// gradients, balance term, peer buffers, pad zeroing) compiled in, else they are off (the
-// single-GPU product path: fewer registers and instructions, same arithmetic)
-template <typename T, int VPL, int KM, int NL, bool FULL>
+// NL = expert pairs per lane (n <= 64 NL); FEAT bit 0 (LOSS) = the loss-variant inputs (spec
+// gradients, external dw, balance term), bit 1 (PEER) = peer-EP buffers (O / dO / dl rows at
+// the experts' owners, pad zeroing of the owner's regions).  Features off are compiled out:
+// fewer registers and instructions, same arithmetic; without LOSS the first block of the dy
+// and (token-ordered) O rows is requested before the routing tables.
+template <typename T, int VPL, int KM, int NL, int FEAT>
 __global__ void __launch_bounds__(256, MOE_CB_MINB) combine_bwd_kernel(
     const T* __restrict__ dy, const T* __restrict__ obuf, const float* __restrict__ w,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of,
@@ -704,12 +706,13 @@ __global__ void __launch_bounds__(256, MOE_CB_MINB) combine_bwd_kernel(
     PeerBufs pdo, __nv_bfloat16* __restrict__ dlr, PeerBufs pdlr, __nv_bfloat16* __restrict__ dropb,
     int32_t* __restrict__ drop_tok, int32_t* __restrict__ drop_cnt, int o_pair, int dx_pair) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
-  const T* dspec = FULL ? dspec_ : nullptr;
-  const float* dw_ext = FULL ? dw_ext_ : nullptr;
-  const float* bal_g = FULL ? bal_g_ : nullptr;
+  constexpr bool LOSS = (FEAT & 1) != 0, PEER = (FEAT & 2) != 0;
+  const T* dspec = LOSS ? dspec_ : nullptr;
+  const float* dw_ext = LOSS ? dw_ext_ : nullptr;
+  const float* bal_g = LOSS ? bal_g_ : nullptr;
   // peer EP (N1): O rows are read from, and dO rows written to, the experts' owners
   if (pad_kept)
-    zero_pads_block(dobuf, dout, pad_kept, ct, (FULL && pdo.nl) ? pdo.nl : n, pad_e0, blockIdx.x,
+    zero_pads_block(dobuf, dout, pad_kept, ct, (PEER && pdo.nl) ? pdo.nl : n, pad_e0, blockIdx.x,
                     gridDim.x);
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -724,7 +727,7 @@ __global__ void __launch_bounds__(256, MOE_CB_MINB) combine_bwd_kernel(
   // order -- of the O rows.
   uint4 g[VPL];
   uint4 u[KM][VPL];
-  if (!FULL) {
+  if (!LOSS) {
 #pragma unroll
     for (int jv = 0; jv < VPL; ++jv) {
       const int v = jv * 32 + lane;
@@ -770,9 +773,9 @@ __global__ void __launch_bounds__(256, MOE_CB_MINB) combine_bwd_kernel(
       if (o_pair) osrc[r] = obuf + ((size_t)t * k + r) * dout;
       if (rows[r] >= 0) {
         if (!o_pair)
-          osrc[r] = FULL ? peer_row(obuf, po, er[r], (size_t)rows[r], dout)
+          osrc[r] = PEER ? peer_row(obuf, po, er[r], (size_t)rows[r], dout)
                          : obuf + (size_t)rows[r] * dout;
-        odst[r] = FULL ? peer_row(dobuf, pdo, er[r], (size_t)rows[r], dout)
+        odst[r] = PEER ? peer_row(dobuf, pdo, er[r], (size_t)rows[r], dout)
                        : dobuf + (size_t)rows[r] * dout;
       }
     }
@@ -788,7 +791,7 @@ __global__ void __launch_bounds__(256, MOE_CB_MINB) combine_bwd_kernel(
     dpos = __shfl_sync(0xffffffffu, dpos, 0);
   }
   for (int vb = 0; vb < nvec; vb += VPL * 32) {  // one pass for d_out*s <= 512*VPL bytes
-  const bool early = !FULL && vb == 0;  // the lean path's first block is already in flight
+  const bool early = !LOSS && vb == 0;  // the lean path's first block is already in flight
 #pragma unroll
   for (int jv = 0; jv < VPL; ++jv) {
     const int v = vb + jv * 32 + lane;
@@ -845,7 +848,7 @@ __global__ void __launch_bounds__(256, MOE_CB_MINB) combine_bwd_kernel(
                  // return rows the dX row is this rank's own (token, choice) row)
         grow[(size_t)t * k + r] = rows[r] < 0 ? -1
                                   : dx_pair ? (int)((size_t)t * k + r)
-                                  : (FULL && pdo.nl) ? rows[r] | ((er[r] / pdo.nl) << MOE_GROW_SHIFT)
+                                  : (PEER && pdo.nl) ? rows[r] | ((er[r] / pdo.nl) << MOE_GROW_SHIFT)
                                            : rows[r];
     }
   float m = -INFINITY, sp = 0.f, cb = 0.f;
@@ -956,7 +959,7 @@ __global__ void __launch_bounds__(256, MOE_CB_MINB) combine_bwd_kernel(
       *reinterpret_cast<__nv_bfloat162*>(dlb + (size_t)t * n_pad + e0) = hi;
       *reinterpret_cast<__nv_bfloat162*>(dlb + ((size_t)maxT + t) * n_pad + e0) = lo;
       if (dlr && rows[0] >= 0) {  // k = 1 fused dispatch backward: the pair by expert row
-        __nv_bfloat16* rr = FULL ? peer_row(dlr, pdlr, er[0], (size_t)rows[0], 2 * n_pad)
+        __nv_bfloat16* rr = PEER ? peer_row(dlr, pdlr, er[0], (size_t)rows[0], 2 * n_pad)
                                  : dlr + (size_t)rows[0] * 2 * n_pad;
         *reinterpret_cast<__nv_bfloat162*>(rr + e0) = hi;
         *reinterpret_cast<__nv_bfloat162*>(rr + n_pad + e0) = lo;
@@ -987,15 +990,21 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
   // single-GPU product path (bf16, k <= 2, no loss variants, no peer buffers): the lean
   // instantiation, <= 4 vectors per lane per pass (the same per-lane order of the dot
   // products as one wider pass), NL = ceil(n / 64)
-  const bool lean = sizeof(T) == 2 && km <= 2 && !b.dspec && !b.dw_ext && !b.bal_g &&
-                    !po.nl && !pdo.nl && !b.pdlr.nl;
+  const bool lean = sizeof(T) == 2 && km <= 2 && !b.dspec && !b.dw_ext && !b.bal_g;
   if (lean) {
     const int nl = n <= 64 ? 1 : (n <= 128 ? 2 : 4);
+    const bool peer = po.nl || pdo.nl || b.pdlr.nl;
 #define CBL(V, K)                                                            \
     {                                                                        \
-      if (nl == 1) CB(V, K, 1, false);                                       \
-      else if (nl == 2) CB(V, K, 2, false);                                  \
-      else CB(V, K, 4, false);                                               \
+      if (peer) {                                                            \
+        if (nl == 1) CB(V, K, 1, 2);                                         \
+        else if (nl == 2) CB(V, K, 2, 2);                                    \
+        else CB(V, K, 4, 2);                                                 \
+      } else {                                                               \
+        if (nl == 1) CB(V, K, 1, 0);                                         \
+        else if (nl == 2) CB(V, K, 2, 0);                                    \
+        else CB(V, K, 4, 0);                                                 \
+      }                                                                      \
     }
     if (km == 2) CBL(2, 2)  // (2 vectors per lane per pass: no spills at k = 2)
     else if (vpl <= 2) CBL(2, 1)
@@ -1003,9 +1012,9 @@ static cudaError_t combine_bwd_t(const void* dy, const void* obuf, RouteBufs b, 
 #undef CBL
     return cudaGetLastError();
   }
-  if (vpl <= 2) { if (km == 1) CB(2, 1, 4, true); else if (km == 2) CB(2, 2, 4, true); else CB(2, 8, 4, true); }
-  else if (vpl <= 4) { if (km == 1) CB(4, 1, 4, true); else if (km == 2) CB(4, 2, 4, true); else CB(4, 8, 4, true); }
-  else { if (km == 1) CB(8, 1, 4, true); else if (km == 2) CB(8, 2, 4, true); else CB(8, 8, 4, true); }
+  if (vpl <= 2) { if (km == 1) CB(2, 1, 4, 3); else if (km == 2) CB(2, 2, 4, 3); else CB(2, 8, 4, 3); }
+  else if (vpl <= 4) { if (km == 1) CB(4, 1, 4, 3); else if (km == 2) CB(4, 2, 4, 3); else CB(4, 8, 4, 3); }
+  else { if (km == 1) CB(8, 1, 4, 3); else if (km == 2) CB(8, 2, 4, 3); else CB(8, 8, 4, 3); }
 #undef CB
   return cudaGetLastError();
 }
