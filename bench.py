@@ -66,11 +66,12 @@ def parse():
                     help="expert-parallel exchange: peer = device-initiated through peer "
                          "memory over NVLink (N1, default); nccl = grouped send/recv")
     ap.add_argument("--fusion", choices=["none", "combine", "dx", "otok", "legacy", "default",
-                                         "all"],
+                                         "combine2", "all"],
                     default="default",
                     help="N2 fusions (k = 1): combine = y written by the second expert GEMM's "
                          "epilogue; dx = dispatch backward inside the dX GEMM; default = combine+dx+otok; "
                          "otok = O stored in (token, choice) order; legacy = combine+dx; "
+                         "combine2 = default + the k = 2 combine in the second GEMM's epilogue; "
                          "all = also gather x rows in the expert GEMMs (TMA gather4)")
     a = ap.parse_args()
     if a.emulate_padded:
@@ -306,12 +307,13 @@ def run_ours(args):
     layer.set_capacity_factors([alpha] * n, T * (ws if use_ep else 1))
     # N2 fusions (moe_set_fusion): gather x rows in the expert GEMMs, combine in FWD2 (k = 1)
     fflags = {"none": 0, "combine": 2, "dx": 4, "otok": 8, "legacy": 6, "default": 14,
-              "all": 15}[args.fusion]
+              "combine2": 30, "all": 15}[args.fusion]
     tc1 = not use_ep and cfg.dtype == "bf16" and getattr(layer, "uses_tcgen05", False)
     gather = tc1 and bool(fflags & 1) and d % 128 == 0 and f % 128 == 0
     fcomb = tc1 and bool(fflags & 2) and k == 1 and do % 128 == 0
     fdx = tc1 and bool(fflags & 4) and k == 1 and d % 128 == 0
     otok = tc1 and bool(fflags & 8) and do % 128 == 0
+    fcomb = fcomb or (otok and bool(fflags & 16) and k == 2)
     # peer EP (N1): return rows from the GEMM epilogues, and the dispatch backward in the
     # owners' dX GEMMs (k = 1)
     pret = (peer and cfg.dtype == "bf16" and getattr(layer, "uses_tcgen05", False)

@@ -385,9 +385,15 @@ MOE_API moe_status_t moe_peer_connect_nccl(moe_handle_t h, void* nccl_comm);
      expert-region order, so the combine and the combine backward read a token's O rows
      without first resolving its routing slots (the row loads issue together with the
      routing-table loads).  Bitwise equal to the expert-order layout; moe_get_routing's o_buf
-     is then [T k x d_out] in token order. */
+     is then [T k x d_out] in token order.
+   MOE_FUSE_COMBINE2 (k == 2, with MOE_FUSE_OTOK in effect, no AggregateSpec outputs): the
+     combine moves into the second GEMM's epilogue as well -- per (token, column block) a
+     counter elects the epilogue that stores its O row second (or alone, when the other
+     pair was dropped) to read both stored rows back and write y = w0 O0 + w1 O1 (the
+     combine kernel's arithmetic, bitwise equal); the counters live in the workspace and
+     reset themselves.  Opt-in (see DESIGN.md §10b for the byte count and measurement). */
 typedef enum { MOE_FUSE_GATHER = 1, MOE_FUSE_COMBINE = 2, MOE_FUSE_DX = 4,
-               MOE_FUSE_OTOK = 8 } moe_fusion_t;
+               MOE_FUSE_OTOK = 8, MOE_FUSE_COMBINE2 = 16 } moe_fusion_t;
 MOE_API moe_status_t moe_set_fusion(moe_handle_t h, int32_t flags);
 
 /* Number of kernels the library launched since the handle was created (for bench

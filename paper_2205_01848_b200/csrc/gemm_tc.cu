@@ -539,6 +539,13 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   if (comb) {
     p.y = (__nv_bfloat16*)fz->y;
     p.wt = fz->w;
+    if (fz->comb2) {  // k = 2: needs the token-ordered O of the return-row store path
+      if (!ret || fz->k != 2 || fz->pret_o.nl != 1) return MOE_ERR_CONFIG;
+      p.comb2 = 1;
+      p.slot2 = fz->slot;
+      p.ycnt = fz->ycnt;
+      p.ycb = N / (bn / 2);
+    }
   }
   if (ret) {
     p.gtos = fz->tos;

@@ -36,6 +36,11 @@ struct TcFusion {
   // token owners' windows in (token, choice) order; nl == 0 = off
   PeerBufs pret_o{}, pret_dx{};
   int tpr = 0;
+  // k = 2 combine in FWD2's epilogue (needs O in (token, choice) order, pret_o.p[0] local):
+  // slot_of [T x 2] and the per-(token, column block) counters, zero before the first forward
+  int comb2 = 0;
+  const int32_t* slot = nullptr;
+  uint32_t* ycnt = nullptr;
 };
 bool tc_gather_supported(int d, int f);     // 2-CTA kernels for FWD1 (N = f) and WGRAD_W1 (N = d)
 bool tc_combine_supported(int dout);        // 2-CTA kernel for FWD2 (N = d_out)

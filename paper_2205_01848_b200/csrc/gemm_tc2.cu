@@ -473,7 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       // N2 combine fusion (k = 1): this row's token and gate weight
       int ytok = -1;
       float yw = 0.f;
-      if (KIND == TC_FWD2 && p.y != nullptr && row_ok) {
+      if (KIND == TC_FWD2 && p.y != nullptr && !p.comb2 && row_ok) {
         ytok = p.gtos[p.ct.base[e] + row];
         yw = p.wt[ytok];
       }
@@ -650,7 +650,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
               *reinterpret_cast<float2*>(s_red + (((it & 1) * 2 + half) * 4 + q) * (CH * 32) +
                                          cc * 32 + 2 * cp) = make_float2(s0, s1);
           }
-          if (KIND == TC_FWD2 && p.y != nullptr) {
+          if (KIND == TC_FWD2 && p.y != nullptr && !p.comb2) {
             // Alg. 1 l.8 for k = 1: y[t] = 0 + w O[row] from the stored (bf16) O, the same
             // arithmetic as the combine kernel (bitwise equal).  Staged in the box buffer once
             // the O store has read it, then written as 64-byte row segments of y.
@@ -721,6 +721,80 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+      if (KIND == TC_FWD2 && p.comb2) {
+        // Alg. 1 l.8 for k = 2 (O stored in (token, choice) order above):
+        //   y[t] = 0 + w[t,0] O[t,0] + w[t,1] O[t,1]   (r order, kept pairs only)
+        // -- the combine kernel's arithmetic on the stored bf16 O rows, so bitwise equal.  A
+        // token's two rows come from different experts' tiles; per (token, column block of
+        // this warp) a self-resetting counter elects the epilogue that finishes second (or the
+        // only one, when the other pair was dropped) to read both rows back and write y.
+        // Runs after the accumulator is released, so the next tile's MMAs are not delayed.
+        constexpr int COLS = BN / 2;            // this warp's column block
+        constexpr int VPL2 = COLS / 32;         // bf16 per lane: 4 (BN 256) or 2 (BN 128)
+        const int cb0 = n0 + half * COLS;
+        int tok = -1;
+        bool both = false, mine = false;
+        if (row_ok) {
+          const int gp = p.gtos[p.ct.base[e] + row];
+          tok = gp >> 1;
+          both = p.slot2[(size_t)tok * 2 + ((gp & 1) ^ 1)] >= 0;
+        }
+        __threadfence();  // this warp's O row segments are visible before its counters
+        __syncwarp();
+        if (row_ok) {
+          if (!both) {
+            mine = true;
+          } else {
+            uint32_t* cnt = p.ycnt + (size_t)tok * p.ycb + cb0 / COLS;
+            if (atomicAdd(cnt, 1u) == 1u) {
+              mine = true;
+              *cnt = 0u;  // both arrivals seen: ready for the next forward
+            }
+          }
+        }
+        __threadfence();  // acquire: the other epilogue's O rows before they are read
+        uint32_t todo = __ballot_sync(0xffffffffu, mine);
+        const __nv_bfloat16* otok = reinterpret_cast<const __nv_bfloat16*>(p.pret.p[0]);
+        while (todo) {
+          const int l = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int tt = __shfl_sync(0xffffffffu, tok, l);
+          const int c = cb0 + lane * VPL2;
+          float acc2[VPL2];
+#pragma unroll
+          for (int i = 0; i < VPL2; ++i) acc2[i] = 0.f;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            if (p.slot2[(size_t)tt * 2 + r] < 0) continue;  // dropped pair: no contribution
+            const float wr = p.wt[(size_t)tt * 2 + r];
+            const __nv_bfloat16* src = otok + ((size_t)tt * 2 + r) * p.N + c;
+            uint32_t u[VPL2 / 2];
+            if (VPL2 == 4) {
+              const uint2 v = __ldcg(reinterpret_cast<const uint2*>(src));
+              u[0] = v.x;
+              u[VPL2 / 2 - 1] = v.y;
+            } else {
+              u[0] = __ldcg(reinterpret_cast<const unsigned int*>(src));
+            }
+#pragma unroll
+            for (int i = 0; i < VPL2 / 2; ++i) {
+              acc2[2 * i] = fmaf(wr, __uint_as_float(u[i] << 16), acc2[2 * i]);
+              acc2[2 * i + 1] = fmaf(wr, __uint_as_float(u[i] & 0xffff0000u), acc2[2 * i + 1]);
+            }
+          }
+          uint32_t o[VPL2 / 2];
+#pragma unroll
+          for (int i = 0; i < VPL2 / 2; ++i) {
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(acc2[2 * i], acc2[2 * i + 1]);
+            o[i] = *reinterpret_cast<const uint32_t*>(&b2);
+          }
+          __nv_bfloat16* dst = p.y + (size_t)tt * p.N + c;
+          if (VPL2 == 4)
+            *reinterpret_cast<uint2*>(dst) = make_uint2(o[0], o[VPL2 / 2 - 1]);
+          else
+            *reinterpret_cast<uint32_t*>(dst) = o[0];
+        }
+      }
     }
   }
   if (warp >= 4 && lane == 0) tma_store_wait_all();

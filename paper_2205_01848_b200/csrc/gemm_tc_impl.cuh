@@ -41,6 +41,13 @@ struct TcParams {
   // N2 combine fusion (FWD2, k = 1): y[t] = w[t] * O[row] written by the epilogue next to O.
   __nv_bfloat16* y;
   const float* wt;
+  // k = 2 (comb2, with O in (token, choice) order in pret.p[0]): per (token, column block) the
+  // epilogue that finishes second reads both stored O rows and writes y (counters ycnt, ycb
+  // blocks per token, self-resetting; slot2 = slot_of [T x 2] to see dropped pairs)
+  int comb2;
+  const int32_t* slot2;
+  uint32_t* ycnt;
+  int ycb;
   // N2 dispatch-backward fusion (DGRAD_X, k = 1): nkx extra k-blocks accumulate the gate term
   // dl[t] W_g (A2 = [hi | lo](dl) rows in expert-row order, B2 = W_g, nbx = n_pad / 64), and
   // the epilogue writes dx[t] (token order, via gtos) instead of the dX buffer.

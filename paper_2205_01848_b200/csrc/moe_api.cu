@@ -40,7 +40,7 @@ int moe::pdl_enabled() {
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
       xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, grow, ep_all, sendbuf, oret, dwg32,
-      pre_dev, dlr, dropb, droptok, sstat, total;
+      pre_dev, dlr, dropb, droptok, sstat, ycnt, total;
 };
 
 struct moe_ctx {
@@ -175,6 +175,8 @@ void compute_layout(moe_ctx* h) {
   L.oret = take(ep ? T * k * (size_t)h->dout * h->s : 0);
   L.dwg32 = take(ep ? n * (size_t)h->d * 4 : 0);
   L.sstat = take(h->use_tc ? T * 16 : 0);
+  // k = 2 combine in FWD2: one counter per (token, column block of <= 64 columns)
+  L.ycnt = take(h->use_tc && k == 2 && !h->use_ep ? T * (size_t)(h->dout / 64) * 4 : 0);
   L.total = o;
 }
 
@@ -456,6 +458,10 @@ moe_status_t moe_set_workspace(moe_handle_t h, void* dptr, size_t bytes) {
   bind_buffers(h);
   (void)was_set;
   CUDA_TRY(h, cudaMemsetAsync(h->ws + h->L.meta, 0, 4096, h->stream));
+  // the k = 2 combine counters reset themselves after each use: zero once per workspace
+  if (h->use_tc && h->k == 2 && !h->use_ep && h->maxT > 0)
+    CUDA_TRY(h, cudaMemsetAsync(h->ws + h->L.ycnt, 0, (size_t)h->maxT * (h->dout / 64) * 4,
+                                h->stream));
   h->have_fwd = 0;
   return MOE_OK;
 }
@@ -524,6 +530,10 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   // store with this rank as the only owner), so the combine and its backward read O by token
   // with no routing-table lookup in front of the row loads
   const bool otok = tc1 && (h->fusion & MOE_FUSE_OTOK) && tc_combine_supported(dout);
+  // k = 2: the combine in FWD2's epilogue (second epilogue of a token writes y), on top of the
+  // token-ordered O
+  const bool fcomb2 = otok && (h->fusion & MOE_FUSE_COMBINE2) && k == 2 && h->spec == nullptr &&
+                      ((uintptr_t)a->y % 16) == 0;
   h->fused_gather = gather;
   h->otok = otok;
   TcFusion fz;
@@ -542,6 +552,13 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     fz.pret_o.p[0] = (char*)O;
     fz.pret_o.nl = 1;
     fz.tpr = T;
+  }
+  if (fcomb2) {
+    fz.y = a->y;
+    fz.w = rb.w;
+    fz.comb2 = 1;
+    fz.slot = rb.slot_of;
+    fz.ycnt = (uint32_t*)(ws + h->L.ycnt);
   }
   CUDA_TRY(h, cudaMemsetAsync(rb.hit_count, 0, 4, s0));
   // softmax statistics from the tcgen05 gate for the combine backward (raw weights or the
@@ -590,7 +607,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->cts, rb,
                                                  gather ? nullptr : X, gather ? nullptr : rb.kept,
                                                  sd, 0, PeerBufs{}, PeerBufs{}, nullptr,
-                                                 fcomb ? a->y : nullptr, dout));
+                                                 (fcomb || fcomb2) ? a->y : nullptr, dout));
   } else if (h->use_peer) {
     // N1: counts exchange + global plan on the device, then the dispatch stores every kept
     // row straight into its owner's X buffer; the barrier publishes "X rows landed".
@@ -661,7 +678,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
                                      kept_local, rb.mtile_prefix, nl, h->ct, h->max_cap_local,
                                      sd, &nk, &h->prof, (uint32_t*)(ws + h->L.mask),
                                      (gather || fcomb || h->peer_ret || otok) ? &fz : nullptr,
-                                     (cached && fcomb) ? +wait_gate : nullptr, &join);
+                                     (cached && (fcomb || fcomb2)) ? +wait_gate : nullptr, &join);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 forward failed");
   } else if (h->use_tf32) {
@@ -716,7 +733,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   rb.spec = h->spec;
   rb.spec_valid = h->spec_valid;
   rb.o_pair = h->peer_ret || otok;
-  if (!fcomb)
+  if (!fcomb && !fcomb2)
     KL(h, T > 0, "combine_fwd", s0, launch_combine_fwd(dt, O_tok, rb, T, k, dout, h->cts, a->y, s0, po));
   rb.spec = nullptr;
   rb.spec_valid = nullptr;
@@ -1215,7 +1232,8 @@ moe_status_t moe_vcomm_destroy(void* comm) { return vcomm_destroy(comm); }
 
 moe_status_t moe_set_fusion(moe_handle_t h, int32_t flags) {
   if (!h) return MOE_ERR_INVALID_ARG;
-  if (flags & ~(MOE_FUSE_GATHER | MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK))
+  if (flags & ~(MOE_FUSE_GATHER | MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK |
+                MOE_FUSE_COMBINE2))
     return fail(h, MOE_ERR_INVALID_ARG, "unknown fusion flag");
   h->fusion = flags;
   return MOE_OK;

@@ -2,9 +2,10 @@
 token_of_slot with TMA gather4 (no dispatched X buffer; opt-in, flag 1); for k = 1 the second
 GEMM's epilogue writes y = w O (no combine pass, flag 2) and the dX GEMM writes
 dx = dX + dl W_g (no dispatch-backward pass, flag 4); the second GEMM stores O in (token,
-choice) order for the combine and its backward (flag 8).  Checked against the fp64 oracle
+choice) order for the combine and its backward (flag 8); for k = 2 the epilogue that stores a
+token's second O row writes y (flag 16).  Checked against the fp64 oracle
 (values within the bf16 budget, routing bit-exact) and against the unfused path of the same
-library: BITWISE equal for flags 1, 2 and 8 (same products, same accumulation order); for flag 4
+library: BITWISE equal for flags 1, 2, 8 and 16 (same products, same accumulation order); for flag 4
 every output but dx is bitwise equal and dx agrees within the bf16 budget (one rounding
 instead of two) -- including at the bench's full c3 size."""
 import numpy as np
@@ -61,7 +62,7 @@ CASES = [  # n, k, d, f, T, renorm, regime, alpha
 ]
 
 
-@pytest.mark.parametrize("fusion", [2, 3, 4, 7, 8, 14, 15])
+@pytest.mark.parametrize("fusion", [2, 3, 4, 7, 8, 14, 15, 30])
 @pytest.mark.parametrize("n,k,d,f,T,renorm,regime,alpha", CASES)
 def test_fused_vs_oracle(n, k, d, f, T, renorm, regime, alpha, fusion):
     from paper_2205_01848_b200 import capacity_from_factors
@@ -88,8 +89,8 @@ def test_fused_bitwise_equals_unfused(n, k, d, f, T, renorm, regime, alpha):
     y0, g0 = _run(layer, g, dy, 0, y_fill=float("nan"))
     assert not torch.isnan(y0).any()
     # combine, gather, both, dx, gather+combine+dx, O in token order (alone, + combine,
-    # default combine+dx+otok, all)
-    for fusion in (2, 1, 3, 4, 7, 8, 10, 14, 15):
+    # default combine+dx+otok, all), k = 2 combine in the second GEMM (alone with otok, default)
+    for fusion in (2, 1, 3, 4, 7, 8, 10, 14, 15, 24, 30):
         y1, g1 = _run(layer, g, dy, fusion, y_fill=float("nan"))
         assert not torch.isnan(y1).any()
         _bitwise(y1, y0, f"y (fusion {fusion})")
@@ -163,3 +164,30 @@ def test_fused_bitwise_at_bench_size():
         ref = float(w[t]) * o
         err = (y1[t].float() - ref).abs().max() / ref.abs().max()
         assert err < 2e-2, (t, float(err))
+
+
+@pytest.mark.parametrize("n,T,alpha,cached", [(8, 999, 1.0, False), (16, 1500, 0.7, False),
+                                               (8, 640, 1.0, True)])
+def test_k2_combine_in_gemm_bitwise(n, T, alpha, cached):
+    """k = 2 combine in the second GEMM's epilogue (flag 16): y bitwise equal to the separate
+    combine kernel, with drops (alpha < 1: tokens with one or both pairs dropped), y poisoned
+    first, two forwards in a row (the per-(token, block) counters must have reset), and in
+    cached mode (the second GEMM waits for the gate weights)."""
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer
+    k, d, f = 2, 256, 256
+    g = {kk: v.cuda() for kk, v in make_layer(n, d, f, d, T, "bf16").items()}
+    dy = make_dy(T, d, "bf16").cuda()
+    layer = MoELayer(n, k, d, f, 0, T, "bf16", 1, device="cuda")
+    layer.set_capacities(capacity_from_factors([alpha] * n, T, k))
+    if cached:
+        gen = torch.Generator(device="cpu").manual_seed(7)
+        cidx = torch.stack([torch.randperm(n, generator=gen)[:k] for _ in range(T)]).int().cuda()
+        layer.set_cached_assignment(cidx)
+    y0, g0 = _run(layer, g, dy, 14, y_fill=float("nan"))
+    for _ in range(2):
+        y1, g1 = _run(layer, g, dy, 30, y_fill=float("nan"))
+        assert not torch.isnan(y1).any()
+        _bitwise(y1, y0, "y (k = 2 combine in the GEMM)")
+        for key in g0:
+            _bitwise(g1[key], g0[key], key)
