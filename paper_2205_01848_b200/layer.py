@@ -330,6 +330,18 @@ class MoELayer:
         out["o_buf"] = view(r.o_buf, r.rows * self.d_out, self.tdtype).view(r.rows, self.d_out)
         return out
 
+    def h_snapshot(self):
+        """Copy of the H buffer (ReLU outputs of the last forward, expert-region rows of the local
+        experts) and the region bases, enqueued on the current stream without any device or
+        stream synchronisation (safe between a forward and its backward while peer ranks of
+        the same GPU wait in barrier kernels).  Test helper: the backward overwrites H."""
+        r = L.Routing()
+        L.check(self.lib.moe_get_routing(self.h, C.byref(r)), self.h)
+        off = r.h_buf - self.ws.data_ptr()
+        nbytes = r.rows * self.f * self.ws.new_empty(0, dtype=self.tdtype).element_size()
+        h = self.ws[off:off + nbytes].view(self.tdtype).view(r.rows, self.f).clone()
+        return h, list(r.base_host)[: self.n // self.world_size + 1]
+
     def stats(self):
         """Per-forward statistics (synchronises the stream): counts, drops, hit_count."""
         if self._pinned is None:

@@ -61,7 +61,7 @@ def test_ep_loopback_cached(comm):
 
 
 def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0, transport="nccl",
-                 iters=1, caps_seq=None, fusion=0):
+                 iters=1, caps_seq=None, fusion=0, keep_h=False):
     """R expert-parallel ranks as threads on one GPU -- over the library's virtual NCCL-style
     communicator, or through the peer-memory transport (N1) with in-process windows -- against
     the single-GPU layer on the concatenated batch.  iters > 1 repeats forward+backward
@@ -122,11 +122,14 @@ def _run_virtual(R, n, k, T, d, f, dtype, renorm, cached_frac=None, lam=0.0, tra
                 with torch.cuda.stream(s):
                     xs = g["x"][r * T:(r + 1) * T]
                     y = L.forward(xs, g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+                    hs = L.h_snapshot() if keep_h else None
                     gr = L.backward(dy[r * T:(r + 1) * T].contiguous())
             with torch.cuda.stream(s):
                 s.synchronize()
                 rt = L.routing(T)
                 s.synchronize()
+            if hs is not None:
+                rt["h_fwd"], rt["h_base"] = hs
             out[r] = (y, gr, rt, L.stats())
         except Exception as ex:  # surfaced in the main thread
             errs.append(ex)
@@ -363,3 +366,52 @@ def test_peer_windows_on_nccl_symmetric_memory(comm, dtype, n, k, renorm):
         assert layer.check_flags()[1] == 0
     finally:
         pl.close()   # deregisters the window while the communicator is alive
+
+
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("R", [2, 4])
+@pytest.mark.parametrize("dtype,k,renorm", [("bf16", 2, 1), ("bf16", 1, 0), ("f32", 2, 0)])
+def test_peer_virtual_ranks_vs_oracle(R, dtype, k, renorm):
+    """R > 1 expert-parallel ranks (peer transport) against the fp64 oracle DIRECTLY, not only
+    against the single-GPU layer: the oracle runs the concatenated global batch with the
+    ranks' fp32 logits (routing decisions, reading 3) and global capacities (reading 12);
+    y / dx / dl / dw per token from the token owners, dW1 / db1 / dW2 / db2 from each expert's
+    owner, dW_g from the rank-order window sum; ReLU' decisions from each owner's stored H
+    within the fp32 rounding band (checked_relu_mask)."""
+    from parity_util import TOL, checked_relu_mask, rel, rel_rows
+    n, T, d, f = 16, 512, 64, 128
+    out, _ = _run_virtual(R, n, k, T, d, f, dtype, renorm, transport="peer", keep_h=True)
+    from synth import make_dy, make_layer, to_numpy64
+    Tg, nl = R * T, n // R
+    cpu = make_layer(n, d, f, d, Tg, dtype)
+    dy64 = to_numpy64(make_dy(Tg, d, dtype))
+    x64 = to_numpy64(cpu["x"])
+    p64 = {kk: to_numpy64(v) for kk, v in cpu.items() if kk != "x"}
+    caps = O.capacities_from_factors([1.0] * n, Tg, k)
+    lg = np.concatenate([o[2]["logits"].cpu().double().numpy() for o in out])
+    st = O.moe_forward(x64, p64, k, caps, renorm, logits=lg, emulate_bf16=(dtype == "bf16"))
+    assert st.routing.drops > 0
+    assert np.array_equal(np.concatenate([o[2]["slot_of"].cpu().numpy() for o in out]),
+                          st.routing.slot_of)
+    kmask = []
+    for e in range(n):
+        rt = out[e // nl][2]
+        b = rt["h_base"][e % nl]
+        kmask.append((rt["h_fwd"][b: b + int(st.routing.kept[e])].float() > 0).cpu().numpy())
+    gr = O.moe_backward(st, dy64, relu_mask=checked_relu_mask(st, kmask, f"R={R}"))
+    got = dict(
+        y=torch.cat([o[0] for o in out]), dx=torch.cat([o[1]["dx"] for o in out]),
+        dw_gate=out[0][1]["dw_gate"],
+        **{kk: sum(o[1][kk].float() for o in out) for kk in ("dw1", "db1", "dw2", "db2")})
+    got = {kk: to_numpy64(v) for kk, v in got.items()}
+    tol = TOL[dtype]
+    errs = {"y": rel(got["y"], st.y), "w": rel(np.concatenate([o[2]["w"].cpu().numpy()
+                                                               for o in out]), st.w)}
+    for kk in ("dx", "dw_gate", "dw1", "db1", "dw2", "db2"):
+        errs[kk] = rel(got[kk], gr[kk])
+    for kk in ("dw1", "db1", "dw2", "db2"):
+        errs[kk + "/expert"] = rel_rows(got[kk], gr[kk])
+    errs["dw"] = rel(np.concatenate([o[2]["dw"].cpu().numpy() for o in out]), gr["dw"])
+    lim = {kk: (1e-5 if kk == "w" else tol) for kk in errs}
+    bad = {kk: v for kk, v in errs.items() if not v <= lim[kk]}
+    assert not bad, f"R={R} parity failures {bad} (all: {errs})"

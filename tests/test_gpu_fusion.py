@@ -191,3 +191,30 @@ def test_k2_combine_in_gemm_bitwise(n, T, alpha, cached):
         _bitwise(y1, y0, "y (k = 2 combine in the GEMM)")
         for key in g0:
             _bitwise(g1[key], g0[key], key)
+
+
+@pytest.mark.parametrize("n,k,d,T,renorm", [(64, 1, 1024, 4096, 0), (16, 2, 256, 1001, 1),
+                                             (130, 2, 128, 777, 0)])
+def test_combine_bwd_lean_equals_full(n, k, d, T, renorm):
+    """The combine backward's lean instantiation (single GPU, no loss-variant inputs: the dy /
+    O rows requested before the routing tables) against the full one (selected by passing
+    all-zero spec-row / gate-weight gradients, which add exact zeros): every output of the
+    backward bitwise equal (dl, dw, dx and all weight gradients)."""
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer
+    g = {kk: v.cuda() for kk, v in make_layer(n, d, 2 * d, d, T, "bf16").items()}
+    dy = make_dy(T, d, "bf16").cuda()
+    layer = MoELayer(n, k, d, 2 * d, 0, T, "bf16", renorm, device="cuda")
+    layer.set_capacities(capacity_from_factors([1.0] * n, T, k))
+    outs = []
+    for full in (False, True):
+        if full:
+            layer.set_spec_grads(torch.zeros(T * k, d, dtype=torch.bfloat16, device="cuda"),
+                                 torch.zeros(T, k, dtype=torch.float32, device="cuda"))
+        y, gr = _run(layer, g, dy, 14, y_fill=float("nan"))
+        r = layer.routing(T)
+        outs.append((gr, r["dl"].clone(), r["dw"].clone()))
+    (g1, dl1, dw1), (g2, dl2, dw2) = outs
+    assert torch.equal(dl1, dl2) and torch.equal(dw1, dw2)
+    for key in g1:
+        _bitwise(g2[key], g1[key], key)
