@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--cached", action="store_true", help="sample-assignment caching (c5)")
     ap.add_argument("--regime", choices=["uniform", "skewed"], default="uniform",
                     help="routing regime of the synthetic inputs (SURVEY §8(d))")
-    ap.add_argument("--capacity", choices=["static", "dynamic"], default="static",
+    ap.add_argument("--capacity", choices=["static", "dynamic"], default=None,
                     help="dynamic: the capacity policy (moe_policy_*) adapts C_e for "
                          "--policy-warmup steps before the timed region (P:221-236)")
     ap.add_argument("--policy-warmup", type=int, default=50)
@@ -78,6 +78,10 @@ def parse():
         os.environ["MOE_DBG_PAD_GEMM"] = "1"
     if a.config is None:
         a.config = "c3" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "c4"
+    if a.capacity is None:
+        # BASELINE configs[1] (c2) and configs[4] (c5) run with dynamic capacity factors on;
+        # an explicit --alpha asks for a static factor
+        a.capacity = "dynamic" if a.config in ("c2", "c5") and a.alpha is None else "static"
     return a
 
 
