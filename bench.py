@@ -692,16 +692,31 @@ def _threads():
     return len(os.sched_getaffinity(0))
 
 
+# The oracle holds fp64 copies of every expert's weights and weight gradients; for the large
+# configs (c4: 128 experts of 2 x 2048 x 8192) that is ~70 GB, so above 12 GB the host sample uses
+# the first n_sub experts with the per-expert load of the full layer (tokens scaled by
+# n_sub / n).  Per token the oracle's work is the same up to the gate (6 d n of 12 k d f FLOPs,
+# 0.4 % at c4), so tokens/s of the sub-layer stands for the full layer's.
+ORACLE_WEIGHT_BYTES = 12 << 30
+
+
+def oracle_expert_sample(n, d, f, do, k):
+    per = (f * d + do * f) * 8 * 2          # fp64 weights + their gradients, one expert
+    return max(k, min(n, ORACLE_WEIGHT_BYTES // per))
+
+
 def cpu_oracle_sample(cfg, g, dy, tokens, alpha):
     """The fp64 oracle, as it stands, on a bounded sample of the same workload."""
     import numpy as np
     from oracle import moe_oracle as O
     from synth import to_numpy64
     n, k = cfg.n_experts, cfg.top_k
-    Ts = min(tokens, g["x"].shape[0])
+    ns = oracle_expert_sample(n, cfg.d_model, cfg.d_ff, cfg.d_out, k)
+    Ts = min(tokens, g["x"].shape[0]) * ns // n
     x = to_numpy64(g["x"][:Ts])
-    p = {kk: g[kk].detach().to("cpu", dtype=__import__("torch").float64).numpy()
+    p = {kk: g[kk][:ns].detach().to("cpu", dtype=__import__("torch").float64).numpy()
          for kk in ("w_gate", "w1", "b1", "w2", "b2")}
+    n_all, n = n, ns
     dyn = to_numpy64(dy[:Ts])
     caps = O.capacities_from_factors([alpha] * n, Ts, k)
     t0 = time.perf_counter()
@@ -709,7 +724,10 @@ def cpu_oracle_sample(cfg, g, dy, tokens, alpha):
     O.moe_backward(st, dyn)
     dt = time.perf_counter() - t0
     out = {"value": round(Ts / dt, 2), "unit": "tokens/s", "cores": _threads(), "kind": "oracle",
-           "sample": f"{Ts} tokens of {cfg.name} (all {n} experts, alpha {alpha}), fwd+bwd, fp64 NumPy",
+           "sample": (f"{Ts} tokens of {cfg.name} (all {n} experts, alpha {alpha}), fwd+bwd, fp64 NumPy"
+                      if n == n_all else
+                      f"{Ts} tokens over {n} of {cfg.name}'s {n_all} experts (the full layer's "
+                      f"per-expert load), alpha {alpha}, fwd+bwd, fp64 NumPy"),
            "seconds": round(dt, 2)}
     try:  # the same oracle on one core (BLAS limited to one thread), a quarter of the sample
         from threadpoolctl import threadpool_limits
@@ -735,11 +753,18 @@ def run_reference(args):
         return
     import numpy as np
     import torch
+    try:  # torchrun sets OMP_NUM_THREADS=1: give the BLAS (loaded with numpy) every host core
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=len(os.sched_getaffinity(0)))
+    except Exception:
+        pass
     from oracle import moe_oracle as O
     from synth import get_config, make_dy, make_layer, to_numpy64
     cfg = get_config(args.config)
     alpha = args.alpha if args.alpha is not None else cfg.alpha
     n, k, d, f, do = cfg.n_experts, cfg.top_k, cfg.d_model, cfg.d_ff, cfg.d_out
+    n_all = n
+    n = oracle_expert_sample(n, d, f, do, k)   # bounded host memory (see ORACLE_WEIGHT_BYTES)
     # per-step sample: as large as the cpu_baseline sample (--cpu-sample) while the whole
     # K + W run stays within ~150 s of host time, calibrated by one 1024-token step (the
     # oracle has a large per-step fixed cost -- full-size fp64 weight gradients -- so small
@@ -776,10 +801,15 @@ def run_reference(args):
            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(dt * 1e3 / args.steps, 2), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"{cfg.name}: {n} experts top-{k}, d_model {d}, d_ff {f}, "
-                                  f"{Ts} tokens/step sample, alpha {alpha}"},
+           "config": {"workload": f"{cfg.name}: {n_all} experts top-{k}, d_model {d}, d_ff {f}, "
+                                  f"{Ts} tokens/step sample"
+                                  + ("" if n == n_all else
+                                     f" over {n} of the {n_all} experts (per-expert load of the "
+                                     f"full layer)") + f", alpha {alpha}"},
            "cpu_baseline": {"value": round(val, 2), "unit": "tokens/s", "cores": _threads(),
-                            "kind": "oracle", "sample": f"{Ts} tokens per step of {cfg.name}"},
+                            "kind": "oracle",
+                            "sample": f"{Ts} tokens per step of {cfg.name}"
+                                      + ("" if n == n_all else f" over {n} of {n_all} experts")},
            "e2e": {"value": round(val, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
