@@ -685,16 +685,13 @@ cudaError_t launch_combine_fwd(int dtype, const void* obuf, RouteBufs b, int T, 
 // raw dl_j = p_j (dp_j - sum_r w_r dw_r) with dp_j = dw_r at j = i_r.  Warp per token; the
 // logits, dy and O rows are all requested before the first use.
 // =====================================================================================
-#ifndef MOE_CB_MINB
-#define MOE_CB_MINB 4  // resident 256-thread blocks per SM (register budget 64)
-#endif
 // NL = expert pairs per lane (n <= 64 NL); FEAT bit 0 (LOSS) = the loss-variant inputs (spec
 // gradients, external dw, balance term), bit 1 (PEER) = peer-EP buffers (O / dO / dl rows at
 // the experts' owners, pad zeroing of the owner's regions).  Features off are compiled out:
 // fewer registers and instructions, same arithmetic; without LOSS the first block of the dy
 // and (token-ordered) O rows is requested before the routing tables.
 template <typename T, int VPL, int KM, int NL, int FEAT>
-__global__ void __launch_bounds__(256, MOE_CB_MINB) combine_bwd_kernel(
+__global__ void __launch_bounds__(256, 4) combine_bwd_kernel(
     const T* __restrict__ dy, const T* __restrict__ obuf, const float* __restrict__ w,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ slot_of,
     const float* __restrict__ logits, CapTable ct, int Tn, int k, int n, int dout, int renorm,
