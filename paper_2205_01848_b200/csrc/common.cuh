@@ -149,7 +149,28 @@ __device__ __forceinline__ void pdl_enter() {
   pdl_wait();
   pdl_trigger();
 }
+// nowait: the kernel's inputs all come from kernels at least two launches back (complete once
+// its predecessor started, PDL order), so it skips the wait and can run beside the tail of its
+// predecessor; the launcher guarantees a full-dependency (non-PDL) launch closes the sequence.
+__device__ __forceinline__ void pdl_enter(int nowait) {
+  if (!nowait) pdl_wait();
+  pdl_trigger();
+}
 int pdl_enabled();  // host: env MOE_PDL (default 1; 0 = plain stream serialisation)
+
+// A launch with full stream dependency (no PDL attribute): starts after ALL earlier work in
+// the stream has completed, including kernels that ran without a PDL wait.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_full(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                               cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.numAttrs = 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,

@@ -60,6 +60,7 @@ struct GateDxParams {
                                // (dx = dl W_g); the others were written by the dX GEMM
   const int32_t* drop_tok;     // drop_only: [count] token of each compacted dropped row
   const int32_t* drop_cnt;     // drop_only: [1] number of dropped tokens (combine_bwd)
+  int nowait;                  // inputs complete before the predecessor started: no PDL wait
 };
 
 // dX row of a gather-table entry (peer EP: owner in the top bits, see MOE_GROW_SHIFT)
@@ -79,6 +80,7 @@ __device__ __forceinline__ const __nv_bfloat16* gdx_row(const GateDxParams& p, i
 struct GateDwParams {
   int T, n, d, chunk, splits;
   float* partial;  // [splits x n x d]
+  int nowait;      // inputs complete before the predecessor started: skip the PDL wait
 };
 
 // --------------------------------------------------------------------------------------
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(GX_THREADS, 1)
     gate_dx_tc_kernel(const __grid_constant__ CUtensorMap tmHi,
                       const __grid_constant__ CUtensorMap tmLo,
                       const __grid_constant__ CUtensorMap tmW, GateDxParams p) {
-  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
+  pdl_enter(p.nowait);  // PDL: predecessor complete + visible (common.cuh)
   constexpr int A_BYTES = TC_BM * TC_BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + BN * TC_BK * 2;
   constexpr uint32_t IDESC = make_idesc(BN, 0, 1);
@@ -644,7 +646,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     gate_dw_tc_kernel(const __grid_constant__ CUtensorMap tmHi,
                       const __grid_constant__ CUtensorMap tmLo,
                       const __grid_constant__ CUtensorMap tmX, GateDwParams p) {
-  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
+  pdl_enter(p.nowait);  // PDL: predecessor complete + visible (common.cuh)
   constexpr int A_BYTES = TC_BM * TC_BK * 2;  // one of hi / lo
   constexpr int STAGE_BYTES = 2 * A_BYTES + BN * TC_BK * 2;
   constexpr uint32_t IDESC = make_idesc(BN, 1, 1);
@@ -848,7 +850,7 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
 cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb, int maxT,
                               int n_pad, RouteBufs b, int T, int k, int n, int d,
                               const CapTable& ct, void* dx, int accumulate, cudaStream_t s,
-                              const PeerBufs& pdx, int drop_only) {
+                              const PeerBufs& pdx, int drop_only, bool nowait) {
   if (T == 0) return cudaSuccess;
   if (!enc_init()) return cudaErrorNotSupported;
   CUtensorMap mhi, mlo, mw;
@@ -865,6 +867,7 @@ cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb
   p.drop_only = drop_only;
   p.drop_tok = b.drop_tok;
   p.drop_cnt = b.drop_cnt;
+  p.nowait = (nowait && drop_only) ? 1 : 0;  // the drop-only pass reads nothing of the dX GEMM
   const int bn = d % 128 == 0 ? 128 : 64;
   const int total = ((T + 127) / 128) * (d / bn);
   const int grid = total < g_sms ? total : g_sms;
@@ -893,7 +896,7 @@ int gate_dw_tc_splits(int T, int n, int d) {
 
 cudaError_t launch_gate_dw_tc(const void* dlb, int maxT, int n_pad, const void* x, int T, int n,
                               int d, float* partial, void* dwg, int accumulate, cudaStream_t s,
-                              float* f32_out) {
+                              float* f32_out, bool nowait) {
   const size_t count = (size_t)n * d;
   if (f32_out && T == 0) return cudaMemsetAsync(f32_out, 0, count * 4, s);
   if (T == 0) {
@@ -911,7 +914,7 @@ cudaError_t launch_gate_dw_tc(const void* dlb, int maxT, int n_pad, const void* 
   if (!map2d(&mhi, hi, n_pad, T, 64, 64) || !map2d(&mlo, lo, n_pad, T, 64, 64) ||
       !map2d(&mx, x, d, T, 64, 64))
     return cudaErrorInvalidValue;
-  GateDwParams p{T, n, d, chunk, splits, partial};
+  GateDwParams p{T, n, d, chunk, splits, partial, nowait ? 1 : 0};
   const int bn = d % 256 == 0 ? 256 : (d % 128 == 0 ? 128 : 64);
   const int total = splits * ((n + 127) / 128) * (d / bn);
   const int grid = total < g_sms ? total : g_sms;
@@ -928,7 +931,9 @@ cudaError_t launch_gate_dw_tc(const void* dlb, int maxT, int n_pad, const void* 
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (f32_out) return launch_reduce_partials(0, partial, splits, count, f32_out, 0, s);
-  return launch_reduce_partials(1, partial, splits, count, dwg, accumulate, s);
+  // nowait: the reduction closes the backward with a full-dependency launch (it also waits for
+  // every kernel that skipped its PDL wait)
+  return launch_reduce_partials(1, partial, splits, count, dwg, accumulate, s, nowait);
 }
 
 }  // namespace moe

@@ -11,9 +11,14 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
 cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb, int maxT,
                               int n_pad, RouteBufs b, int T, int k, int n, int d,
                               const CapTable& ct, void* dx, int accumulate, cudaStream_t s,
-                              const PeerBufs& pdx = PeerBufs{}, int drop_only = 0);
+                              const PeerBufs& pdx = PeerBufs{}, int drop_only = 0,
+                              bool nowait = false);
 cudaError_t launch_gate_dw_tc(const void* dlb, int maxT, int n_pad, const void* x, int T, int n,
                               int d, float* partial, void* dwg, int accumulate, cudaStream_t s,
-                              float* f32_out = nullptr);
+                              float* f32_out = nullptr, bool nowait = false);
+// nowait (single GPU, backward tail): the drop-only gate-dx pass and the gate-weight
+// gradient skip their PDL wait (their inputs are complete before their predecessor started)
+// and run beside the dX GEMM's tail; the gate-weight reduction then closes the backward with
+// a full-dependency launch.
 int gate_dw_tc_splits(int T, int n, int d);
 }  // namespace moe

@@ -457,8 +457,9 @@ bool tc_peer_return_supported(int d, int dout) {
 // db[e][c] = sum of the DGRAD_A column-sum partials of expert e, fixed order (deterministic).
 __global__ void bias_part_reduce_kernel(const float* __restrict__ part,
                                         const int32_t* __restrict__ kept, int N,
-                                        __nv_bfloat16* __restrict__ db, int accumulate) {
-  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
+                                        __nv_bfloat16* __restrict__ db, int accumulate,
+                                        int nowait) {
+  pdl_enter(nowait);  // PDL (nowait: launched after the dX GEMM, DGRAD_A long complete)
   const int e = blockIdx.y;
   __shared__ int s_pre, s_mt;
   if (threadIdx.x < 32) {
@@ -646,7 +647,7 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
                              const int32_t* kept, const int32_t* mtile_prefix, int n_local,
                              const CapTable& ct, int max_cap, cudaStream_t s,
                              int64_t* nlaunch, Prof* prof, uint32_t* mask, float* bias_part,
-                             const TcFusion* fz) {
+                             const TcFusion* fz, int tail_nowait) {
   (void)plan; (void)max_cap;
   // db1 from the DGRAD_A epilogue (2-CTA) instead of the weight-gradient bias warps
   const bool db1_in_dgrad = db1 && bias_part && use_2cta(f, TC_DGRAD_A);
@@ -672,12 +673,19 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   }
   if (st != MOE_OK) return st;
   ++nl;
-  if (db1_in_dgrad) {
+  // db1 partials -> db1: right here, or (tail_nowait) after the dX GEMM without a PDL wait,
+  // beside that GEMM's tail (nothing in between touches the partials or db1)
+  auto db1_reduce = [&](int nowait) -> moe_status_t {
     ProfScope ps(prof, "bias_grad", s);
-    launch_pdl(bias_part_reduce_kernel, dim3((f + 255) / 256, n_local), 256, 0, s, 
-        bias_part, kept, f, (__nv_bfloat16*)db1, accumulate);
+    launch_pdl(bias_part_reduce_kernel, dim3((f + 255) / 256, n_local), 256, 0, s,
+               bias_part, kept, f, (__nv_bfloat16*)db1, accumulate, nowait);
     TC_CUDA(cudaGetLastError());
     ++nl;
+    return MOE_OK;
+  };
+  if (db1_in_dgrad && !tail_nowait) {
+    st = db1_reduce(0);
+    if (st != MOE_OK) return st;
   }
   if (dw1) {  // dW1_e = dA_e^T X_e (db1 fused here only when not produced by DGRAD_A)
     ProfScope ps(prof, "wgrad_w1", s);
@@ -698,6 +706,10 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   }
   if (st != MOE_OK) return st;
   ++nl;
+  if (db1_in_dgrad && tail_nowait) {
+    st = db1_reduce(1);
+    if (st != MOE_OK) return st;
+  }
   *nlaunch = nl;
   return MOE_OK;
 }

@@ -97,7 +97,8 @@ cudaError_t launch_f32_to(int dtype, const float* in, size_t count, void* out, i
                           cudaStream_t s);
 int gate_dw_splits(int T, int d);
 cudaError_t launch_reduce_partials(int dtype, const float* partial, int splits, size_t count,
-                                   void* out, int accumulate, cudaStream_t s);
+                                   void* out, int accumulate, cudaStream_t s,
+                                   bool full_dep = false);
 cudaError_t launch_colsum(int dtype, const void* buf, int cols, const int32_t* kept, int n,
                           const CapTable& ct, void* out, int accumulate, cudaStream_t s);
 

@@ -846,6 +846,14 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
       if (hi < (size_t)n) CUDA_TRY(h, cudaMemsetAsync(base + per[q] * hi, 0, per[q] * (n - hi), s0));
     }
   }
+  // Backward tail (single GPU, fused dispatch backward, dW_g requested): the db1 reduction, the
+  // drop-only gate-dx pass and the gate-weight gradient read only data of kernels that are
+  // complete once the dX GEMM has started, so they skip their PDL wait and run beside that
+  // GEMM's tail and each other; the gate-weight reduction closes the backward with a
+  // full-dependency launch (every later kernel again sees all of this step complete).
+  static const bool tail_env = !(getenv("MOE_TAIL") && getenv("MOE_TAIL")[0] == '0');
+  const bool tail = tail_env && !h->use_ep && h->use_tc && T > 0 && a->dw_gate != nullptr &&
+                    (fdx || a->dx == nullptr);
   if (h->use_tc) {
     int64_t nk = 0;
     TcFusion fz;  // N2: dW1 = dA^T X gathers the x rows like the forward did
@@ -870,7 +878,8 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                                       h->rows, d, f, dout, kept_local, rb.mtile_prefix, nl,
                                       h->ct, h->max_cap_local, s0, &nk, &h->prof,
                                       (uint32_t*)(ws + h->L.mask), (float*)(ws + h->L.bpart),
-                                      (h->fused_gather || fdx || fdx_ep || (peer && h->peer_ret)) ? &fz : nullptr);
+                                      (h->fused_gather || fdx || fdx_ep || (peer && h->peer_ret)) ? &fz : nullptr,
+                                      tail ? 1 : 0);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 backward failed");
   } else if (h->use_tf32) {
@@ -904,7 +913,8 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   auto gate_dw_partial = [&]() -> moe_status_t {
     if (h->use_tc) {
       KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw_tc(dlb, h->maxT, h->n_pad, fa.x, T, n, d,
-                                                            (float*)(ws + h->L.partial), a->dw_gate, acc, s0, dwg_f32));
+                                                            (float*)(ws + h->L.partial), a->dw_gate, acc, s0,
+                                                            dwg_f32, tail));
     } else {
       int splits = gate_dw_splits(h->maxT, d);
       KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw(dt, rb.dl, fa.x, T, n, d, (float*)(ws + h->L.partial),
@@ -938,7 +948,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
       KL(h, T > 0, "gate_dx", s0, launch_gate_dx_tc(fa.w_gate, dX_tok,
                                                     drop_only ? (void*)(ws + h->L.dropb) : dlb,
                                                     h->maxT, h->n_pad, rb, T, k, n, d, h->cts,
-                                                    a->dx, acc, s0, pdx, drop_only ? 1 : 0));
+                                                    a->dx, acc, s0, pdx, drop_only ? 1 : 0, tail));
     else
       KL(h, T > 0, "gate_dx", s0, launch_gate_dx(dt, fa.w_gate, dX_tok, rb, T, k, n, d, h->cts, a->dx, acc, s0,
                                                  pdx));

@@ -1214,7 +1214,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ partial,
                                                               int splits, size_t count,
                                                               T* __restrict__ out, int accumulate) {
-  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
+  pdl_enter();  // PDL: predecessor complete + visible (a no-op for a full-dependency launch)
   __shared__ float sg[8][33];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const size_t i = (size_t)blockIdx.x * 32 + lane;
@@ -1242,14 +1242,17 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
 }
 
 cudaError_t launch_reduce_partials(int dtype, const float* partial, int splits, size_t count,
-                                   void* out, int accumulate, cudaStream_t s) {
+                                   void* out, int accumulate, cudaStream_t s, bool full_dep) {
   int rb = (int)((count + 31) / 32);
-  if (dtype == 1)
-    launch_pdl(reduce_partials_kernel<__nv_bfloat16>, rb, 256, 0, s, partial, splits, count,
-                                                             (__nv_bfloat16*)out, accumulate);
-  else
-    launch_pdl(reduce_partials_kernel<float>, rb, 256, 0, s, partial, splits, count, (float*)out,
-                                                     accumulate);
+  if (dtype == 1) {
+    auto kf = reduce_partials_kernel<__nv_bfloat16>;
+    if (full_dep) launch_full(kf, rb, 256, 0, s, partial, splits, count, (__nv_bfloat16*)out, accumulate);
+    else launch_pdl(kf, rb, 256, 0, s, partial, splits, count, (__nv_bfloat16*)out, accumulate);
+  } else {
+    auto kf = reduce_partials_kernel<float>;
+    if (full_dep) launch_full(kf, rb, 256, 0, s, partial, splits, count, (float*)out, accumulate);
+    else launch_pdl(kf, rb, 256, 0, s, partial, splits, count, (float*)out, accumulate);
+  }
   return cudaGetLastError();
 }
 
