@@ -502,7 +502,7 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
                            int n_local, const void* bias, void* C, int ldc, const int32_t* kept,
                            const int32_t* prefix, const CapTable& ct, cudaStream_t s,
                            uint32_t* mask = nullptr, float* bias_part = nullptr,
-                           const TcFusion* fz = nullptr) {
+                           const TcFusion* fz = nullptr, int nowait = 0) {
   CUtensorMap ma, mb;
   const int bn = pick_bn(N);
   const bool two = use_2cta(N, KIND);
@@ -564,6 +564,7 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   p.sched = tc_sched();
   p.pf_kb = tc_pf();
   p.dbg = tc_dbg();
+  p.nowait = two ? nowait : 0;  // (the 1-CTA kernel always waits)
   if (two) {
     CUtensorMap mc;
     TC_TRY(make_store_map(&mc, C, ldc, rows));
@@ -701,8 +702,11 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   // dX = dA W1_e, W1_e stored [f x d] = [K x N]
   {
     ProfScope ps(prof, "dgrad_dX", s);
+    // tail_nowait: DGRAD_X reads dA (DGRAD_A, two launches back), W1 and the fused dispatch
+    // backward's dl rows / W_g -- nothing of WGRAD_W1, which writes only dW1 -- so it skips the
+    // PDL wait and fills the SMs WGRAD_W1's last wave leaves idle
     st = mgroup<TC_DGRAD_X>(H, rows, f, w1, d, n_local, nullptr, dX, d, kept, mtile_prefix, ct, s,
-                            nullptr, nullptr, fz);
+                            nullptr, nullptr, fz, tail_nowait && dw1 != nullptr);
   }
   if (st != MOE_OK) return st;
   ++nl;

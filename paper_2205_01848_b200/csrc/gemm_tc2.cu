@@ -128,7 +128,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
                     const __grid_constant__ CUtensorMap tmB2, TcParams p) {
-  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
+  pdl_enter(p.nowait);  // PDL: predecessor complete + visible, unless nowait (common.cuh)
   using Tr = KindTraits<KIND>;
   constexpr int BNH = BN / 2;                    // B columns held by each CTA
   constexpr int A_BYTES = TC_BM * TC_BK * 2;     // 16 KB: this CTA's 128 rows

@@ -58,6 +58,7 @@ struct TcParams {
   PeerBufs pret;
   int tpr;
   CapTable ct;                  // base rows of each local expert region
+  int nowait;                   // inputs complete once the predecessor started: no PDL wait
 };
 
 template <int KIND>
