@@ -648,8 +648,13 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
                              const int32_t* kept, const int32_t* mtile_prefix, int n_local,
                              const CapTable& ct, int max_cap, cudaStream_t s,
                              int64_t* nlaunch, Prof* prof, uint32_t* mask, float* bias_part,
-                             const TcFusion* fz, int tail_nowait) {
+                             const TcFusion* fz, int tail_nowait, void* dA_sep) {
   (void)plan; (void)max_cap;
+  // dA in its own buffer (2-CTA DGRAD_A, whose ReLU' mask comes from the FWD1 bits, not from
+  // H): H is then never overwritten, so in the tail mode DGRAD_A can skip its PDL wait on the
+  // dW2 GEMM (which reads H) and take the SMs of that GEMM's last wave
+  void* dA = (dA_sep && use_2cta(f, TC_DGRAD_A) && mask) ? dA_sep : H;
+  const int da_nowait = tail_nowait && dA != H && dw2 != nullptr;
   // db1 from the DGRAD_A epilogue (2-CTA) instead of the weight-gradient bias warps
   const bool db1_in_dgrad = db1 && bias_part && use_2cta(f, TC_DGRAD_A);
   if (!ensure_encode()) return MOE_ERR_CUDA;
@@ -669,8 +674,8 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   // dA = (dO W2_e) * 1[H > 0], W2_e stored [d_out x f] = [K x N]
   {
     ProfScope ps(prof, "dgrad_dA", s);
-    st = mgroup<TC_DGRAD_A>(dO, rows, dout, w2, f, n_local, nullptr, H, f, kept, mtile_prefix, ct, s,
-                            mask, db1_in_dgrad ? bias_part : nullptr);
+    st = mgroup<TC_DGRAD_A>(dO, rows, dout, w2, f, n_local, nullptr, dA, f, kept, mtile_prefix, ct, s,
+                            mask, db1_in_dgrad ? bias_part : nullptr, nullptr, da_nowait);
   }
   if (st != MOE_OK) return st;
   ++nl;
@@ -690,13 +695,13 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
   }
   if (dw1) {  // dW1_e = dA_e^T X_e (db1 fused here only when not produced by DGRAD_A)
     ProfScope ps(prof, "wgrad_w1", s);
-    st = wgrad(H, f, X, d, rows, n_local, dw1, db1_in_dgrad ? nullptr : db1, accumulate, kept, ct, s,
+    st = wgrad(dA, f, X, d, rows, n_local, dw1, db1_in_dgrad ? nullptr : db1, accumulate, kept, ct, s,
                fz);
     if (st != MOE_OK) return st;
     ++nl;
   } else if (db1 && !db1_in_dgrad) {
     ProfScope ps(prof, "bias_grad", s);
-    TC_CUDA(launch_colsum(1, H, f, kept, n_local, ct, db1, accumulate, s));
+    TC_CUDA(launch_colsum(1, dA, f, kept, n_local, ct, db1, accumulate, s));
     ++nl;
   }
   // dX = dA W1_e, W1_e stored [f x d] = [K x N]
@@ -705,7 +710,7 @@ moe_status_t tc_ffn_backward(TcPlan* plan, void* X, void* H, void* dO, void* dX,
     // tail_nowait: DGRAD_X reads dA (DGRAD_A, two launches back), W1 and the fused dispatch
     // backward's dl rows / W_g -- nothing of WGRAD_W1, which writes only dW1 -- so it skips the
     // PDL wait and fills the SMs WGRAD_W1's last wave leaves idle
-    st = mgroup<TC_DGRAD_X>(H, rows, f, w1, d, n_local, nullptr, dX, d, kept, mtile_prefix, ct, s,
+    st = mgroup<TC_DGRAD_X>(dA, rows, f, w1, d, n_local, nullptr, dX, d, kept, mtile_prefix, ct, s,
                             nullptr, nullptr, fz, tail_nowait && dw1 != nullptr);
   }
   if (st != MOE_OK) return st;

@@ -65,9 +65,11 @@ moe_status_t tc_ffn_backward(TcPlan* p, void* X, void* H, void* dO, void* dX, co
                              const int32_t* kept, const int32_t* mtile_prefix, int n_local,
                              const CapTable& ct, int max_cap, cudaStream_t s,
                              int64_t* nlaunch, Prof* prof, uint32_t* mask, float* bias_part,
-                             const TcFusion* fz = nullptr, int tail_nowait = 0);
+                             const TcFusion* fz = nullptr, int tail_nowait = 0,
+                             void* dA_sep = nullptr);
 // tail_nowait: the db1 reduction runs after the dX GEMM without a PDL wait (single GPU; the
-// caller closes the backward with a full-dependency launch)
+// caller closes the backward with a full-dependency launch).  dA_sep: [rows x f] buffer for dA
+// (else dA is written over H); with it, DGRAD_A also skips its wait in the tail mode.
 
 // fp32 path (c1 / c2): the same expert GEMMs on tcgen05 kind::tf32 with 3xTF32 operand
 // splitting (gemm_tf32.cu): fp32 buffers, bias / db fused as in the bf16 1-CTA kernels.

@@ -40,7 +40,7 @@ int moe::pdl_enabled() {
 struct Layout {
   size_t logits, idx, fresh_idx, slot_of, w, dw, dl, tile_hist, tile_off, meta, token_of_slot,
       xbuf, hbuf, obuf, dobuf, dxbuf, partial, dlb, mask, bpart, bal, grow, ep_all, sendbuf, oret, dwg32,
-      pre_dev, dlr, dropb, droptok, sstat, ycnt, total;
+      pre_dev, dlr, dropb, droptok, sstat, ycnt, dabuf, total;
 };
 
 struct moe_ctx {
@@ -177,6 +177,8 @@ void compute_layout(moe_ctx* h) {
   L.sstat = take(h->use_tc ? T * 16 : 0);
   // k = 2 combine in FWD2: one counter per (token, column block of <= 64 columns)
   L.ycnt = take(h->use_tc && k == 2 && !h->use_ep ? T * (size_t)(h->dout / 64) * 4 : 0);
+  // single GPU: dA in its own buffer (H stays intact; lets DGRAD_A overlap the dW2 GEMM)
+  L.dabuf = take(h->use_tc && !h->use_ep ? (size_t)h->rows * h->f * h->s : 0);
   L.total = o;
 }
 
@@ -879,7 +881,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
                                       h->ct, h->max_cap_local, s0, &nk, &h->prof,
                                       (uint32_t*)(ws + h->L.mask), (float*)(ws + h->L.bpart),
                                       (h->fused_gather || fdx || fdx_ep || (peer && h->peer_ret)) ? &fz : nullptr,
-                                      tail ? 1 : 0);
+                                      tail ? 1 : 0, tail ? (void*)(ws + h->L.dabuf) : nullptr);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 backward failed");
   } else if (h->use_tf32) {
