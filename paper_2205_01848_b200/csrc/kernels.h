@@ -62,8 +62,8 @@ cudaError_t launch_cache_update(int32_t* table, int64_t num, int k, const int64_
 cudaError_t launch_gate_topk(int dtype, const void* x, const void* wg, int T, int n, int d,
                              int k, int renorm, const int32_t* cached, RouteBufs b,
                              cudaStream_t s);
-cudaError_t launch_route_hist(const int32_t* idx, int T, int k, int n, int32_t* hist,
-                              cudaStream_t s);
+cudaError_t launch_route_hist(int32_t* idx, int T, int k, int n, int32_t* hist,
+                              cudaStream_t s, const int32_t* src = nullptr);
 cudaError_t launch_route_scan(const int32_t* hist, int ntiles, int n, const CapTable& ct,
                               RouteBufs b, cudaStream_t s);
 cudaError_t launch_dispatch(int dtype, const int32_t* idx, const void* x, int T, int k,

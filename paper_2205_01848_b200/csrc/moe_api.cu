@@ -581,8 +581,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, s0));
     CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
     sd = h->side;
-    if (T > 0 && !tab)
-      CUDA_TRY(h, cudaMemcpyAsync(rb.idx, h->cached, (size_t)T * k * 4, cudaMemcpyDeviceToDevice, sd));
+    // (raw cached indices are copied into idx by the histogram kernel itself, below)
   } else {
     // fallback mode: the gate rewrites the rows of unknown samples with their fresh top-k
     rb.idx_fix = fallback ? rb.idx : nullptr;
@@ -602,7 +601,8 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
                                                             rb.idx, rb.hit_count, rb.flags, s0));
   }
   if (!rb.gate_hist)
-    KL(h, T > 0, "route_hist", sd, launch_route_hist(rb.idx, T, k, n, rb.tile_hist, sd));
+    KL(h, T > 0, "route_hist", sd, launch_route_hist(rb.idx, T, k, n, rb.tile_hist, sd,
+                                                     (cached && !tab) ? h->cached : nullptr));
   rb.gate_hist = 0;
   KL(h, 1, "route_scan", sd, launch_route_scan(rb.tile_hist, ntiles, n, h->ct, rb, sd));
   if (!h->use_ep) {

@@ -196,8 +196,10 @@ cudaError_t launch_gate_topk(int dtype, const void* x, const void* wg, int T, in
 // =====================================================================================
 // K2a: per-tile expert histogram of the dispatch indices (order-independent counts).
 // =====================================================================================
-__global__ void route_hist_kernel(const int32_t* __restrict__ idx, int Tn, int k, int n,
-                                  int32_t* __restrict__ hist) {
+// src != null (cached mode): the dispatch indices are read from the caller's cached array and
+// copied into idx on the way (one pass instead of a device copy + this kernel)
+__global__ void route_hist_kernel(int32_t* __restrict__ idx, int Tn, int k, int n,
+                                  int32_t* __restrict__ hist, const int32_t* __restrict__ src) {
   pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
   __shared__ int32_t h[MOE_MAX_E];
   for (int e = threadIdx.x; e < n; e += blockDim.x) h[e] = 0;
@@ -205,18 +207,20 @@ __global__ void route_hist_kernel(const int32_t* __restrict__ idx, int Tn, int k
   int t = blockIdx.x * MOE_ROUTE_TILE + threadIdx.x;
   if (t < Tn)
     for (int r = 0; r < k; ++r) {
-      const int e = idx[(size_t)t * k + r];
+      const size_t i = (size_t)t * k + r;
+      const int e = src ? src[i] : idx[i];
+      if (src) idx[i] = e;
       if ((unsigned)e < (unsigned)n) atomicAdd(&h[e], 1);  // invalid cached index: flagged
     }
   __syncthreads();
   for (int e = threadIdx.x; e < n; e += blockDim.x) hist[(size_t)blockIdx.x * n + e] = h[e];
 }
 
-cudaError_t launch_route_hist(const int32_t* idx, int T, int k, int n, int32_t* hist,
-                              cudaStream_t s) {
+cudaError_t launch_route_hist(int32_t* idx, int T, int k, int n, int32_t* hist,
+                              cudaStream_t s, const int32_t* src) {
   if (T == 0) return cudaSuccess;
   int ntiles = (T + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE;
-  launch_pdl(route_hist_kernel, ntiles, MOE_ROUTE_TILE, 0, s, idx, T, k, n, hist);
+  launch_pdl(route_hist_kernel, ntiles, MOE_ROUTE_TILE, 0, s, idx, T, k, n, hist, src);
   return cudaGetLastError();
 }
 
