@@ -412,7 +412,8 @@ MOE_API moe_status_t moe_profile_enable(moe_handle_t h, int32_t on);
 MOE_API moe_status_t moe_profile_read(moe_handle_t h, moe_kernel_time_t* out, int32_t max,
                                       int32_t* count, int32_t reset);
 
-/* Human-readable description of the last error on this handle (never NULL). */
+/* Human-readable description of the last error on this handle (never NULL); with h == NULL,
+   why the last moe_init on the calling thread failed (e.g. the peer window allocation). */
 MOE_API const char* moe_last_error(moe_handle_t h);
 
 /* ----------------------------------------------------------------------------------- *

@@ -148,7 +148,8 @@ class MoEError(RuntimeError):
 
 def check(status, handle=None, what=""):
     if status != MOE_OK:
-        msg = ""
-        if handle is not None:
-            msg = load().moe_last_error(handle).decode()
+        # handle None (moe_init): the library keeps the reason of the last failed init
+        msg = load().moe_last_error(handle).decode()
+        if msg == "null handle":
+            msg = ""
         raise MoEError(status, f"{what} {msg}".strip())

@@ -274,7 +274,13 @@ int64_t tokens_global(const moe_ctx* h) { return (int64_t)h->maxT * h->R; }
 
 extern "C" {
 
-const char* moe_last_error(moe_handle_t h) { return h ? h->err.c_str() : "null handle"; }
+// why the last moe_init on this thread failed (moe_last_error(NULL))
+static thread_local std::string g_init_err;
+
+const char* moe_last_error(moe_handle_t h) {
+  if (h) return h->err.c_str();
+  return g_init_err.empty() ? "null handle" : g_init_err.c_str();
+}
 
 moe_status_t moe_capacity_from_factors(int32_t n, int64_t tokens_global, int32_t k,
                                        const double* alpha, int32_t* cap_out) {
@@ -321,10 +327,13 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
   h->use_tc = (c.dtype == MOE_BF16) && !(fs && fs[0] == '1');
   h->use_tf32 = (c.dtype == MOE_F32) && !(fs && fs[0] == '1') && tf32_supported(h->d, h->f, dout);
 
+  g_init_err.clear();
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_gate, cudaEventDisableTiming) != cudaSuccess) {
+    g_init_err = std::string("moe_init: stream / event creation: ") +
+                 cudaGetErrorString(cudaGetLastError());
     delete h;
     return MOE_ERR_CUDA;
   }
@@ -349,9 +358,12 @@ moe_status_t moe_init(const moe_config_t* cfg, moe_handle_t* out) {
     // zeroed and COMPLETE before any rank can see the window: the epoch / flag words start at
     // 0, and a memset still in flight (legacy stream) could race with a peer's first count
     // push or with kernels on non-blocking streams
-    if (cudaMalloc((void**)&h->pwin, h->PL.total) != cudaSuccess ||
-        cudaMemset(h->pwin, 0, h->PL.total) != cudaSuccess ||
-        cudaDeviceSynchronize() != cudaSuccess) {
+    cudaError_t ce = cudaMalloc((void**)&h->pwin, h->PL.total);
+    if (ce == cudaSuccess) ce = cudaMemset(h->pwin, 0, h->PL.total);
+    if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+    if (ce != cudaSuccess) {
+      g_init_err = "moe_init: peer window of " + std::to_string(h->PL.total >> 20) +
+                   " MiB (window_rows " + std::to_string(wrows) + "): " + cudaGetErrorString(ce);
       if (h->pwin) cudaFree(h->pwin);
       cudaEventDestroy(h->ev_fork);
       cudaEventDestroy(h->ev_join);
