@@ -865,7 +865,8 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   // complete once the dX GEMM has started, so they skip their PDL wait and run beside that
   // GEMM's tail and each other; the gate-weight reduction closes the backward with a
   // full-dependency launch (every later kernel again sees all of this step complete).
-  static const bool tail_env = !(getenv("MOE_TAIL") && getenv("MOE_TAIL")[0] == '0');
+  const char* tail_e = getenv("MOE_TAIL");  // (read per call: the tests toggle it)
+  const bool tail_env = !(tail_e && tail_e[0] == '0');
   const bool tail = tail_env && !h->use_ep && h->use_tc && T > 0 && a->dw_gate != nullptr &&
                     (fdx || a->dx == nullptr);
   if (h->use_tc) {

@@ -218,3 +218,31 @@ def test_combine_bwd_lean_equals_full(n, k, d, T, renorm):
     assert torch.equal(dl1, dl2) and torch.equal(dw1, dw2)
     for key in g1:
         _bitwise(g2[key], g1[key], key)
+
+
+@pytest.mark.parametrize("n,k,d,T,alpha", [(64, 1, 1024, 4096, 1.0), (16, 1, 256, 1500, 0.7)])
+def test_backward_tail_mode_bitwise(n, k, d, T, alpha, monkeypatch):
+    """The backward tail without PDL waits (db1 reduction, drop-only gate-dx pass, gate-weight
+    gradient, dA / dX GEMMs overlapping their predecessors; dA in its own buffer) against the
+    plain PDL chain (MOE_TAIL=0): every output bitwise equal, over three iterations with
+    gradient accumulation and dropped tokens (outputs poisoned first)."""
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer
+    g = {kk: v.cuda() for kk, v in make_layer(n, d, 4 * d, d, T, "bf16").items()}
+    dy = make_dy(T, d, "bf16").cuda()
+    outs = []
+    for tail in ("1", "0"):
+        monkeypatch.setenv("MOE_TAIL", tail)
+        layer = MoELayer(n, k, d, 4 * d, 0, T, "bf16", 0, device="cuda")
+        layer.set_capacities(capacity_from_factors([alpha] * n, T, k))
+        grads = None
+        for it in range(3):
+            y = layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+            grads = layer.backward(dy, grads=grads, accumulate=it > 0)
+        torch.cuda.synchronize()
+        outs.append((y.clone(), {kk: v.clone() for kk, v in grads.items()}))
+        layer.close()
+    (y1, g1), (y0, g0) = outs
+    _bitwise(y1, y0, "y")
+    for key in g0:
+        _bitwise(g1[key], g0[key], key)
