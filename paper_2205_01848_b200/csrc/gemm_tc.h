@@ -71,8 +71,9 @@ moe_status_t tc_ffn_backward(TcPlan* p, void* X, void* H, void* dO, void* dX, co
 // caller closes the backward with a full-dependency launch).  dA_sep: [rows x f] buffer for dA
 // (else dA is written over H); with it, DGRAD_A also skips its wait in the tail mode.
 
-// fp32 path (c1 / c2): the same expert GEMMs on tcgen05 kind::tf32 with split-operand
-// splitting (gemm_tf32.cu): fp32 buffers, bias / db fused as in the bf16 1-CTA kernels.
+// fp32 path (c1 / c2): the same expert GEMMs on tcgen05 kind::tf32 with each fp32 operand
+// split into two tf32 terms (gemm_tf32.cu): fp32 buffers, bias / db fused as in the bf16
+// 1-CTA kernels.
 bool tf32_supported(int d, int f, int dout);   // d, f, d_out multiples of 32
 moe_status_t tf32_ffn_forward(void* X, const void* w1, const void* b1, const void* w2,
                               const void* b2, void* H, void* O, int64_t rows, int d, int f,
