@@ -84,6 +84,7 @@ moe_status_t tf32_ffn_backward(void* X, void* H, void* dO, void* dX, const void*
                                const void* w2, void* dw1, void* db1, void* dw2, void* db2,
                                int accumulate, int64_t rows, int d, int f, int dout,
                                const int32_t* kept, const int32_t* mtile_prefix, int n_local,
-                               const CapTable& ct, cudaStream_t s, int64_t* nlaunch, Prof* prof);
+                               const CapTable& ct, cudaStream_t s, int64_t* nlaunch, Prof* prof,
+                               int tail_nowait = 0, void* dA_sep = nullptr);
 
 }  // namespace moe

@@ -59,6 +59,8 @@ struct TcParams {
   int tpr;
   CapTable ct;                  // base rows of each local expert region
   int nowait;                   // inputs complete once the predecessor started: no PDL wait
+  const void* hsrc;             // fp32 DGRAD_A: H for the ReLU' test when dA is not written
+                                // over it (null = C itself holds H)
 };
 
 template <int KIND>

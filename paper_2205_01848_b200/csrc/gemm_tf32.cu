@@ -107,7 +107,7 @@ template <int KIND, int BN, int STAGES>
 __global__ void __launch_bounds__(TF_THREADS, 1)
     tf32_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      TcParams p) {
-  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
+  pdl_enter(p.nowait);  // PDL: predecessor complete + visible, unless nowait (backward tail)
   using Tr = KindTraits<KIND>;
   constexpr int A_BYTES = TC_BM * TF_BK * 4;   // 16 KB
   constexpr int B_BYTES = BN * TF_BK * 4;
@@ -332,6 +332,9 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
       const bool row_ok = row < Me;
       float* crow = Tr::kgroup ? Cbase + ((size_t)e * p.M + row) * p.N
                                : Cbase + (size_t)(p.ct.base[e] + row) * p.ldc;
+      const float* hrow = (KIND == TC_DGRAD_A && p.hsrc)
+                              ? reinterpret_cast<const float*>(p.hsrc) + (crow - Cbase)
+                              : crow;
       const uint32_t taddr = tmem_base + acc * 2 * BN + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           if (row_ok) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
-              const float4 h = *reinterpret_cast<const float4*>(crow + col0 + i);
+              const float4 h = *reinterpret_cast<const float4*>(hrow + col0 + i);
               v[i] = h.x > 0.f ? v[i] : 0.f;
               v[i + 1] = h.y > 0.f ? v[i + 1] : 0.f;
               v[i + 2] = h.z > 0.f ? v[i + 2] : 0.f;
@@ -489,7 +492,8 @@ int pick_bn32(int N, int64_t tiles_128) {
 template <int KIND>
 moe_status_t mgroup32(const void* A, int64_t rows, int K, const void* B, int N, int n_local,
                       const void* bias, void* C, int ldc, const int32_t* kept,
-                      const int32_t* prefix, const CapTable& ct, cudaStream_t s) {
+                      const int32_t* prefix, const CapTable& ct, cudaStream_t s, int nowait = 0,
+                      const void* hsrc = nullptr) {
   CUtensorMap ma, mb;
   const int bn = pick_bn32(N, (rows / TC_BM) * (N / 128));
   TF_TRY(map32(&ma, A, K, rows, 32, 128));
@@ -500,6 +504,8 @@ moe_status_t mgroup32(const void* A, int64_t rows, int K, const void* B, int N, 
   TcParams p{};
   p.kept = kept; p.mtile_prefix = prefix; p.n_local = n_local; p.M = 0; p.N = N; p.K = K;
   p.bias = (const __nv_bfloat16*)bias; p.C = (__nv_bfloat16*)C; p.ldc = ldc; p.ct = ct;
+  p.nowait = nowait;
+  p.hsrc = hsrc;
   TF_CUDA(launch_tf32_bn<KIND>(bn, ma, mb, p, s));
   return MOE_OK;
 }
@@ -552,8 +558,12 @@ moe_status_t tf32_ffn_backward(void* X, void* H, void* dO, void* dX, const void*
                                const void* w2, void* dw1, void* db1, void* dw2, void* db2,
                                int accumulate, int64_t rows, int d, int f, int dout,
                                const int32_t* kept, const int32_t* mtile_prefix, int n_local,
-                               const CapTable& ct, cudaStream_t s, int64_t* nlaunch, Prof* prof) {
+                               const CapTable& ct, cudaStream_t s, int64_t* nlaunch, Prof* prof,
+                               int tail_nowait, void* dA_sep) {
   if (!enc32_init()) return MOE_ERR_CUDA;
+  // dA in its own buffer (the ReLU' test then reads the intact H): no write-after-read hazard
+  // on the dW2 GEMM's H reads, so in the tail mode DGRAD_A and DGRAD_X skip their PDL waits
+  void* dA = dA_sep ? dA_sep : H;
   *nlaunch = 0;
   if (rows == 0 || n_local == 0) return MOE_OK;
   int64_t nl = 0;
@@ -568,27 +578,28 @@ moe_status_t tf32_ffn_backward(void* X, void* H, void* dO, void* dX, const void*
     TF_CUDA(launch_colsum(0, dO, dout, kept, n_local, ct, db2, accumulate, s));
     ++nl;
   }
-  {  // dA = (dO W2_e) * 1[H > 0], W2_e stored [d_out x f] = [K x N]; written over H
+  {  // dA = (dO W2_e) * 1[H > 0], W2_e stored [d_out x f] = [K x N]; over H or into dA_sep
     ProfScope ps(prof, "dgrad_dA", s);
-    st = mgroup32<TC_DGRAD_A>(dO, rows, dout, w2, f, n_local, nullptr, H, f, kept, mtile_prefix,
-                              ct, s);
+    st = mgroup32<TC_DGRAD_A>(dO, rows, dout, w2, f, n_local, nullptr, dA, f, kept, mtile_prefix,
+                              ct, s, tail_nowait && dA != H && dw2 != nullptr,
+                              dA != H ? H : nullptr);
   }
   if (st != MOE_OK) return st;
   ++nl;
   if (dw1) {  // dW1_e = dA_e^T X_e, db1 = sum dA fused in
     ProfScope ps(prof, "wgrad_w1", s);
-    st = wgrad32(H, f, X, d, rows, n_local, dw1, db1, accumulate, kept, ct, s);
+    st = wgrad32(dA, f, X, d, rows, n_local, dw1, db1, accumulate, kept, ct, s);
     if (st != MOE_OK) return st;
     ++nl;
   } else if (db1) {
     ProfScope ps(prof, "bias_grad", s);
-    TF_CUDA(launch_colsum(0, H, f, kept, n_local, ct, db1, accumulate, s));
+    TF_CUDA(launch_colsum(0, dA, f, kept, n_local, ct, db1, accumulate, s));
     ++nl;
   }
   {  // dX = dA W1_e, W1_e stored [f x d] = [K x N]
     ProfScope ps(prof, "dgrad_dX", s);
-    st = mgroup32<TC_DGRAD_X>(H, rows, f, w1, d, n_local, nullptr, dX, d, kept, mtile_prefix,
-                              ct, s);
+    st = mgroup32<TC_DGRAD_X>(dA, rows, f, w1, d, n_local, nullptr, dX, d, kept, mtile_prefix,
+                              ct, s, tail_nowait && dA != H && dw1 != nullptr);
   }
   if (st != MOE_OK) return st;
   ++nl;

@@ -92,7 +92,8 @@ cudaError_t launch_gate_dx(int dtype, const void* wg, const void* dxbuf, RouteBu
 // f32_out != null: write the fp32 sum there instead (EP: all-reduced before rounding)
 cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int n, int d,
                            float* partial, int splits, void* dwg, int accumulate,
-                           cudaStream_t s, float* f32_out = nullptr);
+                           cudaStream_t s, float* f32_out = nullptr, bool nowait = false);
+// (nowait: no PDL wait in the partial kernel, full-dependency reduction -- the backward tail)
 cudaError_t launch_f32_to(int dtype, const float* in, size_t count, void* out, int accumulate,
                           cudaStream_t s);
 int gate_dw_splits(int T, int d);

@@ -178,7 +178,7 @@ void compute_layout(moe_ctx* h) {
   // k = 2 combine in FWD2: one counter per (token, column block of <= 64 columns)
   L.ycnt = take(h->use_tc && k == 2 && !h->use_ep ? T * (size_t)(h->dout / 64) * 4 : 0);
   // single GPU: dA in its own buffer (H stays intact; lets DGRAD_A overlap the dW2 GEMM)
-  L.dabuf = take(h->use_tc && !h->use_ep ? (size_t)h->rows * h->f * h->s : 0);
+  L.dabuf = take((h->use_tc || h->use_tf32) && !h->use_ep ? (size_t)h->rows * h->f * h->s : 0);
   L.total = o;
 }
 
@@ -869,6 +869,9 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
   const bool tail_env = !(tail_e && tail_e[0] == '0');
   const bool tail = tail_env && !h->use_ep && h->use_tc && T > 0 && a->dw_gate != nullptr &&
                     (fdx || a->dx == nullptr);
+  // fp32 (split-tf32 GEMMs): dA / dX GEMMs and the gate-weight partials skip their waits the
+  // same way; the gate-dx pass (it reads dX) keeps its wait on the dX GEMM
+  const bool tail32 = tail_env && !h->use_ep && h->use_tf32 && T > 0 && a->dw_gate != nullptr;
   if (h->use_tc) {
     int64_t nk = 0;
     TcFusion fz;  // N2: dW1 = dA^T X gathers the x rows like the forward did
@@ -901,7 +904,8 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
     int64_t nk = 0;
     moe_status_t st = tf32_ffn_backward(X, H, dO, dXb, w1, w2, dw1, db1, dw2, db2, acc, h->rows,
                                         d, f, dout, kept_local, rb.mtile_prefix, nl, h->ct, s0,
-                                        &nk, &h->prof);
+                                        &nk, &h->prof, tail32 ? 1 : 0,
+                                        tail32 ? (void*)(ws + h->L.dabuf) : nullptr);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 tf32 backward failed");
   } else {
@@ -933,7 +937,7 @@ moe_status_t moe_backward(moe_handle_t h, const moe_bwd_args_t* a) {
     } else {
       int splits = gate_dw_splits(h->maxT, d);
       KL(h, T > 0 ? 2 : 0, "gate_dw", s0, launch_gate_dw(dt, rb.dl, fa.x, T, n, d, (float*)(ws + h->L.partial),
-                                          splits, a->dw_gate, acc, s0, dwg_f32));
+                                          splits, a->dw_gate, acc, s0, dwg_f32, tail32));
     }
     if (T == 0 && dwg_f32) CUDA_TRY(h, cudaMemsetAsync(dwg_f32, 0, (size_t)n * d * 4, s0));  // no tokens
     return MOE_OK;

@@ -1166,8 +1166,8 @@ template <typename T, int NJ>
 __global__ void __launch_bounds__(256) gate_dw_kernel(const float* __restrict__ dl,
                                                       const T* __restrict__ x, int Tn, int n,
                                                       int d, int chunk,
-                                                      float* __restrict__ partial) {
-  pdl_enter();  // PDL: predecessor complete + visible (common.cuh)
+                                                      float* __restrict__ partial, int nowait) {
+  pdl_enter(nowait);  // PDL (nowait: the backward tail, see launch_gate_dw_tc / moe_api)
   extern __shared__ float sm[];
   float* xs = sm;                 // [32][64]
   float* ls = sm + 32 * 64;       // [32][n]
@@ -1269,7 +1269,8 @@ int gate_dw_splits(int T, int d) {
 
 cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int n, int d,
                            float* partial, int splits, void* dwg, int accumulate,
-                           cudaStream_t s, float* f32_out) {
+                           cudaStream_t s, float* f32_out, bool nowait) {
+  const int nw = nowait ? 1 : 0;
   size_t count = (size_t)n * d;
   if (f32_out && T == 0) return cudaMemsetAsync(f32_out, 0, count * 4, s);
   if (T == 0) {
@@ -1286,11 +1287,11 @@ cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int
     if (dtype == 1) {                                                                       \
       auto kf = gate_dw_kernel<__nv_bfloat16, NJ>;                                          \
       cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-      launch_pdl(kf, grid, 256, smem, s, dl, (const __nv_bfloat16*)x, T, n, d, chunk, partial);     \
+      launch_pdl(kf, grid, 256, smem, s, dl, (const __nv_bfloat16*)x, T, n, d, chunk, partial, nw);  \
     } else {                                                                                \
       auto kf = gate_dw_kernel<float, NJ>;                                                  \
       cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-      launch_pdl(kf, grid, 256, smem, s, dl, (const float*)x, T, n, d, chunk, partial);             \
+      launch_pdl(kf, grid, 256, smem, s, dl, (const float*)x, T, n, d, chunk, partial, nw);         \
     }                                                                                       \
   } else
   GDW_CASE(2) GDW_CASE(4) GDW_CASE(8) GDW_CASE(16) GDW_CASE(32) GDW_CASE(64) {
@@ -1300,7 +1301,7 @@ cudaError_t launch_gate_dw(int dtype, const float* dl, const void* x, int T, int
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   if (f32_out) return launch_reduce_partials(0, partial, splits, count, f32_out, 0, s);
-  return launch_reduce_partials(dtype, partial, splits, count, dwg, accumulate, s);
+  return launch_reduce_partials(dtype, partial, splits, count, dwg, accumulate, s, nowait);
 }
 
 template <typename T>
