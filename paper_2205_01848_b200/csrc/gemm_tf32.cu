@@ -473,9 +473,14 @@ cudaError_t launch_tf32_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, c
   return launch_tf32<KIND, 64>(a, b, p, s);
 }
 
-// 128-column tiles when they still give every SM a tile (about tiles_128 of them), else 64
-int pick_bn32(int N, int64_t tiles_128) {
-  return (N % 128 == 0 && tiles_128 >= g_sms32) ? 128 : 64;
+// 64-column tiles unless 128-column ones need fewer waves of tiles over the SMs: at these sizes
+// a tile's time is set by its k-loop latency, not its width, so the wave count decides
+// (m_tiles: the m-tiles of the launch, an upper bound from the buffer rows)
+int pick_bn32(int N, int64_t m_tiles) {
+  if (N % 128 != 0) return 64;
+  const int64_t w128 = (m_tiles * (N / 128) + g_sms32 - 1) / g_sms32;
+  const int64_t w64 = (m_tiles * ((N + 63) / 64) + g_sms32 - 1) / g_sms32;
+  return w128 < w64 ? 128 : 64;
 }
 
 #define TF_TRY(x)                              \
@@ -495,7 +500,7 @@ moe_status_t mgroup32(const void* A, int64_t rows, int K, const void* B, int N, 
                       const int32_t* prefix, const CapTable& ct, cudaStream_t s, int nowait = 0,
                       const void* hsrc = nullptr) {
   CUtensorMap ma, mb;
-  const int bn = pick_bn32(N, (rows / TC_BM) * (N / 128));
+  const int bn = pick_bn32(N, rows / TC_BM);
   TF_TRY(map32(&ma, A, K, rows, 32, 128));
   if (KindTraits<KIND>::b_mn)
     TF_TRY(map32(&mb, B, N, (uint64_t)n_local * K, 32, 32, true));
@@ -521,7 +526,7 @@ moe_status_t wgrad32(const void* Abuf, int M, const void* Bbuf, int N, int64_t r
   p.kept = kept; p.mtile_prefix = nullptr; p.n_local = n_local; p.M = M; p.N = N; p.K = 0;
   p.C = (__nv_bfloat16*)Out; p.bias_out = (__nv_bfloat16*)bias_out; p.accumulate = accumulate;
   p.ct = ct;
-  const int bn = pick_bn32(N, (int64_t)n_local * ((M + TC_BM - 1) / TC_BM) * (N / 128));
+  const int bn = pick_bn32(N, (int64_t)n_local * ((M + TC_BM - 1) / TC_BM));
   TF_CUDA(launch_tf32_bn<TC_WGRAD>(bn, ma, mb, p, s));
   return MOE_OK;
 }
