@@ -423,6 +423,13 @@ static int tc_dbg() {  // MOE_TC_DBG: timing experiments only (1: skip epilogue 
   return v;
 }
 
+// MOE_HALF_TILES=0 turns off M = 128 remainder tiles in the 2-CTA M-grouped kernels (A/B
+// comparisons; read per call).
+static int tc_half() {
+  const char* e = getenv("MOE_HALF_TILES");
+  return e ? atoi(e) != 0 : 1;
+}
+
 static int tc_sched() {  // MOE_TC_SCHED: 2-CTA tile schedule (see TcParams::sched)
   static int v = -1;
   if (v < 0) {
@@ -565,6 +572,7 @@ static moe_status_t mgroup(const void* A, int64_t rows, int K, const void* B, in
   p.pf_kb = tc_pf();
   p.dbg = tc_dbg();
   p.nowait = two ? nowait : 0;  // (the 1-CTA kernel always waits)
+  p.half_tiles = two && !p.comb2 && tc_half();  // (comb2 counts per BN/2 column block)
   if (two) {
     CUtensorMap mc;
     TC_TRY(make_store_map(&mc, C, ldc, rows));

@@ -107,9 +107,9 @@ __device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
 }
 
 // instruction descriptor for M = 256 (cta_group::2)
-__host__ __device__ constexpr uint32_t make_idesc2(int n, int a_mn, int b_mn) {
+__host__ __device__ constexpr uint32_t make_idesc2(int n, int a_mn, int b_mn, int m = 256) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 constexpr int TC2_M = 256;
@@ -135,6 +135,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   constexpr int B_BYTES = BNH * TC_BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t IDESC = make_idesc2(BN, Tr::a_mn, Tr::b_mn);
+  constexpr uint32_t IDESC_H = make_idesc2(BN, Tr::a_mn, Tr::b_mn, 128);
+  // The last m-tile of an expert with at most 128 valid rows runs as an M = 128 MMA over the
+  // pair (64 rows per CTA): with dynamic capacities (no drops) many experts hold just over a
+  // multiple of 256 rows, and a full 256-row tile would be mostly padding.
+  auto half_tile = [&](int e, int mt) {
+    return !Tr::kgroup && p.half_tiles && p.kept[e] - mt * TC2_M <= TC_BM;
+  };
   constexpr int EPI_WARPS = TC_EPI_THREADS / 32;
   const bool fuse_bias = Tr::kgroup && p.bias_out != nullptr;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -229,7 +236,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       for (int t = t_begin; t < t_end; t += t_step) {
         int e, mt, nt;
         if (!decode_tile_ord<Tr::kgroup>(t, s_prefix, n_local, MT, NT, nfast, e, mt, nt)) break;
-        const int m0 = mt * TC2_M + (int)crank * TC_BM;
+        // (a half tile uses rows [0, 64) of each CTA's A tile; the 128 loaded rows keep the
+        // stage's transaction count)
+        const int m0 = mt * TC2_M + (int)crank * (half_tile(e, mt) ? TC_BM / 2 : TC_BM);
         const int n0 = nt * BN + (int)crank * BNH;
         const int base = p.ct.base[e];
         const int kept = p.kept[e];
@@ -274,7 +283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       for (int t = t_begin; t < t_end; t += t_step) {
         int e, mt, nt;
         if (!decode_tile_ord<Tr::kgroup>(t, s_prefix, n_local, MT, NT, nfast, e, mt, nt)) break;
-        const int m0 = mt * TC2_M + (int)crank * TC_BM;   // this CTA's A rows
+        const int m0 = mt * TC2_M + (int)crank * (half_tile(e, mt) ? TC_BM / 2 : TC_BM);  // A rows
         const int n0 = nt * BN + (int)crank * BNH;        // this CTA's B columns
         const int base = p.ct.base[e];
         const int nk = Tr::kgroup ? (p.kept[e] + TC_BK - 1) / TC_BK : p.K / TC_BK;
@@ -350,6 +359,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         mbar_wait_cluster(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
+        const uint32_t idesc = half_tile(e, mt) ? IDESC_H : IDESC;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -361,7 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                                    : umma_desc(sa + k * 32, 16, 1024);
             uint64_t db = Tr::b_mn ? umma_desc(sb + k * 2048, 8192, 1024)
                                    : umma_desc(sb + k * 32, 16, 1024);
-            tc_mma2(tmem_d, da, db, IDESC, (kb | k) != 0);
+            tc_mma2(tmem_d, da, db, idesc, (kb | k) != 0);
           }
           tc_commit2_mc(&empty_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -433,19 +443,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     // ============================ epilogue (both CTAs) ============================
     const int q = warp & 3;
     const int half = (warp - 4) >> 2;
-    const int row_in_tile = (int)crank * TC_BM + q * 32 + lane;
+    constexpr int CH = BN / 64;  // 32-column chunks per warp (full tile)
     const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty_bar[0]), 0);
     uint8_t* stg0 = s_stg + (warp - 4) * TC2_NBUF * TC2_STG_BYTES;
     int nbox = 0;
-    const int blk_in_tile = (int)crank * TC_BM + q * 32;  // this warp's first row in the tile
     int it = 0;
     for (int t = t_begin; t < t_end; t += t_step, ++it) {
       int e, mt, nt;
       if (!decode_tile_ord<Tr::kgroup>(t, s_prefix, n_local, MT, NT, nfast, e, mt, nt)) break;
       const int acc = it & 1;
       const int m0 = mt * TC2_M, n0 = nt * BN;
-      const int row = m0 + row_in_tile;
-      const int blk_row = m0 + blk_in_tile;  // warp-uniform
+      // Half tile (M = 128 over the pair: 64 rows per CTA): the accumulator of a CTA's 64 rows
+      // holds columns [0, BN/2) in TMEM lanes 0..63 and [BN/2, BN) in lanes 64..127, both in
+      // TMEM columns [0, BN/2), so lane quarter q drains rows 32 (q & 1) + lane of column half
+      // q >> 1, and the warp's `half` splits that into two BN/4 blocks (CH/2 chunks).
+      const bool ht = half_tile(e, mt);
+      const int rpc = ht ? TC_BM / 2 : TC_BM;                    // rows per CTA in this tile
+      const int blk_row = m0 + (int)crank * rpc + (ht ? (q & 1) * 32 : q * 32);  // warp-uniform
+      const int row = blk_row + lane;
+      const int nch = ht ? CH / 2 : CH;                             // chunks this warp drains
+      const int cbase = ht ? (q >> 1) * (BN / 2) + half * (BN / 4) : half * (BN / 2);
+      const int tbase = ht ? half * (BN / 4) : half * (BN / 2);    // TMEM column of chunk 0
       const bool zero_acc = Tr::kgroup && p.kept[e] == 0;
       const int Me = Tr::kgroup ? p.M : p.kept[e];
       const bool row_ok = row < Me;
@@ -456,7 +474,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         crow = p.C + ((size_t)e * p.M + row) * p.N;
       else
         crow = p.C + (size_t)(p.ct.base[e] + row) * p.ldc;
-      constexpr int CH = BN / 64;
       // Side inputs of the whole tile (bias, H mask, old gradient) are fetched BEFORE waiting
       // for the accumulator, so their DRAM/L2 latency overlaps this tile's MMAs.
       uint4 pre[CH][4];
@@ -468,7 +485,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       uint32_t* mrow = p.mask ? p.mask + (size_t)(p.ct.base[e] + row) * mask_ld : nullptr;
       if (KIND == TC_DGRAD_A && row_ok && !(p.dbg & 4)) {  // relu' mask bits written by FWD1
 #pragma unroll
-        for (int cc = 0; cc < CH; ++cc) mbits[cc] = mrow[(n0 >> 5) + half * CH + cc];
+        for (int cc = 0; cc < CH; ++cc)
+          if (cc < nch) mbits[cc] = mrow[((n0 + cbase) >> 5) + cc];
       }
       // N2 combine fusion (k = 1): this row's token and gate weight
       int ytok = -1;
@@ -499,7 +517,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       if (need_side) {
 #pragma unroll
         for (int cc = 0; cc < CH; ++cc) {
-          const int col0 = n0 + (half * CH + cc) * 32;
+          if (cc >= nch) continue;
+          const int col0 = n0 + cbase + cc * 32;
           const __nv_bfloat16* src = (KIND == TC_FWD1 || KIND == TC_FWD2)
                                          ? p.bias + (size_t)e * p.N + col0
                                          : crow + col0;
@@ -512,12 +531,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
 #pragma unroll
       for (int cc = 0; cc < CH; ++cc) {
-        const int c = half * CH + cc;
-        const int col0 = n0 + c * 32;
+        if (cc >= nch) continue;  // (warp-uniform)
+        const int col0 = n0 + cbase + cc * 32;
         uint4* side = pre[cc];
         uint32_t r[32];
         if (!zero_acc) {
-          tmem_ld32(taddr + c * 32, r);
+          tmem_ld32(taddr + tbase + cc * 32, r);
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = 0u;
@@ -701,22 +720,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         if (q == 0) {
           const float* rb = s_red + (((it & 1) * 2 + half) * 4) * (CH * 32);
           const size_t prow = (size_t)(s_prefix[e] + mt) * 2 + crank;
+          if (!ht) {
 #pragma unroll
-          for (int j = 0; j < CH; ++j) {
-            const int c = j * 32 + lane;
-            const float sum = ((rb[c] + rb[CH * 32 + c]) + rb[2 * CH * 32 + c]) + rb[3 * CH * 32 + c];
-            const int col = n0 + half * CH * 32 + c;
-            if (col < p.N) p.bias_part[prow * p.N + col] = sum;
+            for (int j = 0; j < CH; ++j) {
+              const int c = j * 32 + lane;
+              const float sum = ((rb[c] + rb[CH * 32 + c]) + rb[2 * CH * 32 + c]) + rb[3 * CH * 32 + c];
+              const int col = n0 + half * CH * 32 + c;
+              if (col < p.N) p.bias_part[prow * p.N + col] = sum;
+            }
+          } else {
+            // half tile: quarters 2g and 2g + 1 hold the two 32-row halves of column block g
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+#pragma unroll
+              for (int j = 0; j < CH / 2; ++j) {
+                const int c = j * 32 + lane;
+                const float sum = rb[(2 * g) * CH * 32 + c] + rb[(2 * g + 1) * CH * 32 + c];
+                const int col = n0 + g * (BN / 2) + half * (BN / 4) + c;
+                if (col < p.N) p.bias_part[prow * p.N + col] = sum;
+              }
           }
         }
       }
       if (KIND == TC_FWD1 && mrow && (row_ok || row_pad)) {  // one vector store per thread
-        uint32_t* mdst = mrow + (n0 >> 5) + half * CH;
-        if (CH == 4)
+        uint32_t* mdst = mrow + ((n0 + cbase) >> 5);
+        if (CH == 4 && !ht)
           *reinterpret_cast<uint4*>(mdst) = make_uint4(mout[0], mout[1 % CH], mout[2 % CH], mout[3 % CH]);
         else
 #pragma unroll
-          for (int cc = 0; cc < CH; ++cc) mdst[cc] = mout[cc];
+          for (int cc = 0; cc < CH; ++cc)
+            if (cc < nch) mdst[cc] = mout[cc];
       }
       tc_fence_before();
       __syncwarp();

@@ -59,6 +59,7 @@ struct TcParams {
   int tpr;
   CapTable ct;                  // base rows of each local expert region
   int nowait;                   // inputs complete once the predecessor started: no PDL wait
+  int half_tiles;               // 2-CTA M-grouped: remainder m-tiles of <= 128 rows run as M = 128
   const void* hsrc;             // fp32 DGRAD_A: H for the ReLU' test when dA is not written
                                 // over it (null = C itself holds H)
 };

@@ -246,3 +246,40 @@ def test_backward_tail_mode_bitwise(n, k, d, T, alpha, monkeypatch):
     _bitwise(y1, y0, "y")
     for key in g0:
         _bitwise(g1[key], g0[key], key)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,k,d,T,alpha,fusion", [
+    (8, 1, 512, 2048, 4.0, 14), (8, 1, 512, 2048, 4.0, 0), (16, 2, 256, 1500, 3.0, 14),
+    (16, 2, 256, 1500, 3.0, 0), (8, 1, 256, 2500, 1.0, 15)])
+def test_half_tiles_bitwise(n, k, d, T, alpha, fusion, monkeypatch):
+    """Remainder m-tiles of <= 128 rows run as M = 128 tiles over the CTA pair
+    (MOE_HALF_TILES=1, the default) against full 256-row tiles: every output bitwise equal
+    except db1, whose per-CTA row partials split the tile's rows differently (fp32 sums in
+    another order, one bf16 rounding: within 1 ulp).  No-drop capacities give remainders of
+    every size, so both tile shapes occur in each GEMM."""
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer
+    g = {kk: v.cuda() for kk, v in make_layer(n, d, 4 * d, d, T, "bf16").items()}
+    dy = make_dy(T, d, "bf16").cuda()
+    outs = []
+    for half in ("1", "0"):
+        monkeypatch.setenv("MOE_HALF_TILES", half)
+        layer = MoELayer(n, k, d, 4 * d, 0, T, "bf16", 0, device="cuda")
+        layer.set_capacities(capacity_from_factors([alpha] * n, T, k))
+        layer.set_fusion(fusion)
+        grads = None
+        for it in range(2):
+            y = layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+            grads = layer.backward(dy, grads=grads, accumulate=it > 0)
+        torch.cuda.synchronize()
+        outs.append((y.clone(), {kk: v.clone() for kk, v in grads.items()}))
+        layer.close()
+    (y1, g1), (y0, g0) = outs
+    _bitwise(y1, y0, "y")
+    for key in g0:
+        if key == "db1":
+            a, b = g1[key].float(), g0[key].float()
+            assert torch.all((a - b).abs() <= b.abs() * 2.0 ** -7 + 1e-30), "db1 beyond 1 ulp"
+        else:
+            _bitwise(g1[key], g0[key], key)
