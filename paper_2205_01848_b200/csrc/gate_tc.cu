@@ -42,6 +42,19 @@ struct GateFwdParams {
   float4* stats;           // [T] softmax statistics for the combine backward, or null:
                            // (max logit m, sum_e exp(l_e - m), sum over the experts NOT in the
                            // dispatch set of exp(l_e - m), 0)
+  // Cached mode: the dispatch indices are known before the gate, so A4 rides on
+  // the x stream the gate reads anyway -- warps 2-3 compute the tile's slots (token-major
+  // ranks, as the dispatch kernel does) and copy each x k-block from the TMA stage to the
+  // kept rows of X_buf once the stage has landed.  didx == null: off.
+  const int32_t* didx;     // [T x k] dispatch indices (the cached rows)
+  const int32_t* tile_off; // [ntiles x n] exclusive per-tile slot offsets (route_scan)
+  int32_t* slot_of;        // [T x k]
+  int32_t* token_of_slot;  // [rows]
+  __nv_bfloat16* xbuf;     // X_buf rows
+  const int32_t* kept;     // [n]: pad rows [kept_e, roundup(kept_e, 64)) are zeroed here
+  __nv_bfloat16* yz;       // fused combine: y rows of tokens with every pair dropped -> 0
+  int dout;
+  CapTable ct;             // capacities, region bases
 };
 
 // logits staging of the gate epilogue: one 32-row x 16-column fp32 box (2 KB, 64-byte
@@ -96,7 +109,7 @@ struct Bars {
 
 template <int STAGES>
 __device__ __forceinline__ Bars setup_bars(uint8_t* after_stages, int ncols, int warp, int lane,
-                                           int epi_threads = 128) {
+                                           int epi_threads = 128, int empty_count = 1) {
   Bars b;
   b.full = reinterpret_cast<uint64_t*>(after_stages);
   b.empty = b.full + STAGES;
@@ -106,7 +119,7 @@ __device__ __forceinline__ Bars setup_bars(uint8_t* after_stages, int ncols, int
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&b.full[s], 1);
-      mbar_init(&b.empty[s], 1);
+      mbar_init(&b.empty[s], empty_count);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&b.tfull[s], 1);
@@ -158,9 +171,13 @@ __global__ void __launch_bounds__(G_THREADS, 2)
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
   }
-  Bars b = setup_bars<STAGES>(smem + STAGES * STAGE_BYTES, 2 * BN, warp, lane);
+  // empty[s]: the MMA commit, plus one arrive per dispatch warp in fused cached mode
+  Bars b = setup_bars<STAGES>(smem + STAGES * STAGE_BYTES, 2 * BN, warp, lane, 128,
+                              p.didx ? 3 : 1);
   uint8_t* s_stg = smem + STAGES * STAGE_BYTES + 1024;  // [4 warps][2 KB], 1 KB aligned
   int32_t* s_hist = reinterpret_cast<int32_t*>(s_stg + 4 * GF_STG_BYTES);  // [256]
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_hist + 256);  // fused dispatch: [n][4]
+  int32_t* s_row = reinterpret_cast<int32_t*>(s_mask + 4 * p.n);   // [128 x k] X_buf row / -1
   const uint32_t tmem_base = *b.tmem;
   const int MT = (p.T + TC_BM - 1) / TC_BM;
   const int nk = K / TC_BK;
@@ -204,6 +221,92 @@ __global__ void __launch_bounds__(G_THREADS, 2)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         tc_commit(&b.tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 2 || warp == 3) {
+    if (p.didx) {
+      // ============== fused cached-mode dispatch (A4, S4.2): warps 2-3, 64 threads ==============
+      const int dt = threadIdx.x - 64;
+      const int n = p.n, k = p.k;
+      // pad rows [kept_e, roundup(kept_e, 64)) of expert regions blockIdx.x, + gridDim.x, ...
+      // (the token-contraction GEMMs read whole 64-row K-blocks)
+      for (int e = blockIdx.x; e < n; e += gridDim.x) {
+        const int kp = p.kept[e];
+        const int r0 = p.ct.base[e] + kp;
+        const int r1 = p.ct.base[e] + ((kp + MOE_PAD_ROWS - 1) / MOE_PAD_ROWS) * MOE_PAD_ROWS;
+        const size_t total = (size_t)max(r1 - r0, 0) * (K / 8);
+        for (size_t i = dt; i < total; i += 64)
+          st_v4(p.xbuf + (size_t)r0 * K + i * 8, make_uint4(0, 0, 0, 0));
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < MT; tile += gridDim.x) {
+        asm volatile("bar.sync 2, 64;" ::: "memory");  // the previous tile's rows are copied
+        for (int i = dt; i < 4 * n; i += 64) s_mask[i] = 0u;
+        asm volatile("bar.sync 2, 64;" ::: "memory");
+        // token-major ranks inside the routing tile (an expert appears at most once per token)
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int lt = dt + 64 * h2, t = tile * TC_BM + lt;
+          if (t < p.T)
+            for (int r = 0; r < k; ++r) {
+              const int e = p.didx[(size_t)t * k + r];
+              if ((unsigned)e < (unsigned)n) atomicOr(&s_mask[e * 4 + (lt >> 5)], 1u << (lt & 31));
+            }
+        }
+        asm volatile("bar.sync 2, 64;" ::: "memory");
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int lt = dt + 64 * h2, t = tile * TC_BM + lt;
+          bool any = false;
+          for (int r = 0; r < k; ++r) {
+            int row = -1;
+            if (t < p.T) {
+              const int e = p.didx[(size_t)t * k + r];
+              int slot = -1;
+              if ((unsigned)e < (unsigned)n) {  // invalid cached index: dropped (flag raised)
+                int rank = __popc(s_mask[e * 4 + (lt >> 5)] & ((1u << (lt & 31)) - 1u));
+                for (int q2 = 0; q2 < (lt >> 5); ++q2) rank += __popc(s_mask[e * 4 + q2]);
+                slot = p.ct.pre[e] + p.tile_off[(size_t)tile * n + e] + rank;
+                if (slot < p.ct.cap[e]) {
+                  row = p.ct.base[e] + slot;
+                  p.token_of_slot[row] = t * k + r;
+                } else {
+                  slot = -1;
+                }
+              }
+              p.slot_of[(size_t)t * k + r] = slot;
+            }
+            any |= row >= 0;
+            s_row[lt * k + r] = row;
+          }
+          if (!any && t < p.T && p.yz)  // every pair dropped: y[t] = 0
+            for (int v = 0; v < p.dout / 8; ++v)
+              st_v4(p.yz + (size_t)t * p.dout + v * 8, make_uint4(0, 0, 0, 0));
+        }
+        asm volatile("bar.sync 2, 64;" ::: "memory");
+        // each k-block: 128 rows x 128 bytes in the stage (128-byte swizzle: 16-byte chunk c of
+        // row r at c ^ (r & 7)); lane -> chunk lane % 8 of row 4 i + lane / 8 (a quarter warp
+        // reads one whole row: conflict-free), one full 128-byte line per row and destination
+        const int ch = lane & 7;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&b.full[stage], phase);
+          const uint8_t* sa = smem + stage * STAGE_BYTES;
+#pragma unroll 4
+          for (int i = 0; i < TC_BM / 8; ++i) {
+            const int lr = i * 8 + (warp - 2) * 4 + (lane >> 3);
+            if (tile * TC_BM + lr >= p.T) break;
+            const uint4 v = *reinterpret_cast<const uint4*>(sa + lr * 128 + ((ch ^ (lr & 7)) << 4));
+            for (int r = 0; r < k; ++r) {
+              const int row = s_row[lr * k + r];
+              if (row >= 0) st_v4(p.xbuf + (size_t)row * K + kb * TC_BK + ch * 8, v);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&b.empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
     __syncwarp();
@@ -806,7 +909,8 @@ static size_t smem_for(int stage_bytes, int stages) {
 }
 
 cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int d, int k,
-                               int renorm, const int32_t* cached, RouteBufs b, cudaStream_t s) {
+                               int renorm, const int32_t* cached, RouteBufs b, cudaStream_t s,
+                               const GateDispatch* gd) {
   if (T == 0) return cudaSuccess;
   if (!enc_init()) return cudaErrorNotSupported;
   CUtensorMap mx, mw;
@@ -828,6 +932,20 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
                   b.hit_count, b.flags, cached ? b.idx_fix : nullptr,
                   getenv("MOE_GATE_DBG") ? atoi(getenv("MOE_GATE_DBG")) : 0, tma_logits,
                   (!cached && b.gate_hist) ? b.tile_hist : nullptr, (float4*)b.sstat};
+  size_t extra = 0;  // fused dispatch: tile masks [n][4] + destination rows [128 x k]
+  if (gd) {
+    if (!cached || d % 64 != 0) return cudaErrorInvalidValue;
+    p.didx = b.idx;
+    p.tile_off = b.tile_off;
+    p.slot_of = b.slot_of;
+    p.token_of_slot = b.token_of_slot;
+    p.xbuf = (__nv_bfloat16*)gd->xbuf;
+    p.kept = b.kept;
+    p.yz = (__nv_bfloat16*)gd->y_zero;
+    p.dout = gd->dout;
+    p.ct = *gd->ct;
+    extra = (size_t)n * 16 + (size_t)128 * k * 4;
+  }
   const int MT = (T + 127) / 128;
   // two CTAs per SM (4-stage rings): twice the epilogue warps, which bound this kernel
   const int grid = MT < 2 * g_sms ? MT : 2 * g_sms;
@@ -837,7 +955,7 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
                      : (k == 2 ? gate_fwd_tc_kernel<BN, ST, 2>                           \
                                : (k <= 4 ? gate_fwd_tc_kernel<BN, ST, 4>                 \
                                          : gate_fwd_tc_kernel<BN, ST, 8>));              \
-    size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 1024 + 4 * GF_STG_BYTES + 1024;      \
+    size_t sm = smem_for((128 + BN) * 64 * 2, ST) + 1024 + 4 * GF_STG_BYTES + 1024 + extra; \
     cudaError_t e = set_smem(kf, sm);                                                    \
     if (e != cudaSuccess) return e;                                                      \
     launch_pdl(kf, grid, G_THREADS, sm, s, mx, mw, ml, p, d);                                    \

@@ -6,8 +6,19 @@
 #include "kernels.h"
 
 namespace moe {
+// Cached mode with the dispatch fused into the gate (single GPU, bf16): the gate kernel also
+// writes slot_of / token_of_slot from the cached rows and copies the kept x rows into X_buf
+// from its TMA stages (x read once for both), zeroes X_buf's pad rows and, with the fused
+// combine, the y rows of tokens with every pair dropped.  Needs route_scan's tile offsets.
+struct GateDispatch {
+  const CapTable* ct;
+  void* xbuf;
+  void* y_zero;  // or null
+  int dout;
+};
 cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int d, int k,
-                               int renorm, const int32_t* cached, RouteBufs b, cudaStream_t s);
+                               int renorm, const int32_t* cached, RouteBufs b, cudaStream_t s,
+                               const GateDispatch* gd = nullptr);
 cudaError_t launch_gate_dx_tc(const void* wg, const void* dxbuf, const void* dlb, int maxT,
                               int n_pad, RouteBufs b, int T, int k, int n, int d,
                               const CapTable& ct, void* dx, int accumulate, cudaStream_t s,

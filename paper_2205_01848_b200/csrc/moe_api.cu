@@ -72,7 +72,7 @@ struct moe_ctx {
   int64_t launches = 0;
   int use_tc = 0;             // tcgen05 path for bf16 (env MOE_FORCE_SIMT=1 disables)
   int use_tf32 = 0;           // fp32: expert GEMMs on tcgen05 kind::tf32 (split operands), else SIMT
-  int fusion = MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK;  // N2 (moe_set_fusion; GATHER opt-in)
+  int fusion = MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK | MOE_FUSE_CDISP;  // N2 (moe_set_fusion; GATHER opt-in)
   int fused_gather = 0;       // the last forward gathered x rows in the GEMMs (no X buffer)
   int peer_ret = 0;           // peer EP: O / dX rows returned by the GEMM epilogues (N1)
   int otok = 0;               // the last forward stored O in (token, choice) order (MOE_FUSE_OTOK)
@@ -548,6 +548,9 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   // token-ordered O
   const bool fcomb2 = otok && (h->fusion & MOE_FUSE_COMBINE2) && k == 2 && h->spec == nullptr &&
                       ((uintptr_t)a->y % 16) == 0;
+  // Cached mode, one GPU, tcgen05 gate: the dispatch (A4) rides inside the gate kernel (x read
+  // once for the gate GEMM and the row copies), so the chain stays on s0 with no fork / join
+  const bool cdisp = cached && tc1 && !gather && (h->fusion & MOE_FUSE_CDISP) && d % 64 == 0;
   h->fused_gather = gather;
   h->otok = otok;
   TcFusion fz;
@@ -589,7 +592,10 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   // side stream concurrently with the gate; the join is before the combine, the first step
   // that needs the gate weights.
   cudaStream_t sd = s0;
-  if (cached) {
+  if (cdisp) {
+    // (raw cached indices are copied into idx by the histogram kernel; the gate follows the
+    // routing scan on s0 and performs the dispatch)
+  } else if (cached) {
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, s0));
     CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
     sd = h->side;
@@ -617,7 +623,14 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
                                                      (cached && !tab) ? h->cached : nullptr));
   rb.gate_hist = 0;
   KL(h, 1, "route_scan", sd, launch_route_scan(rb.tile_hist, ntiles, n, h->ct, rb, sd));
-  if (!h->use_ep) {
+  if (cdisp) {
+    GateDispatch gd{&h->cts, X, (fcomb || fcomb2) ? a->y : nullptr, dout};
+    KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, cidx,
+                                                     rb, s0, &gd));
+    if (tab)  // cache_step
+      KL(h, T > 0, "cache_update", s0, launch_cache_update(h->ctab, h->ctab_num, k, h->cids, T,
+                                                           rb.fresh_idx, s0));
+  } else if (!h->use_ep) {
     KL(h, T > 0, "dispatch", sd, launch_dispatch(dt, rb.idx, a->x, T, k, n, d, 0, h->cts, rb,
                                                  gather ? nullptr : X, gather ? nullptr : rb.kept,
                                                  sd, 0, PeerBufs{}, PeerBufs{}, nullptr,
@@ -663,7 +676,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
   // Cached (S4.2): the gate is enqueued now -- after the routing / dispatch chain on the side
   // stream, before the expert GEMMs -- so it runs concurrently with the routing and dispatch
   // (enqueued after FWD1 it could only start once the persistent GEMM frees the SMs).
-  if (cached) {
+  if (cached && !cdisp) {
     if (h->use_tc)
       KL(h, T > 0, "gate_topk", s0, launch_gate_fwd_tc(a->x, a->w_gate, T, n, d, k, h->renorm, cidx, rb, s0));
     else
@@ -692,7 +705,8 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
                                      kept_local, rb.mtile_prefix, nl, h->ct, h->max_cap_local,
                                      sd, &nk, &h->prof, (uint32_t*)(ws + h->L.mask),
                                      (gather || fcomb || h->peer_ret || otok) ? &fz : nullptr,
-                                     (cached && (fcomb || fcomb2)) ? +wait_gate : nullptr, &join);
+                                     (cached && !cdisp && (fcomb || fcomb2)) ? +wait_gate : nullptr,
+                                     &join);
     h->launches += nk;
     if (st != MOE_OK) return fail(h, st, "tcgen05 forward failed");
   } else if (h->use_tf32) {
@@ -721,7 +735,7 @@ moe_status_t moe_forward(moe_handle_t h, const moe_fwd_args_t* a) {
     moe_status_t st = ep_from_experts(h->ep, h->plan, O, O_tok, h->ct, dout, (int)h->s, sd, &err);  // C3
     if (st != MOE_OK) return fail(h, st, err);
   }
-  if (cached) {  // join: everything after needs both the gate and the expert outputs
+  if (cached && !cdisp) {  // join: everything after needs both the gate and the expert outputs
     CUDA_TRY(h, cudaEventRecord(h->ev_join, sd));
     CUDA_TRY(h, cudaStreamWaitEvent(s0, h->ev_join, 0));
   }
@@ -1262,7 +1276,7 @@ moe_status_t moe_vcomm_destroy(void* comm) { return vcomm_destroy(comm); }
 moe_status_t moe_set_fusion(moe_handle_t h, int32_t flags) {
   if (!h) return MOE_ERR_INVALID_ARG;
   if (flags & ~(MOE_FUSE_GATHER | MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK |
-                MOE_FUSE_COMBINE2))
+                MOE_FUSE_COMBINE2 | MOE_FUSE_CDISP))
     return fail(h, MOE_ERR_INVALID_ARG, "unknown fusion flag");
   h->fusion = flags;
   return MOE_OK;

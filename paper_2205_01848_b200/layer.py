@@ -186,14 +186,15 @@ class MoELayer:
         self.generation += 1
 
     # -- N2 fusions ---------------------------------------------------------------------
-    FUSE_GATHER, FUSE_COMBINE, FUSE_DX, FUSE_OTOK, FUSE_COMBINE2 = 1, 2, 4, 8, 16
+    FUSE_GATHER, FUSE_COMBINE, FUSE_DX, FUSE_OTOK, FUSE_COMBINE2, FUSE_CDISP = 1, 2, 4, 8, 16, 32
 
     def set_fusion(self, flags: int):
         """moe_set_fusion: bitmask of FUSE_GATHER (x rows gathered by the expert GEMMs, no X
         buffer), FUSE_COMBINE (k = 1: y written by the second GEMM's epilogue) and FUSE_DX
         (k = 1: dx = dX + dl W_g written by the dX GEMM) and FUSE_OTOK (O stored in (token,
         choice) order for the combine and its backward), FUSE_COMBINE2 (k = 2: the combine in the
-        second GEMM's epilogue too, opt-in).  Default COMBINE | DX | OTOK."""
+        second GEMM's epilogue too, opt-in), FUSE_CDISP (cached assignments: the dispatch inside
+        the gate kernel).  Default COMBINE | DX | OTOK | CDISP."""
         L.check(self.lib.moe_set_fusion(self.h, int(flags)), self.h)
         self.generation += 1
 

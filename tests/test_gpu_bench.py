@@ -1,6 +1,5 @@
 """bench.py contract on the GPU: one JSON line with the keys the driver reads, at N = 1 and
-through the multi-process (torchrun) path with two ranks sharing cuda:0 (peer transport over
-CUDA IPC, gloo plumbing: MOE_BENCH_SHARE_GPU=1)."""
+through the multi-process (torchrun) path with two ranks, one GPU each (skipped on a one-GPU box)."""
 import json
 import os
 import subprocess
@@ -35,8 +34,17 @@ def test_bench_one_gpu_small():
     assert j["e2e"]["h2d_bytes_per_step"] > 0 and j["device_flags"] == 0
 
 
-def test_bench_two_ranks_share_gpu():
-    env = dict(os.environ, MOE_BENCH_SHARE_GPU="1")
+@pytest.mark.skipif(
+    __import__("torch").cuda.device_count() < 2 and os.environ.get("MOE_TEST_SHARED_GPU_PROCS") != "1",
+    reason="needs one GPU per rank: ranks whose kernels spin on each other's flags must not share "
+           "a GPU as separate processes (B200_PROFILING.md, Xid 109)")
+def test_bench_two_ranks():
+    """Two ranks, one GPU each (the driver's N = 2 launch).  With MOE_TEST_SHARED_GPU_PROCS=1 on
+    a one-GPU box both ranks share cuda:0 through the MOE_BENCH_SHARE_GPU hook (manual only)."""
+    import torch
+    env = dict(os.environ)
+    if torch.cuda.device_count() < 2:
+        env["MOE_BENCH_SHARE_GPU"] = "1"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2",
            "--config", "c1", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"]

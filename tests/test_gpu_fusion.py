@@ -283,3 +283,60 @@ def test_half_tiles_bitwise(n, k, d, T, alpha, fusion, monkeypatch):
             assert torch.all((a - b).abs() <= b.abs() * 2.0 ** -7 + 1e-30), "db1 beyond 1 ulp"
         else:
             _bitwise(g1[key], g0[key], key)
+
+
+@pytest.mark.parametrize("n,k,d,f,T,renorm,alpha,fusion", [
+    (8, 1, 256, 256, 999, 0, 1.0, 14),      # c5 kind: fused combine, ragged last tile
+    (16, 1, 128, 256, 1500, 0, 0.6, 14),    # heavy drops: y rows of dropped tokens zeroed
+    (8, 2, 256, 384, 777, 1, 1.0, 14),      # k = 2: two destination rows per x row
+    (130, 2, 128, 128, 700, 0, 0.8, 14),    # n > 128 (256-wide gate tile), n % 32 != 0
+    (8, 1, 64, 128, 257, 1, 1.25, 0),       # d = 64 (one k-block), no other fusion
+    (64, 1, 1024, 512, 4096, 0, 1.0, 14),   # c5 widths, several tiles per CTA
+])
+def test_cached_dispatch_in_gate_bitwise(n, k, d, f, T, renorm, alpha, fusion):
+    """FUSE_CDISP (flag 32): with cached assignments the gate kernel also computes the slots
+    and copies the kept x rows into X_buf from its TMA stages.  Every output -- y, all
+    gradients, the routing tables, the dispatched X rows and the zeroed pad rows -- is bitwise
+    equal to the unfused cached path (dispatch kernel on the side stream); outputs poisoned
+    first, two forwards in a row (the second over the first's buffers)."""
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer
+    g = {kk: v.cuda() for kk, v in make_layer(n, d, f, d, T, "bf16").items()}
+    dy = make_dy(T, d, "bf16").cuda()
+    gen = torch.Generator(device="cpu").manual_seed(11 + n + k)
+    cidx = torch.stack([torch.randperm(n, generator=gen)[:k] for _ in range(T)]).int().cuda()
+    layer = MoELayer(n, k, d, f, 0, T, "bf16", renorm, device="cuda")
+    layer.set_capacities(capacity_from_factors([alpha] * n, T, k))
+    layer.set_cached_assignment(cidx)
+
+    def tables():
+        r = layer.routing(T)
+        rows = r["x_buf"].clone()
+        return {kk: r[kk] for kk in ("idx", "fresh_idx", "slot_of", "w", "logits", "kept",
+                                     "counts", "token_of_slot")}, rows, r["base"]
+
+    def poison_x():  # every X_buf row NaN: the fused path must write the kept and pad rows
+        import ctypes as C
+        from paper_2205_01848_b200 import _lib as L
+        r = L.Routing()
+        L.check(layer.lib.moe_get_routing(layer.h, C.byref(r)), layer.h)
+        off = r.x_buf - layer.ws.data_ptr()
+        layer.ws[off:off + r.rows * d * 2].view(torch.bfloat16).fill_(float("nan"))
+
+    y0, g0 = _run(layer, g, dy, fusion, y_fill=float("nan"))
+    t0, x0, base = tables()
+    for it in range(2):
+        poison_x()
+        y1, g1 = _run(layer, g, dy, fusion | 32, y_fill=float("nan"))
+        t1, x1, _ = tables()
+        _bitwise(y1, y0, f"y (it {it})")
+        for key in g0:
+            _bitwise(g1[key], g0[key], f"{key} (it {it})")
+        for key in t0:
+            assert torch.equal(t1[key], t0[key]), f"{key} (it {it})"
+        # X rows of every expert region up to the zeroed pad end (roundup(kept, 64))
+        kept = t0["kept"].tolist()
+        for e in range(n):
+            r1 = base[e] + (kept[e] + 63) // 64 * 64
+            _bitwise(x1[base[e]:r1], x0[base[e]:r1], f"X rows of expert {e}")
+    assert int(t0["slot_of"].lt(0).sum()) > 0 or alpha >= 1.0

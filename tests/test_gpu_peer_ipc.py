@@ -1,15 +1,21 @@
 """Peer-memory transport across PROCESSES (N1): two ranks as two processes, windows opened
 from CUDA IPC handles (moe_peer_export / moe_peer_import) all-gathered over a gloo group.
-On the one-GPU test box both processes share cuda:0 (the kernels time-slice, so this checks
-the IPC plumbing and the cross-process flag protocol, not speed)."""
+Each process takes its own GPU.  With fewer GPUs than ranks the test is skipped: kernels that
+spin on flags another process writes must not share one GPU (B200_PROFILING.md: two such
+processes on one B200 raised Xid 109, a context-switch timeout); MOE_TEST_SHARED_GPU_PROCS=1
+forces the shared-GPU run for manual checks.  The multi-rank protocol is covered on one GPU by
+the in-process virtual-rank tests (test_gpu_ep.py) and on the CPU by test_ep_cpu.py."""
 import os
 import socket
 import subprocess
 import sys
 
 import pytest
+import torch
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(
+    torch.cuda.device_count() < 2 and os.environ.get("MOE_TEST_SHARED_GPU_PROCS") != "1",
+    reason="needs one GPU per process (spinning cross-process kernels must not share a GPU)")]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 

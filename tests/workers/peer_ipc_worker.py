@@ -1,4 +1,4 @@
-"""Worker of tests/test_gpu_peer_ipc.py: one process per rank (all on cuda:0 here), the
+"""Worker of tests/test_gpu_peer_ipc.py: one process per rank, each on its own GPU, the
 peer-memory transport connected through CUDA IPC handles all-gathered over a gloo group;
 each rank checks its shard of the outputs against the single-GPU layer bit for bit."""
 import os
@@ -15,7 +15,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 def main():
     dist.init_process_group("gloo")
     R, r = dist.get_world_size(), dist.get_rank()
-    torch.cuda.set_device(0)
+    dev = f"cuda:{r % torch.cuda.device_count()}"
+    torch.cuda.set_device(dev)
     from oracle import moe_oracle as O
     from paper_2205_01848_b200 import MoELayer
     from paper_2205_01848_b200.dist import peer_connect
@@ -29,7 +30,7 @@ def main():
     g = {kk: v.cuda() for kk, v in cpu.items()}
     dy = make_dy(Tg, d, dtype).cuda()
     caps = O.capacities_from_factors([1.0] * n, Tg, k)
-    L = MoELayer(n, k, d, f, 0, T, dtype, renorm, world_size=R, rank=r, device="cuda:0",
+    L = MoELayer(n, k, d, f, 0, T, dtype, renorm, world_size=R, rank=r, device=dev,
                  transport="peer")
     peer_connect(L)
     L.set_capacities(caps)
@@ -37,7 +38,7 @@ def main():
         y = L.forward(g["x"][r * T:(r + 1) * T], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
         gr = L.backward(dy[r * T:(r + 1) * T].contiguous())
     torch.cuda.synchronize()
-    ref = MoELayer(n, k, d, f, 0, Tg, dtype, renorm, device="cuda:0")
+    ref = MoELayer(n, k, d, f, 0, Tg, dtype, renorm, device=dev)
     ref.set_capacities(caps)
     y_ref = ref.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
     gr_ref = ref.backward(dy)
