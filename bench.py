@@ -66,15 +66,15 @@ def parse():
                     help="expert-parallel exchange: peer = device-initiated through peer "
                          "memory over NVLink (N1, default); nccl = grouped send/recv")
     ap.add_argument("--fusion", choices=["none", "combine", "dx", "otok", "legacy", "default",
-                                         "combine2", "all", "nocdisp"],
+                                         "combine2", "all", "cdisp"],
                     default="default",
                     help="N2 fusions (k = 1): combine = y written by the second expert GEMM's "
                          "epilogue; dx = dispatch backward inside the dX GEMM; default = combine+dx+otok; "
                          "otok = O stored in (token, choice) order; legacy = combine+dx; "
                          "combine2 = default + the k = 2 combine in the second GEMM's epilogue; "
                          "all = also gather x rows in the expert GEMMs (TMA gather4); "
-                         "default includes cdisp = cached mode: the dispatch inside the gate "
-                         "kernel (x read once); nocdisp = default without it")
+                         "cdisp = default + (cached mode) the dispatch inside the gate kernel "
+                         "(x read once)")
     a = ap.parse_args()
     if a.emulate_padded:
         os.environ["MOE_DBG_PAD_GEMM"] = "1"
@@ -312,8 +312,8 @@ def run_ours(args):
             layer.peer_attach([layer.peer_window()])
     layer.set_capacity_factors([alpha] * n, T * (ws if use_ep else 1))
     # N2 fusions (moe_set_fusion): gather x rows in the expert GEMMs, combine in FWD2 (k = 1)
-    fflags = {"none": 0, "combine": 2, "dx": 4, "otok": 8, "legacy": 6, "default": 46,
-              "combine2": 62, "all": 47, "nocdisp": 14}[args.fusion]
+    fflags = {"none": 0, "combine": 2, "dx": 4, "otok": 8, "legacy": 6, "default": 14,
+              "combine2": 30, "all": 15, "cdisp": 46}[args.fusion]
     tc1 = not use_ep and cfg.dtype == "bf16" and getattr(layer, "uses_tcgen05", False)
     gather = tc1 and bool(fflags & 1) and d % 128 == 0 and f % 128 == 0
     fcomb = tc1 and bool(fflags & 2) and k == 1 and do % 128 == 0

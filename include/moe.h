@@ -358,7 +358,7 @@ MOE_API moe_status_t moe_peer_import(moe_handle_t h, const void* handles /* host
 MOE_API moe_status_t moe_peer_connect_nccl(moe_handle_t h, void* nccl_comm);
 
 /* N2 fusions of the single-GPU tcgen05 path, a bitmask of moe_fusion_t;
-   default MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK | MOE_FUSE_CDISP (GATHER is opt-in: on B200 the TMA gather4 stream
+   default MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK (GATHER is opt-in: on B200 the TMA gather4 stream
    is slower than the dispatch copy it replaces).  GATHER and COMBINE give
    bitwise identical results (same products, same accumulation order); DX see below.
    MOE_FUSE_GATHER: the expert GEMMs that read x rows (H = relu(X W1^T + b1) and
@@ -398,7 +398,9 @@ MOE_API moe_status_t moe_peer_connect_nccl(moe_handle_t h, void* nccl_comm);
      128-token tile from the cached rows and copy every x k-block from the gate's TMA stage
      to the kept X_buf rows, so x is read once for the gate GEMM and the dispatch; the whole
      forward then stays on the caller's stream (no side-stream fork / join).  Bitwise equal
-     to the unfused cached path (same routing tables, same copied rows). */
+     to the unfused cached path (same routing tables, same copied rows).  Opt-in: measured
+     no faster than the default cached path, where the gate overlaps the routing chain on a
+     side stream. */
 typedef enum { MOE_FUSE_GATHER = 1, MOE_FUSE_COMBINE = 2, MOE_FUSE_DX = 4,
                MOE_FUSE_OTOK = 8, MOE_FUSE_COMBINE2 = 16, MOE_FUSE_CDISP = 32 } moe_fusion_t;
 MOE_API moe_status_t moe_set_fusion(moe_handle_t h, int32_t flags);

@@ -287,25 +287,48 @@ __global__ void __launch_bounds__(G_THREADS, 2)
         }
         asm volatile("bar.sync 2, 64;" ::: "memory");
         // each k-block: 128 rows x 128 bytes in the stage (128-byte swizzle: 16-byte chunk c of
-        // row r at c ^ (r & 7)); lane -> chunk lane % 8 of row 4 i + lane / 8 (a quarter warp
-        // reads one whole row: conflict-free), one full 128-byte line per row and destination
+        // row r at c ^ (r & 7)).  Thread (warp w, lane l) owns chunk l % 8 of the 16 rows
+        // 8 i + 4 (w - 2) + l / 8: all 16 chunks are read into registers with back-to-back
+        // shared loads (a quarter warp reads one whole row: conflict-free), the stage is
+        // released at once, and the registers then leave as 16-byte stores (one full 128-byte
+        // line per row and destination) while the next stage lands.
         const int ch = lane & 7;
+        const int rsub = (warp - 2) * 4 + (lane >> 3);
+        int rowr[TC_BM / 8];
+        if (KM == 1) {
+#pragma unroll
+          for (int i = 0; i < TC_BM / 8; ++i) {
+            const int lr = i * 8 + rsub;
+            rowr[i] = tile * TC_BM + lr < p.T ? s_row[lr] : -1;
+          }
+        }
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&b.full[stage], phase);
-          const uint8_t* sa = smem + stage * STAGE_BYTES;
-#pragma unroll 4
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          uint4 v[TC_BM / 8];
+#pragma unroll
           for (int i = 0; i < TC_BM / 8; ++i) {
-            const int lr = i * 8 + (warp - 2) * 4 + (lane >> 3);
-            if (tile * TC_BM + lr >= p.T) break;
-            const uint4 v = *reinterpret_cast<const uint4*>(sa + lr * 128 + ((ch ^ (lr & 7)) << 4));
-            for (int r = 0; r < k; ++r) {
-              const int row = s_row[lr * k + r];
-              if (row >= 0) st_v4(p.xbuf + (size_t)row * K + kb * TC_BK + ch * 8, v);
-            }
+            const int lr = i * 8 + rsub;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v[i].x), "=r"(v[i].y), "=r"(v[i].z), "=r"(v[i].w)
+                         : "r"(sa + lr * 128 + ((ch ^ (lr & 7)) << 4)));
           }
-          __syncwarp();
+          __syncwarp();  // (orders every lane's shared loads before the release below)
           if (lane == 0) mbar_arrive(&b.empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+#pragma unroll
+          for (int i = 0; i < TC_BM / 8; ++i) {
+            const int lr = i * 8 + rsub;
+            if (KM == 1) {
+              if (rowr[i] >= 0)
+                st_v4(p.xbuf + (size_t)rowr[i] * K + kb * TC_BK + ch * 8, v[i]);
+            } else if (tile * TC_BM + lr < p.T) {
+              for (int r = 0; r < k; ++r) {
+                const int row = s_row[lr * k + r];
+                if (row >= 0) st_v4(p.xbuf + (size_t)row * K + kb * TC_BK + ch * 8, v[i]);
+              }
+            }
+          }
         }
       }
     }

@@ -72,7 +72,7 @@ struct moe_ctx {
   int64_t launches = 0;
   int use_tc = 0;             // tcgen05 path for bf16 (env MOE_FORCE_SIMT=1 disables)
   int use_tf32 = 0;           // fp32: expert GEMMs on tcgen05 kind::tf32 (split operands), else SIMT
-  int fusion = MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK | MOE_FUSE_CDISP;  // N2 (moe_set_fusion; GATHER opt-in)
+  int fusion = MOE_FUSE_COMBINE | MOE_FUSE_DX | MOE_FUSE_OTOK;  // N2 (moe_set_fusion; GATHER, COMBINE2, CDISP opt-in)
   int fused_gather = 0;       // the last forward gathered x rows in the GEMMs (no X buffer)
   int peer_ret = 0;           // peer EP: O / dX rows returned by the GEMM epilogues (N1)
   int otok = 0;               // the last forward stored O in (token, choice) order (MOE_FUSE_OTOK)

@@ -194,7 +194,7 @@ class MoELayer:
         (k = 1: dx = dX + dl W_g written by the dX GEMM) and FUSE_OTOK (O stored in (token,
         choice) order for the combine and its backward), FUSE_COMBINE2 (k = 2: the combine in the
         second GEMM's epilogue too, opt-in), FUSE_CDISP (cached assignments: the dispatch inside
-        the gate kernel).  Default COMBINE | DX | OTOK | CDISP."""
+        the gate kernel, opt-in).  Default COMBINE | DX | OTOK."""
         L.check(self.lib.moe_set_fusion(self.h, int(flags)), self.h)
         self.generation += 1
 
