@@ -130,8 +130,16 @@ class ClockSampler:
 
     def start(self):
         if self.nvml is not None:
+            # the poller must get the GIL while the main thread enqueues the timed steps: a
+            # short switch interval, and the timed region starts only once it is sampling
+            self.switch = sys.getswitchinterval()
+            sys.setswitchinterval(0.0002)
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 1.0:
+                time.sleep(0.0005)
+            self.rows.clear()
             return
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -153,7 +161,14 @@ class ClockSampler:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((sm, rs))
+                pw = None
+                try:  # instantaneous board power (W); the plain power reading is a 1 s average
+                    fv = nv.nvmlDeviceGetFieldValues(h, [nv.NVML_FI_DEV_POWER_INSTANT])[0]
+                    if fv.nvmlReturn == 0:
+                        pw = fv.value.uiVal / 1000.0
+                except Exception:
+                    pw = None
+                self.rows.append((sm, rs, pw))
             except Exception:
                 pass
             time.sleep(0.002)
@@ -166,17 +181,25 @@ class ClockSampler:
         if self.nvml is not None:
             self.stop_flag = True
             self.t.join(timeout=2)
+            sys.setswitchinterval(self.switch)
             nv, h = self.nvml
             if not self.rows:
                 return None
             sm = sorted(r[0] for r in self.rows)
+            pw = sorted(r[2] for r in self.rows if r[2] is not None)
             try:
                 mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
             except Exception:
                 mx = None
-            reasons = sorted({nm for _, rs in self.rows for nm, bit in self.REASONS if rs & bit})
+            try:
+                lim = nv.nvmlDeviceGetEnforcedPowerLimit(h) / 1000.0
+            except Exception:
+                lim = None
+            reasons = sorted({nm for _, rs, _ in self.rows for nm, bit in self.REASONS if rs & bit})
             return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": reasons,
-                    "samples": len(sm), "source": "nvml, 2 ms"}
+                    "samples": len(sm), "source": "nvml, 2 ms",
+                    "power_w": ({"median": round(pw[len(pw) // 2], 1), "max": round(pw[-1], 1),
+                                 "limit": lim, "source": "nvml instant"} if pw else None)}
         if self.proc is None:
             return None
         self.proc.terminate()
