@@ -430,6 +430,13 @@ static int tc_half() {
   return e ? atoi(e) != 0 : 1;
 }
 
+// MOE_NO_KTRIM=1: the 2-CTA weight-gradient GEMMs issue every 16-deep MMA of their last
+// k-block, pad tokens included (A/B comparisons; read per call).
+static int tc_no_ktrim() {
+  const char* e = getenv("MOE_NO_KTRIM");
+  return e ? atoi(e) != 0 : 0;
+}
+
 static int tc_sched() {  // MOE_TC_SCHED: 2-CTA tile schedule (see TcParams::sched)
   static int v = -1;
   if (v < 0) {
@@ -609,6 +616,7 @@ static moe_status_t wgrad(const void* Abuf, int M, const void* Bbuf, int N, int6
   p.sched = tc_sched();
   p.pf_kb = tc_pf();
   p.dbg = tc_dbg();
+  p.no_ktrim = tc_no_ktrim();
   if (use_2cta(N, TC_WGRAD)) {
     CUtensorMap mc;
     TC_TRY(make_store_map(&mc, Out, N, (uint64_t)n_local * M));

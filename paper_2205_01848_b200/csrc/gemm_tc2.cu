@@ -360,13 +360,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
         const uint32_t idesc = half_tile(e, mt) ? IDESC_H : IDESC;
+        // token-K GEMMs (weight gradients): the last k-block issues only the 16-deep MMAs
+        // that hold kept tokens (rows past kept are zero pads; skipping them adds nothing)
+        const int klast = Tr::kgroup && !p.no_ktrim ? (p.kept[e] - (nk - 1) * TC_BK + 15) / 16
+                                                    : TC_BK / 16;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
+          const int nsub = kb == nk - 1 ? klast : TC_BK / 16;
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k) {
+            if (k >= nsub) break;
             uint64_t da = Tr::a_mn ? umma_desc(sa + k * 2048, 8192, 1024)
                                    : umma_desc(sa + k * 32, 16, 1024);
             uint64_t db = Tr::b_mn ? umma_desc(sb + k * 2048, 8192, 1024)

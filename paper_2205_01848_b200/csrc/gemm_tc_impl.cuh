@@ -60,6 +60,8 @@ struct TcParams {
   CapTable ct;                  // base rows of each local expert region
   int nowait;                   // inputs complete once the predecessor started: no PDL wait
   int half_tiles;               // 2-CTA M-grouped: remainder m-tiles of <= 128 rows run as M = 128
+  int no_ktrim;                 // 2-CTA WGRAD: 1 = the last k-block issues all four 16-deep MMAs
+                                // (A/B switch MOE_NO_KTRIM=1; default: only those holding tokens)
   const void* hsrc;             // fp32 DGRAD_A: H for the ReLU' test when dA is not written
                                 // over it (null = C itself holds H)
 };

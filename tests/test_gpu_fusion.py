@@ -340,3 +340,37 @@ def test_cached_dispatch_in_gate_bitwise(n, k, d, f, T, renorm, alpha, fusion):
             r1 = base[e] + (kept[e] + 63) // 64 * 64
             _bitwise(x1[base[e]:r1], x0[base[e]:r1], f"X rows of expert {e}")
     assert int(t0["slot_of"].lt(0).sum()) > 0 or alpha >= 1.0
+
+
+@pytest.mark.parametrize("n,k,d,T,alpha,fusion", [
+    (8, 1, 512, 2048, 4.0, 14), (16, 2, 256, 1500, 3.0, 0), (8, 1, 256, 2500, 1.0, 15),
+    (64, 1, 1024, 8192, 1.0, 14)])
+def test_wgrad_k_tail_trim_bitwise(n, k, d, T, alpha, fusion, monkeypatch):
+    """The weight-gradient GEMMs issue only the 16-deep MMAs of their last token k-block that
+    hold kept tokens (default) against all four (MOE_NO_KTRIM=1): the skipped MMAs would add
+    products of zero pad rows, so every output is bitwise equal -- kept counts of every
+    residue mod 64 occur (no-drop capacities), with gradient accumulation on the second
+    iteration and the gather fusion (flag 1) in one case."""
+    from paper_2205_01848_b200 import MoELayer, capacity_from_factors
+    from synth import make_dy, make_layer
+    g = {kk: v.cuda() for kk, v in make_layer(n, d, 4 * d, d, T, "bf16").items()}
+    dy = make_dy(T, d, "bf16").cuda()
+    outs = []
+    for trim in ("0", "1"):
+        monkeypatch.setenv("MOE_NO_KTRIM", trim)
+        layer = MoELayer(n, k, d, 4 * d, 0, T, "bf16", 0, device="cuda")
+        layer.set_capacities(capacity_from_factors([alpha] * n, T, k))
+        layer.set_fusion(fusion)
+        grads = None
+        for it in range(2):
+            y = layer.forward(g["x"], g["w_gate"], g["w1"], g["b1"], g["w2"], g["b2"])
+            grads = layer.backward(dy, grads=grads, accumulate=it > 0)
+        torch.cuda.synchronize()
+        kept = layer.routing(T)["kept"]
+        outs.append((y.clone(), {kk: v.clone() for kk, v in grads.items()}))
+        layer.close()
+    assert bool(((kept % 16) != 0).any())
+    (y1, g1), (y0, g0) = outs
+    _bitwise(y1, y0, "y")
+    for key in g0:
+        _bitwise(g1[key], g0[key], key)
