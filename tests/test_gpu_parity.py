@@ -266,3 +266,20 @@ def test_confident_router_dl_precision(k, renorm):
     dl = layer.routing(T)["dl"].cpu().double().numpy()
     assert rel(dl, gr["dl"]) <= 1e-5
     assert rel(to_numpy64(grads["dw_gate"]), gr["dw_gate"]) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_maximum_experts_and_topk(dtype):
+    """The largest configuration the library accepts (n = 256 experts, the capacity table's
+    size; k = 8, MOE_MAX_K) against the oracle, with drops; one expert more or one choice
+    more is refused at moe_init."""
+    n, k, T, d, f = 256, 8, 600, 64, 64
+    caps = _caps(n, T, k, 1.0)
+    layer, gpu, st, gr, ol = run_pair(n, k, d, f, T, dtype, caps, 1)
+    assert st.routing.drops > 0
+    assert_routing_exact(gpu, st, k)
+    assert_values(gpu, st, gr, ol, dtype)
+    from paper_2205_01848_b200 import MoELayer
+    for nn, kk in ((257, 1), (16, 9)):
+        with pytest.raises(Exception):
+            MoELayer(nn, kk, d, f, 0, T, dtype, 1, device="cuda")
