@@ -22,8 +22,8 @@
 //   DGRAD_X   dX = dA W1_e                                 K        MN       kept_e
 //   WGRAD     dW = A^T B over kept_e tokens (+ fused db)   MN       MN       d_out / f
 //
-// Roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator, warp 3
-// bias-gradient warp (WGRAD), warps 4..7 epilogue (TMEM lane quarters), warps 8..11 split the
+// Roles (512 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator, warp 3
+// bias-gradient warp (WGRAD), warps 4..7 epilogue (TMEM lane quarters), warps 8..15 split the
 // landed fp32 tiles (a0 in place, a1 in its own buffer) and signal the MMA warp.  Stage =
 // {A0, A1 (128 x 32), B0, B1 (BN x 32)} fp32; K-major operands use the 128-byte swizzle,
 // MN-major ones the 128-byte swizzle with 32-byte atoms (the only MN-major tf32 layout); the
@@ -46,9 +46,9 @@ namespace moe {
 namespace {
 
 constexpr int TF_BK = 32;            // fp32 elements per 128-byte smem row
-constexpr int TF_THREADS = 384;
-constexpr int TF_CONV_WARP0 = 8;     // warps 8..11 split the stages
-constexpr int TF_CONV_THREADS = 128;
+constexpr int TF_THREADS = 512;
+constexpr int TF_CONV_WARP0 = 8;     // warps 8..15 split the stages
+constexpr int TF_CONV_THREADS = 256;
 
 // kind::tf32 instruction descriptor: tf32 x tf32 -> fp32, M = 128, N = n
 __host__ __device__ constexpr uint32_t make_idesc_tf32(int n, int a_mn, int b_mn) {
@@ -88,18 +88,34 @@ __device__ __forceinline__ float tf32_rna(float a) {
   return __uint_as_float(r);
 }
 
-// split n16 16-byte vectors starting at `raw`: a0 in place, a1 at raw + off
+// split n16 16-byte vectors starting at `raw`: a0 in place, a1 at raw + off.  Shared-window
+// addresses (ld / st.shared, not generic), every load of the thread's vectors issued first.
 __device__ __forceinline__ void split_vecs(uint8_t* raw, int off, int n16, int tid) {
-  for (int i = tid; i < n16; i += TF_CONV_THREADS) {
-    float4* p = reinterpret_cast<float4*>(raw) + i;
-    const float4 a = *p;
-    float4 h, m;
-    h.x = tf32_rna(a.x); m.x = tf32_rna(a.x - h.x);
-    h.y = tf32_rna(a.y); m.y = tf32_rna(a.y - h.y);
-    h.z = tf32_rna(a.z); m.z = tf32_rna(a.z - h.z);
-    h.w = tf32_rna(a.w); m.w = tf32_rna(a.w - h.w);
-    *p = h;
-    *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(p) + off) = m;
+  constexpr int PER = 4;  // vectors per thread per batch
+  const uint32_t base = smem_u32(raw);
+  for (int i0 = tid; i0 < n16; i0 += PER * TF_CONV_THREADS) {
+    float4 a[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (i0 + j * TF_CONV_THREADS >= n16) break;  // (uniform: n16 is a multiple of 256)
+      const uint32_t ad = base + (uint32_t)(i0 + j * TF_CONV_THREADS) * 16u;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(a[j].x), "=f"(a[j].y), "=f"(a[j].z), "=f"(a[j].w) : "r"(ad));
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (i0 + j * TF_CONV_THREADS >= n16) break;
+      float4 h, m;
+      h.x = tf32_rna(a[j].x); m.x = tf32_rna(a[j].x - h.x);
+      h.y = tf32_rna(a[j].y); m.y = tf32_rna(a[j].y - h.y);
+      h.z = tf32_rna(a[j].z); m.z = tf32_rna(a[j].z - h.z);
+      h.w = tf32_rna(a[j].w); m.w = tf32_rna(a[j].w - h.w);
+      const uint32_t ad = base + (uint32_t)(i0 + j * TF_CONV_THREADS) * 16u;
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ad), "f"(h.x), "f"(h.y),
+                   "f"(h.z), "f"(h.w) : "memory");
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ad + (uint32_t)off),
+                   "f"(m.x), "f"(m.y), "f"(m.z), "f"(m.w) : "memory");
+    }
   }
 }
 
