@@ -971,7 +971,11 @@ cudaError_t launch_gate_fwd_tc(const void* x, const void* wg, int T, int n, int 
   }
   const int MT = (T + 127) / 128;
   // two CTAs per SM (4-stage rings): twice the epilogue warps, which bound this kernel
-  const int grid = MT < 2 * g_sms ? MT : 2 * g_sms;
+  // as many tiles on every CTA: the fewest CTAs (up to two per SM) that keep the per-CTA tile
+  // count (c3: 512 tiles on 256 CTAs x 2 rather than 296 CTAs with 1 or 2; measured 1.5 us)
+  int grid = MT < 2 * g_sms ? MT : 2 * g_sms;
+  const int per_cta = (MT + grid - 1) / grid;
+  grid = (MT + per_cta - 1) / per_cta;
 #define GF(BN, ST)                                                                       \
   {                                                                                      \
     auto kf = k == 1 ? gate_fwd_tc_kernel<BN, ST, 1>                                     \
